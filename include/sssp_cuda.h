@@ -1,0 +1,146 @@
+/*
+ * sssp_cuda.h -- C ABI of the B200-native matrix-scan Dijkstra.
+ *
+ * Drop-in boundary for the reference's solve path:
+ *   reference  sssp::dijkstra_serial(const Graph&, VertexId)      serial.hpp:65-68
+ *              sssp::dijkstra_serial(g, s, OpCounters&, visit*)  serial.hpp:26-28
+ *              sssp::dijkstra_partitioned(g, s, p, mode)         partitioned.hpp:184-186
+ *   replaced by  sssp_graph_create + sssp_solve (+ sssp_graph_destroy); the C++
+ *   wrapper include/sssp/cuda.hpp restores the reference's exact signature and
+ *   return type (ShortestPathResult, result.hpp:13-19).
+ *
+ * Plain pointers and sizes only; no exceptions cross this boundary.  The
+ * input is the reference's own Graph::adj layout: row-major n*n uint64
+ * weights, UINT64_MAX = no edge (weight.hpp:13, graph.hpp:30-45).  Outputs
+ * use the reference encoding: dist UINT64_MAX = unreachable, pred
+ * UINT64_MAX = kNoVertex (weight.hpp:13, :21).
+ *
+ * Threading: a handle is not safe for concurrent solves (its exchange
+ * buffers and scratch are per handle); distinct handles are independent.
+ * Every solve is synchronous unless the *_enqueue entry points are used.
+ * There is no CPU fallback: without a usable CUDA device every entry point
+ * returns SSSP_ERR_CUDA.
+ */
+#ifndef SSSP_CUDA_H
+#define SSSP_CUDA_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SSSP_ABI_VERSION 1
+#define SSSP_IPC_HANDLE_BYTES 64 /* sizeof(cudaIpcMemHandle_t) */
+#define SSSP_MAX_SHARDS 8
+
+typedef enum {
+  SSSP_OK = 0,
+  SSSP_ERR_BAD_SOURCE = 1,   /* source >= n: std::invalid_argument at serial.hpp:30 */
+  SSSP_ERR_BAD_ARG = 2,      /* p < 1 (partitioned.hpp:187), n == 0, bad shard ids ... */
+  SSSP_ERR_WEIGHT_RANGE = 3, /* a weight/distance this device encoding cannot hold */
+  SSSP_ERR_OOM = 4,          /* device or pinned-host allocation failed */
+  SSSP_ERR_CUDA = 5,         /* CUDA runtime error (no device, launch failure ...) */
+  SSSP_ERR_NO_PEER = 6,      /* peer access / IPC import failed between shards */
+  SSSP_ERR_TIMEOUT = 7,      /* the persistent kernel's exchange watchdog fired */
+  SSSP_ERR_UNSUPPORTED = 8   /* configuration not supported on this device */
+} sssp_status;
+
+/* Election/relaxation engine of a solve. */
+typedef enum {
+  SSSP_ENGINE_AUTO = 0, /* the n-round persistent scan kernel (north-star path) */
+  SSSP_ENGINE_SCAN = 1  /* same, explicitly */
+} sssp_engine;
+
+typedef struct {
+  int engine;             /* sssp_engine */
+  uint32_t ctas_per_shard;/* 0 = auto (<= SM count); CTAs of one solve on one shard */
+  uint32_t flags;         /* bit0: runner-up row prefetch, bit1: owner L2 row prefetch;
+                             SSSP_FLAGS_DEFAULT when the options pointer is NULL */
+  uint32_t max_batch;     /* concurrent solves a batch launch may run (0 = auto) */
+  uint64_t timeout_ms;    /* exchange watchdog (0 = 60000) */
+  int record_visit_order; /* 1: keep the elected vertex of every round */
+} sssp_options;
+
+#define SSSP_FLAGS_DEFAULT 3u
+
+/* Per-solve statistics; phases mirror the reference's data-parallel timing
+ * scope {transfer_in, rounds, transfer_out} (bench.hpp:50-51). */
+typedef struct {
+  double transfer_in_s;   /* graph upload (narrow + permute + H2D) of the handle */
+  double rounds_s;        /* kernel time, CUDA events on the launch stream */
+  double transfer_out_s;  /* D2H of dist/pred */
+  uint64_t iterations;    /* elections executed (= vertices reached) */
+  uint64_t relax_checks;  /* iterations * columns scanned (OpCounters analogue) */
+  uint64_t mispredicts;   /* rounds whose row was not prefetched */
+  uint64_t matrix_bytes;  /* device bytes of the stored matrix (all local shards) */
+  uint32_t weight_bytes;  /* device weight encoding: 1, 2 or 4 bytes */
+  uint32_t ctas;          /* CTAs per solve per shard */
+  uint32_t shards;        /* P */
+  uint32_t packed_key;    /* 1 if the single-redux packed local key is in use */
+} sssp_solve_stats;
+
+typedef struct sssp_graph sssp_graph;
+
+const char* sssp_status_string(int status);
+const char* sssp_last_error(void); /* thread-local detail of the last failure */
+int sssp_abi_version(void);
+int sssp_device_count(int* count);
+
+/* Single-GPU (devices == NULL or ndev == 1) or single-process multi-GPU
+ * column-partitioned graph: shard k of P = ndev owns columns
+ * [k*loc_n, (k+1)*loc_n) with loc_n = pad_vertex_count(n, P)/P
+ * (partition.hpp:25-41).  Repeating a device id runs several shards on one
+ * GPU (the "P logical shards" simulation of the multi-GPU protocol).
+ * `directed` is recorded only; the matrix is taken as given. */
+int sssp_graph_create(const uint64_t* adj, uint64_t n, int directed, const int* devices,
+                      int ndev, const sssp_options* opt, sssp_graph** out);
+
+/* One process per GPU: this process owns shard `rank` of `world`.
+ * `block` holds rows 0..n-1 of the shard's real columns
+ * [rank*loc_n, min(n, (rank+1)*loc_n)) with leading dimension `ld` (pass the
+ * full matrix with ld = n and block = adj + rank*loc_n, or a column block).
+ * `max_weight` = largest finite weight of the WHOLE graph (0 = derive it from
+ * the block, exact only when world == 1).  After every rank has called
+ * sssp_shard_export, pass the world * SSSP_IPC_HANDLE_BYTES handles gathered
+ * in rank order to sssp_shard_connect. */
+int sssp_shard_create(const uint64_t* block, uint64_t ld, uint64_t n, uint32_t world,
+                      uint32_t rank, uint64_t max_weight, int device, const sssp_options* opt,
+                      sssp_graph** out);
+int sssp_shard_export(sssp_graph* g, void* handle_out);
+int sssp_shard_connect(sssp_graph* g, const void* handles);
+/* Columns [*col_begin, *col_begin + *col_count) are this process's slice. */
+int sssp_shard_range(const sssp_graph* g, uint64_t* col_begin, uint64_t* col_count);
+
+int sssp_graph_destroy(sssp_graph* g);
+int sssp_graph_info(const sssp_graph* g, sssp_solve_stats* st);
+
+/* Synchronous solve.  dist_out/pred_out: n entries (single process), or the
+ * shard's col_count entries in shard mode.  visit_order_out (optional, n
+ * entries, filled up to stats.iterations; needs record_visit_order). */
+int sssp_solve(sssp_graph* g, uint64_t source, uint64_t* dist_out, uint64_t* pred_out,
+               uint64_t* visit_order_out, sssp_solve_stats* st);
+
+/* k independent sources; outputs are k consecutive n-entry rows. */
+int sssp_solve_batch(sssp_graph* g, const uint64_t* sources, uint32_t k, uint64_t* dist_out,
+                     uint64_t* pred_out, sssp_solve_stats* st);
+
+/* Asynchronous form for device-side timing: enqueue k solves on the handle's
+ * stream (results stay on the device), then sssp_finish waits and checks the
+ * watchdog.  sssp_stream returns the cudaStream_t of shard `local` as a
+ * pointer so a caller can record its own CUDA events around the launches. */
+int sssp_enqueue(sssp_graph* g, const uint64_t* sources, uint32_t k);
+int sssp_finish(sssp_graph* g, sssp_solve_stats* st);
+void* sssp_stream(sssp_graph* g, int local);
+
+/* t_sync_min microbenchmark (the roofline's sync term): runs
+ * `rounds` exchange rounds with the solve's launch shape and exchange code
+ * but no relaxation; *seconds_per_round = max over shards of elapsed/rounds
+ * (device %globaltimer).  Collective in shard mode: every rank must call. */
+int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* SSSP_CUDA_H */

@@ -1,0 +1,44 @@
+/*
+ * sssp_graph_gen.h -- host-side graph builders exported by libsssp_cuda.so.
+ *
+ * These produce the reference's Graph::adj layout (row-major uint64, INF =
+ * UINT64_MAX, diagonal 0; graph.hpp:30-45) for the benchmark and test
+ * inputs, restating the reference generators (generate.hpp:15-83) and
+ * graph_from_edges (graph.hpp:73-88).  Every builder can emit a column
+ * block [col_begin, col_begin+col_count) with leading dimension ld, so a
+ * process that owns one shard (partition.hpp:31-41) never materialises the
+ * whole matrix.  Pass col_begin = 0, col_count = ld = n for the full matrix.
+ */
+#ifndef SSSP_GRAPH_GEN_H
+#define SSSP_GRAPH_GEN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* graph_from_edges(generate_dense(n, seed), directed): complete graph,
+ * weights 1 + uniform_below(100) drawn for u < v in row-major order. */
+int sssp_gen_dense(uint64_t n, uint64_t seed, int directed, uint64_t col_begin,
+                   uint64_t col_count, uint64_t ld, uint64_t* out);
+
+/* graph_from_edges(generate_sparse(n, seed), directed): 3n distinct edges. */
+int sssp_gen_sparse(uint64_t n, uint64_t seed, int directed, uint64_t col_begin,
+                    uint64_t col_count, uint64_t ld, uint64_t* out);
+
+/* Bernoulli graph of BASELINE configs 2 and 4: pairs in
+ * row-major order (u < v undirected, u != v directed), kept iff
+ * (rng() >> 11) < p_q53 (p = p_q53 / 2^53), weight 1 + uniform_below(100). */
+int sssp_gen_bernoulli(uint64_t n, uint64_t p_q53, uint64_t seed, int directed,
+                       uint64_t col_begin, uint64_t col_count, uint64_t ld, uint64_t* out);
+
+/* graph_from_edges over m (u, v, w) triples; returns SSSP_ERR_BAD_ARG on
+ * the inputs the reference rejects (endpoint >= n, self-loop, w > 2^32-1). */
+int sssp_graph_from_edges(uint64_t n, const uint64_t* edges, uint64_t m, int directed,
+                          uint64_t col_begin, uint64_t col_count, uint64_t ld, uint64_t* out);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

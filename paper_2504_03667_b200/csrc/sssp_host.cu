@@ -1,0 +1,939 @@
+// sssp_host.cu -- the C-ABI host side (include/sssp_cuda.h).
+//
+// Owns: choosing the device encoding of the reference's uint64 matrix
+// (weight.hpp:9-26), the column partition (partition.hpp:25-41), the
+// narrow -> H2D -> permute upload pipeline, the exchange buffers of the
+// persistent kernel (scan_kernel.cuh), and the launch / finish / D2H of a
+// solve.  No CPU solve path exists: every error surfaces as a status code.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/sssp_cuda.h"
+#include "scan_kernel.cuh"
+
+using namespace sssp_b200;
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const std::string& msg) {
+  g_err = msg;
+  return code;
+}
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      return fail(e_ == cudaErrorMemoryAllocation ? SSSP_ERR_OOM : SSSP_ERR_CUDA,    \
+                  std::string(#call) + ": " + cudaGetErrorString(e_));               \
+    }                                                                                \
+  } while (0)
+
+double now_s() {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch())
+      .count();
+}
+
+uint32_t bitlen(uint64_t x) {
+  uint32_t b = 0;
+  while (x) {
+    ++b;
+    x >>= 1;
+  }
+  return b;
+}
+
+// partition.hpp:25-29
+uint64_t pad_vertex_count(uint64_t n, uint64_t p) {
+  if (p > n) return p;
+  return n + (p - n % p) % p;
+}
+
+using KernelFn = void (*)(const ScanParams);
+
+template <typename W, int EPL>
+KernelFn pick_np(int np) {
+  switch (np) {
+    case 2: return scan_dijkstra_kernel<W, EPL, 2>;
+    case 4: return scan_dijkstra_kernel<W, EPL, 4>;
+    case 16: return scan_dijkstra_kernel<W, EPL, 16>;
+  }
+  return nullptr;
+}
+
+template <typename W>
+KernelFn pick_epl(int epl, int np) {
+  switch (epl) {
+    case 4: return pick_np<W, 4>(np);
+    case 8: return pick_np<W, 8>(np);
+    case 16: return pick_np<W, 16>(np);
+    case 32: return pick_np<W, 32>(np);
+    case 64: return pick_np<W, 64>(np);
+  }
+  return nullptr;
+}
+
+KernelFn pick_kernel(int wbytes, int epl, int np) {
+  switch (wbytes) {
+    case 1: return pick_epl<uint8_t>(epl, np);
+    case 2: return pick_epl<uint16_t>(epl, np);
+    case 4: return pick_epl<uint32_t>(epl, np);
+  }
+  return nullptr;
+}
+
+// Rearranges a chunk of staged rows (natural column order) into the
+// cyclic-by-CTA layout of scan_kernel.cuh.  Padding columns get INF.
+template <typename W>
+__global__ void permute_rows_kernel(const W* __restrict__ stage, uint32_t cols,
+                                    W* __restrict__ dst, uint64_t row_stride, uint64_t row0,
+                                    uint32_t rows, uint32_t G, uint32_t L) {
+  const uint64_t total = (uint64_t)rows * row_stride;
+  for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t r = idx / row_stride;
+    const uint32_t q = (uint32_t)(idx - r * row_stride);
+    const uint32_t c = q / L, s = q - c * L;
+    const uint32_t vl = s * G + c;
+    dst[(row0 + r) * row_stride + q] =
+        vl < cols ? stage[r * cols + vl] : (W)WInf<W>::v;
+  }
+}
+
+template <typename F>
+void parallel_for(uint64_t begin, uint64_t end, unsigned nthreads, F&& f) {
+  if (end <= begin) return;
+  nthreads = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(nthreads, end - begin));
+  if (nthreads == 1) {
+    f(begin, end, 0u);
+    return;
+  }
+  std::vector<std::thread> ts;
+  const uint64_t span = end - begin;
+  for (unsigned t = 0; t < nthreads; ++t) {
+    const uint64_t a = begin + span * t / nthreads, b = begin + span * (t + 1) / nthreads;
+    ts.emplace_back([&f, a, b, t] { f(a, b, t); });
+  }
+  for (auto& th : ts) th.join();
+}
+
+unsigned host_threads() {
+  const unsigned h = std::thread::hardware_concurrency();
+  return std::max(1u, std::min(h ? h : 1u, 32u));
+}
+
+}  // namespace
+
+struct Shard {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev0 = nullptr, ev1 = nullptr;
+  void* d_adj = nullptr;
+  uint64_t row_stride = 0;  // G*L
+  uint32_t G = 0, EPL = 0, L = 0, NP = 0;
+  uint32_t k = 0;           // shard index
+  uint64_t col_base = 0, loc_n = 0, cols = 0;  // cols = real columns held
+  uint64_t* d_slots = nullptr;
+  uint64_t* d_dist = nullptr;
+  uint64_t* d_pred = nullptr;
+  uint64_t* d_info = nullptr;
+  uint32_t* d_sources = nullptr;
+  uint32_t* d_visit = nullptr;
+  uint32_t* h_sources = nullptr;  // pinned
+  uint64_t* h_info = nullptr;     // pinned
+  uint64_t* peer[kMaxShards] = {};
+  bool peer_ipc[kMaxShards] = {};
+  KernelFn fn = nullptr;
+};
+
+struct sssp_graph {
+  uint64_t n = 0;
+  int directed = 0;
+  uint32_t P = 1;
+  bool multiproc = false;
+  bool connected = false;
+  std::vector<Shard> sh;
+  sssp_options opt{};
+  uint32_t wbytes = 0;
+  uint64_t max_w = 0, min_w = ~0ull;
+  uint32_t vbits = 0, sbits = 0, packed = 0;
+  uint32_t max_batch = 1;
+  uint64_t slot_stride = 0, bstride = 0;
+  uint64_t exch_base = 0;
+  double transfer_in_s = 0;
+  uint32_t pending = 0;  // solves enqueued and not yet finished
+  uint64_t matrix_bytes = 0;
+};
+
+namespace {
+
+sssp_options default_options(const sssp_options* o) {
+  sssp_options d{};
+  if (o) d = *o;
+  else d.flags = SSSP_FLAGS_DEFAULT;
+  if (d.timeout_ms == 0) d.timeout_ms = 60000;
+  return d;
+}
+
+// Chooses EPL/G for a shard of loc_n columns with at most gmax CTAs.
+int plan_layout(Shard& s, uint64_t loc_n, uint32_t gmax) {
+  static const uint32_t epls[] = {4, 8, 16, 32, 64};
+  for (uint32_t epl : epls) {
+    const uint64_t L = 32ull * epl;
+    const uint64_t G = (loc_n + L - 1) / L;
+    if (G <= gmax || epl == 64) {
+      if (G > gmax) return fail(SSSP_ERR_UNSUPPORTED, "graph too large for one shard");
+      s.EPL = epl;
+      s.L = (uint32_t)L;
+      s.G = (uint32_t)std::max<uint64_t>(1, G);
+      s.row_stride = (uint64_t)s.G * s.L;
+      return SSSP_OK;
+    }
+  }
+  return SSSP_ERR_UNSUPPORTED;
+}
+
+struct ScanResult {
+  std::atomic<bool> overflow{false};
+  uint64_t max_w = 0, min_w = ~0ull;
+};
+
+// Narrows the caller's uint64 block (rows 0..n-1, `cols` columns, leading
+// dimension ld, global column offset col_base) to W and uploads it in the
+// permuted layout.  Sets res.overflow if some finite weight exceeds W's
+// finite range (the caller then retries with a wider W).
+template <typename W>
+int upload_block(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, ScanResult& res) {
+  const uint64_t WINF64 = WInf<W>::v;
+  const uint64_t fmax = WINF64 - 1;  // largest finite weight W can carry
+  const uint64_t cols = s.cols;
+  const uint64_t row_in_bytes = std::max<uint64_t>(1, cols) * 8;
+  const uint64_t R = std::max<uint64_t>(1, std::min<uint64_t>(n, (64ull << 20) / row_in_bytes));
+  const uint64_t stage_elems = R * std::max<uint64_t>(1, cols);
+  W* pin[2] = {nullptr, nullptr};
+  W* dst[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  bool used[2] = {false, false};
+  int rc = SSSP_OK;
+  const unsigned nt = host_threads();
+  std::vector<uint64_t> tmax(nt, 0), tmin(nt, ~0ull);
+  std::vector<char> tover(nt, 0);
+
+  auto cleanup = [&]() {
+    cudaStreamSynchronize(s.stream);
+    for (int b = 0; b < 2; ++b) {
+      if (pin[b]) cudaFreeHost(pin[b]);
+      if (dst[b]) cudaFree(dst[b]);
+      if (done[b]) cudaEventDestroy(done[b]);
+    }
+  };
+  for (int b = 0; b < 2; ++b) {
+    if (cudaHostAlloc(&pin[b], stage_elems * sizeof(W), cudaHostAllocDefault) != cudaSuccess ||
+        cudaMalloc(&dst[b], stage_elems * sizeof(W)) != cudaSuccess ||
+        cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming) != cudaSuccess) {
+      cleanup();
+      return fail(SSSP_ERR_OOM, "upload staging allocation failed");
+    }
+  }
+  uint64_t chunk = 0;
+  for (uint64_t r0 = 0; r0 < n && rc == SSSP_OK; r0 += R, ++chunk) {
+    const int b = (int)(chunk & 1);
+    const uint64_t rows = std::min<uint64_t>(R, n - r0);
+    if (used[b]) cudaEventSynchronize(done[b]);
+    W* out = pin[b];
+    parallel_for(r0, r0 + rows, nt, [&](uint64_t a, uint64_t e, unsigned t) {
+      uint64_t mx = tmax[t], mn = tmin[t];
+      bool over = false;
+      for (uint64_t r = a; r < e; ++r) {
+        const uint64_t* row = src + r * ld;
+        W* o = out + (r - r0) * cols;
+        const uint64_t diag = (r >= s.col_base && r < s.col_base + cols) ? r - s.col_base : ~0ull;
+        for (uint64_t j = 0; j < cols; ++j) {
+          const uint64_t x = row[j];
+          const bool inf = x == ~0ull;
+          over |= !inf && x > fmax;
+          o[j] = inf ? (W)WINF64 : (W)x;
+          if (!inf) {
+            mx = x > mx ? x : mx;
+            if (j != diag) mn = x < mn ? x : mn;
+          }
+        }
+      }
+      tmax[t] = mx;
+      tmin[t] = mn;
+      if (over) tover[t] = 1;
+    });
+    for (unsigned t = 0; t < nt; ++t)
+      if (tover[t]) res.overflow = true;
+    if (res.overflow) break;
+    if (cols) {
+      cudaError_t e = cudaMemcpyAsync(dst[b], out, rows * cols * sizeof(W),
+                                      cudaMemcpyHostToDevice, s.stream);
+      if (e != cudaSuccess) {
+        rc = fail(SSSP_ERR_CUDA, std::string("H2D: ") + cudaGetErrorString(e));
+        break;
+      }
+    }
+    const uint64_t total = rows * s.row_stride;
+    const unsigned blocks = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+    permute_rows_kernel<W><<<blocks, 256, 0, s.stream>>>(dst[b], (uint32_t)cols,
+                                                        static_cast<W*>(s.d_adj), s.row_stride,
+                                                        r0, (uint32_t)rows, s.G, s.L);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+      rc = fail(SSSP_ERR_CUDA, std::string("permute launch: ") + cudaGetErrorString(e));
+      break;
+    }
+    cudaEventRecord(done[b], s.stream);
+    used[b] = true;
+  }
+  for (unsigned t = 0; t < nt; ++t) {
+    res.max_w = std::max(res.max_w, tmax[t]);
+    res.min_w = std::min(res.min_w, tmin[t]);
+  }
+  cleanup();
+  if (rc == SSSP_OK) {
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) rc = fail(SSSP_ERR_CUDA, cudaGetErrorString(e));
+  }
+  return rc;
+}
+
+int alloc_matrix(Shard& s, uint64_t n, uint32_t wbytes) {
+  if (s.d_adj) {
+    cudaFree(s.d_adj);
+    s.d_adj = nullptr;
+  }
+  CK(cudaMalloc(&s.d_adj, n * s.row_stride * wbytes));
+  return SSSP_OK;
+}
+
+// Uploads with the narrowest encoding that holds every finite weight.
+int upload_shard(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, uint64_t hint_max_w,
+                 uint32_t* wbytes_out, uint64_t* max_w, uint64_t* min_w) {
+  CK(cudaSetDevice(s.device));
+  uint32_t wb = hint_max_w == 0 ? 1 : hint_max_w <= 0xFEull ? 1 : hint_max_w <= 0xFFFEull ? 2 : 4;
+  while (true) {
+    if (hint_max_w > 0xFFFFFFFEull)
+      return fail(SSSP_ERR_WEIGHT_RANGE, "finite weight 0xFFFFFFFF needs the wide encoding");
+    int rc = alloc_matrix(s, n, wb);
+    if (rc) return rc;
+    ScanResult res;
+    rc = wb == 1 ? upload_block<uint8_t>(s, src, ld, n, res)
+         : wb == 2 ? upload_block<uint16_t>(s, src, ld, n, res)
+                   : upload_block<uint32_t>(s, src, ld, n, res);
+    if (rc) return rc;
+    if (!res.overflow) {
+      *wbytes_out = wb;
+      *max_w = res.max_w;
+      *min_w = res.min_w;
+      return SSSP_OK;
+    }
+    if (wb == 4)
+      return fail(SSSP_ERR_WEIGHT_RANGE, "finite weight 0xFFFFFFFF needs the wide encoding");
+    wb *= 2;
+  }
+}
+
+int alloc_state(sssp_graph* g, Shard& s) {
+  CK(cudaSetDevice(s.device));
+  const uint64_t B = g->max_batch;
+  CK(cudaMalloc(&s.d_slots, B * g->slot_stride * sizeof(uint64_t)));
+  CK(cudaMemset(s.d_slots, 0, B * g->slot_stride * sizeof(uint64_t)));
+  CK(cudaMalloc(&s.d_dist, B * std::max<uint64_t>(1, s.loc_n) * sizeof(uint64_t)));
+  CK(cudaMalloc(&s.d_pred, B * std::max<uint64_t>(1, s.loc_n) * sizeof(uint64_t)));
+  CK(cudaMalloc(&s.d_info, B * 4 * sizeof(uint64_t)));
+  CK(cudaMalloc(&s.d_sources, B * sizeof(uint32_t)));
+  CK(cudaHostAlloc(&s.h_sources, B * sizeof(uint32_t), cudaHostAllocDefault));
+  CK(cudaHostAlloc(&s.h_info, B * 4 * sizeof(uint64_t), cudaHostAllocDefault));
+  if (g->opt.record_visit_order && s.k == 0)
+    CK(cudaMalloc(&s.d_visit, B * g->n * sizeof(uint32_t)));
+  return SSSP_OK;
+}
+
+// Encoding-dependent constants shared by every shard; requires max_w.
+int finalize_encoding(sssp_graph* g) {
+  const uint64_t n = g->n;
+  // u32 distances: every candidate du + w <= n*max_w must stay below INF.
+  if (g->max_w != 0 && n > 0xFFFFFFFEull / g->max_w)
+    return fail(SSSP_ERR_WEIGHT_RANGE, "n * max_weight exceeds the 32-bit distance encoding");
+  const Shard& s0 = g->sh[0];
+  g->sbits = bitlen(s0.L) - 1;
+  const uint64_t dmax = n * g->max_w;
+  g->packed = (dmax + 1) < (1ull << (32 - g->sbits)) ? 1u : 0u;
+  const uint64_t total_cols = (uint64_t)g->P * s0.loc_n;
+  g->vbits = std::max<uint32_t>(1, bitlen(total_cols));
+  if (g->vbits > 29) return fail(SSSP_ERR_UNSUPPORTED, "vertex count exceeds the 29-bit key field");
+  g->bstride = ((uint64_t)g->P * s0.G + 1) & ~1ull;
+  g->slot_stride = 2 * g->bstride;
+  const uint64_t nslot = (uint64_t)g->P * s0.G;
+  const uint32_t np = nslot <= 128 ? 2 : nslot <= 256 ? 4 : nslot <= 1024 ? 16 : 0;
+  if (!np) return fail(SSSP_ERR_UNSUPPORTED, "too many exchange participants");
+  for (auto& s : g->sh) {
+    s.NP = np;
+    s.fn = pick_kernel((int)g->wbytes, (int)s.EPL, (int)np);
+    if (!s.fn) return fail(SSSP_ERR_UNSUPPORTED, "no kernel instance for this layout");
+  }
+  return SSSP_OK;
+}
+
+// Concurrent solves one launch may hold while keeping every CTA resident
+// (the persistent kernel spins, so all CTAs must be co-resident).
+int compute_max_batch(sssp_graph* g) {
+  uint32_t cap = ~0u;
+  // shards sharing a device share its SMs
+  for (auto& s : g->sh) {
+    CK(cudaSetDevice(s.device));
+    int per_sm = 0, sms = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, s.fn, 32, 0));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
+    uint32_t same = 0;
+    for (auto& t : g->sh) same += (t.device == s.device) ? 1 : 0;
+    const uint64_t blocks = (uint64_t)per_sm * sms;
+    const uint64_t need = (uint64_t)s.G * same;
+    if (need > blocks) return fail(SSSP_ERR_UNSUPPORTED, "shards do not fit co-resident");
+    cap = std::min<uint32_t>(cap, (uint32_t)(blocks / need));
+  }
+  uint32_t want = g->opt.max_batch ? g->opt.max_batch : 64;
+  g->max_batch = std::max<uint32_t>(1, std::min(cap, want));
+  return SSSP_OK;
+}
+
+int setup_common(sssp_graph* g) {
+  int rc = finalize_encoding(g);
+  if (rc) return rc;
+  rc = compute_max_batch(g);
+  if (rc) return rc;
+  g->matrix_bytes = 0;
+  for (auto& s : g->sh) {
+    rc = alloc_state(g, s);
+    if (rc) return rc;
+    g->matrix_bytes += g->n * s.row_stride * g->wbytes;
+  }
+  return SSSP_OK;
+}
+
+int create_shard_objects(sssp_graph* g, uint32_t P, const int* devices, uint32_t nlocal,
+                         uint32_t first_k) {
+  const uint64_t padded = pad_vertex_count(g->n, P);
+  const uint64_t loc_n = padded / P;
+  uint32_t gmax = g->opt.ctas_per_shard;
+  g->sh.resize(nlocal);
+  for (uint32_t i = 0; i < nlocal; ++i) {
+    Shard& s = g->sh[i];
+    s.device = devices[i];
+    s.k = first_k + i;
+    s.col_base = (uint64_t)s.k * loc_n;
+    s.loc_n = loc_n;
+    s.cols = s.col_base >= g->n ? 0 : std::min<uint64_t>(loc_n, g->n - s.col_base);
+    int sms = 148;
+    CK(cudaSetDevice(s.device));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
+    uint32_t gm = gmax;
+    if (!gm) gm = P == 1 ? (uint32_t)sms : std::max<uint32_t>(4, std::min<uint32_t>(sms, 256 / P));
+    int rc = plan_layout(s, loc_n, gm);
+    if (rc) return rc;
+    CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    CK(cudaEventCreate(&s.ev0));
+    CK(cudaEventCreate(&s.ev1));
+  }
+  return SSSP_OK;
+}
+
+void destroy_graph(sssp_graph* g) {
+  for (auto& s : g->sh) {
+    cudaSetDevice(s.device);
+    if (s.stream) cudaStreamSynchronize(s.stream);
+    for (int j = 0; j < kMaxShards; ++j)
+      if (s.peer_ipc[j] && s.peer[j]) cudaIpcCloseMemHandle(s.peer[j]);
+    cudaFree(s.d_adj);
+    cudaFree(s.d_slots);
+    cudaFree(s.d_dist);
+    cudaFree(s.d_pred);
+    cudaFree(s.d_info);
+    cudaFree(s.d_sources);
+    cudaFree(s.d_visit);
+    if (s.h_sources) cudaFreeHost(s.h_sources);
+    if (s.h_info) cudaFreeHost(s.h_info);
+    if (s.ev0) cudaEventDestroy(s.ev0);
+    if (s.ev1) cudaEventDestroy(s.ev1);
+    if (s.stream) cudaStreamDestroy(s.stream);
+  }
+  delete g;
+}
+
+// Enqueues one launch of k solves on every local shard.
+int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
+  if (g->multiproc && !g->connected)
+    return fail(SSSP_ERR_BAD_ARG, "shard not connected: call sssp_shard_connect first");
+  if (k == 0 || k > g->max_batch) return fail(SSSP_ERR_BAD_ARG, "bad batch size");
+  for (uint32_t i = 0; i < k; ++i)
+    if (sources[i] >= g->n) return fail(SSSP_ERR_BAD_SOURCE, "dijkstra: source out of range");
+  // Single process: reset the exchange buffers of every shard first, and make
+  // every launch wait for all resets (a peer may publish into our buffers as
+  // soon as its kernel starts).
+  std::vector<cudaEvent_t> reset_ev;
+  if (!g->multiproc) {
+    g->exch_base = 0;
+    for (auto& s : g->sh) {
+      CK(cudaSetDevice(s.device));
+      CK(cudaMemsetAsync(s.d_slots, 0, (uint64_t)k * g->slot_stride * sizeof(uint64_t), s.stream));
+      if (g->sh.size() > 1) {
+        cudaEvent_t e;
+        CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        CK(cudaEventRecord(e, s.stream));
+        reset_ev.push_back(e);
+      }
+    }
+  }
+  for (auto& s : g->sh) {
+    CK(cudaSetDevice(s.device));
+    for (cudaEvent_t e : reset_ev) CK(cudaStreamWaitEvent(s.stream, e, 0));
+    for (uint32_t i = 0; i < k; ++i) s.h_sources[i] = (uint32_t)sources[i];
+    CK(cudaMemcpyAsync(s.d_sources, s.h_sources, k * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                       s.stream));
+    CK(cudaMemsetAsync(s.d_info, 0, (uint64_t)k * 4 * sizeof(uint64_t), s.stream));
+    ScanParams p{};
+    p.adj = s.d_adj;
+    p.row_stride = s.row_stride;
+    p.n = (uint32_t)g->n;
+    p.G = s.G;
+    p.col_base = (uint32_t)s.col_base;
+    p.loc_n = (uint32_t)s.loc_n;
+    p.vbits = g->vbits;
+    p.shard = s.k;
+    p.nshards = g->P;
+    p.packed = g->packed;
+    p.sbits = g->sbits;
+    p.flags = g->opt.flags;
+    p.slots = s.d_slots;
+    for (uint32_t j = 0; j < g->P && j < (uint32_t)kMaxShards; ++j)
+      p.peer_slots[j] = g->multiproc ? s.peer[j] : g->sh[j].d_slots;
+    p.slot_stride = g->slot_stride;
+    p.bstride = (uint32_t)g->bstride;
+    p.exch_base = g->exch_base;
+    p.sources = s.d_sources;
+    p.nsolve = k;
+    p.dist_out = s.d_dist;
+    p.pred_out = s.d_pred;
+    p.visit_order = s.d_visit;
+    p.info = s.d_info;
+    p.timeout_ns = g->opt.timeout_ms * 1000000ull;
+    CK(cudaEventRecord(s.ev0, s.stream));
+    s.fn<<<k * s.G, 32, 0, s.stream>>>(p);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(s.ev1, s.stream));
+  }
+  for (cudaEvent_t e : reset_ev) cudaEventDestroy(e);
+  g->pending = k;
+  return SSSP_OK;
+}
+
+// Waits for the pending launch, checks the watchdog, fills stats.
+int finish(sssp_graph* g, sssp_solve_stats* st) {
+  const uint32_t k = g->pending;
+  if (k == 0) return fail(SSSP_ERR_BAD_ARG, "nothing enqueued");
+  double rounds = 0;
+  uint64_t iters = 0, last = 0, mis = 0;
+  bool timeout = false;
+  for (auto& s : g->sh) {
+    CK(cudaSetDevice(s.device));
+    CK(cudaMemcpyAsync(s.h_info, s.d_info, (uint64_t)k * 4 * sizeof(uint64_t),
+                       cudaMemcpyDeviceToHost, s.stream));
+    CK(cudaStreamSynchronize(s.stream));
+    float ms = 0;
+    CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
+    rounds = std::max(rounds, ms * 1e-3);
+    for (uint32_t i = 0; i < k; ++i) {
+      iters += s.k == g->sh[0].k ? s.h_info[4 * i] : 0;
+      last = std::max(last, s.h_info[4 * i + 1]);
+      timeout |= s.h_info[4 * i + 2] != 0;
+      mis += s.k == g->sh[0].k ? s.h_info[4 * i + 3] : 0;
+    }
+  }
+  g->pending = 0;
+  if (g->multiproc) g->exch_base = last + 1;
+  if (st) {
+    st->transfer_in_s = g->transfer_in_s;
+    st->rounds_s = rounds;
+    st->iterations = iters;
+    st->relax_checks = iters * g->sh[0].row_stride * g->P;
+    st->mispredicts = mis;
+    st->matrix_bytes = g->matrix_bytes;
+    st->weight_bytes = g->wbytes;
+    st->ctas = g->sh[0].G;
+    st->shards = g->P;
+    st->packed_key = g->packed;
+  }
+  if (timeout) return fail(SSSP_ERR_TIMEOUT, "exchange watchdog fired (a peer never published)");
+  return SSSP_OK;
+}
+
+// Copies solve i's owned columns of every local shard into the caller rows.
+int copy_out(sssp_graph* g, uint32_t k, uint64_t* dist_out, uint64_t* pred_out,
+             uint64_t row_len) {
+  for (auto& s : g->sh) {
+    if (s.cols == 0) continue;
+    CK(cudaSetDevice(s.device));
+    const uint64_t off = g->multiproc ? 0 : s.col_base;
+    if (dist_out)
+      CK(cudaMemcpy2DAsync(dist_out + off, row_len * 8, s.d_dist, s.loc_n * 8, s.cols * 8, k,
+                           cudaMemcpyDeviceToHost, s.stream));
+    if (pred_out)
+      CK(cudaMemcpy2DAsync(pred_out + off, row_len * 8, s.d_pred, s.loc_n * 8, s.cols * 8, k,
+                           cudaMemcpyDeviceToHost, s.stream));
+  }
+  for (auto& s : g->sh) {
+    CK(cudaSetDevice(s.device));
+    CK(cudaStreamSynchronize(s.stream));
+  }
+  return SSSP_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* sssp_status_string(int status) {
+  switch (status) {
+    case SSSP_OK: return "ok";
+    case SSSP_ERR_BAD_SOURCE: return "source out of range";
+    case SSSP_ERR_BAD_ARG: return "bad argument";
+    case SSSP_ERR_WEIGHT_RANGE: return "weight outside the device encoding";
+    case SSSP_ERR_OOM: return "out of memory";
+    case SSSP_ERR_CUDA: return "CUDA error";
+    case SSSP_ERR_NO_PEER: return "peer access unavailable";
+    case SSSP_ERR_TIMEOUT: return "exchange watchdog timeout";
+    case SSSP_ERR_UNSUPPORTED: return "unsupported configuration";
+  }
+  return "unknown status";
+}
+
+const char* sssp_last_error(void) { return g_err.c_str(); }
+
+int sssp_abi_version(void) { return SSSP_ABI_VERSION; }
+
+int sssp_device_count(int* count) {
+  *count = 0;
+  CK(cudaGetDeviceCount(count));
+  return SSSP_OK;
+}
+
+int sssp_graph_create(const uint64_t* adj, uint64_t n, int directed, const int* devices,
+                      int ndev, const sssp_options* opt, sssp_graph** out) {
+  *out = nullptr;
+  if (n == 0 || !adj) return fail(SSSP_ERR_BAD_ARG, "empty graph");
+  if (n > 0x1FFFFFFFull) return fail(SSSP_ERR_UNSUPPORTED, "n exceeds 2^29");
+  if (ndev < 0 || ndev > SSSP_MAX_SHARDS) return fail(SSSP_ERR_BAD_ARG, "1..8 shards");
+  const int dev0 = 0;
+  if (!devices || ndev == 0) {
+    devices = &dev0;
+    ndev = 1;
+  }
+  int count = 0;
+  CK(cudaGetDeviceCount(&count));
+  for (int i = 0; i < ndev; ++i)
+    if (devices[i] < 0 || devices[i] >= count) return fail(SSSP_ERR_BAD_ARG, "bad device id");
+  const double t0 = now_s();
+  sssp_graph* g = new sssp_graph();
+  g->n = n;
+  g->directed = directed;
+  g->P = (uint32_t)ndev;
+  g->opt = default_options(opt);
+  int rc = create_shard_objects(g, g->P, devices, g->P, 0);
+  // peer access between distinct devices
+  for (int i = 0; rc == SSSP_OK && i < ndev; ++i)
+    for (int j = 0; j < ndev; ++j) {
+      if (devices[i] == devices[j]) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devices[i], devices[j]);
+      if (!can) {
+        rc = fail(SSSP_ERR_NO_PEER, "no peer access between devices");
+        break;
+      }
+      cudaSetDevice(devices[i]);
+      cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
+        rc = fail(SSSP_ERR_NO_PEER, cudaGetErrorString(e));
+        break;
+      }
+      cudaGetLastError();
+    }
+  // Several shards must agree on one encoding: take it from a scan of the
+  // whole matrix.  A single shard widens optimistically inside the upload.
+  uint64_t hint = 0;
+  if (rc == SSSP_OK && g->P > 1) {
+    const unsigned nt = host_threads();
+    std::vector<uint64_t> tm(nt, 0);
+    parallel_for(0, n, nt, [&](uint64_t a, uint64_t e, unsigned t) {
+      uint64_t mx = 0;
+      for (uint64_t i = a * n; i < e * n; ++i) {
+        const uint64_t x = adj[i];
+        if (x != ~0ull && x > mx) mx = x;
+      }
+      tm[t] = mx;
+    });
+    for (uint64_t x : tm) hint = std::max(hint, x);
+  }
+  for (uint32_t i = 0; rc == SSSP_OK && i < g->P; ++i) {
+    Shard& s = g->sh[i];
+    uint32_t wb = 0;
+    uint64_t mx = 0, mn = ~0ull;
+    rc = upload_shard(s, adj + s.col_base, n, n, hint, &wb, &mx, &mn);
+    g->wbytes = std::max(g->wbytes, wb);
+    g->max_w = std::max(g->max_w, mx);
+    g->min_w = std::min(g->min_w, mn);
+  }
+  if (rc == SSSP_OK) rc = setup_common(g);
+  if (rc) {
+    destroy_graph(g);
+    return rc;
+  }
+  g->transfer_in_s = now_s() - t0;
+  *out = g;
+  return SSSP_OK;
+}
+
+int sssp_shard_create(const uint64_t* block, uint64_t ld, uint64_t n, uint32_t world,
+                      uint32_t rank, uint64_t max_weight, int device, const sssp_options* opt,
+                      sssp_graph** out) {
+  *out = nullptr;
+  if (n == 0 || !block) return fail(SSSP_ERR_BAD_ARG, "empty graph");
+  if (world < 1 || world > SSSP_MAX_SHARDS || rank >= world)
+    return fail(SSSP_ERR_BAD_ARG, "bad rank/world");
+  const double t0 = now_s();
+  sssp_graph* g = new sssp_graph();
+  g->n = n;
+  g->P = world;
+  g->multiproc = world > 1;
+  g->connected = world == 1;
+  g->opt = default_options(opt);
+  int rc = create_shard_objects(g, world, &device, 1, rank);
+  if (rc == SSSP_OK) {
+    uint32_t wb = 0;
+    uint64_t mx = 0, mn = ~0ull;
+    rc = upload_shard(g->sh[0], block, ld, n, max_weight, &wb, &mx, &mn);
+    g->wbytes = wb;
+    g->max_w = std::max(mx, max_weight);
+    g->min_w = mn;
+    // all ranks must agree on the encoding: derive it from the global bound
+    if (rc == SSSP_OK && max_weight) {
+      const uint32_t want = max_weight <= 0xFE ? 1 : max_weight <= 0xFFFE ? 2 : 4;
+      if (want != wb) rc = fail(SSSP_ERR_WEIGHT_RANGE, "max_weight hint below the block's weights");
+    }
+  }
+  if (rc == SSSP_OK) rc = setup_common(g);
+  if (rc == SSSP_OK && world == 1) g->sh[0].peer[0] = g->sh[0].d_slots;
+  if (rc) {
+    destroy_graph(g);
+    return rc;
+  }
+  g->transfer_in_s = now_s() - t0;
+  *out = g;
+  return SSSP_OK;
+}
+
+int sssp_shard_export(sssp_graph* g, void* handle_out) {
+  if (!g || g->sh.size() != 1) return fail(SSSP_ERR_BAD_ARG, "not a shard handle");
+  CK(cudaSetDevice(g->sh[0].device));
+  cudaIpcMemHandle_t h;
+  CK(cudaIpcGetMemHandle(&h, g->sh[0].d_slots));
+  std::memcpy(handle_out, &h, sizeof(h));
+  return SSSP_OK;
+}
+
+int sssp_shard_connect(sssp_graph* g, const void* handles) {
+  if (!g || g->sh.size() != 1) return fail(SSSP_ERR_BAD_ARG, "not a shard handle");
+  Shard& s = g->sh[0];
+  CK(cudaSetDevice(s.device));
+  for (uint32_t j = 0; j < g->P; ++j) {
+    if (j == s.k) {
+      s.peer[j] = s.d_slots;
+      continue;
+    }
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, static_cast<const char*>(handles) + (size_t)j * SSSP_IPC_HANDLE_BYTES,
+                sizeof(h));
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(SSSP_ERR_NO_PEER, cudaGetErrorString(e));
+    s.peer[j] = static_cast<uint64_t*>(p);
+    s.peer_ipc[j] = true;
+  }
+  g->connected = true;
+  return SSSP_OK;
+}
+
+int sssp_shard_range(const sssp_graph* g, uint64_t* col_begin, uint64_t* col_count) {
+  if (!g || g->sh.empty()) return fail(SSSP_ERR_BAD_ARG, "null handle");
+  *col_begin = g->sh[0].col_base;
+  *col_count = g->multiproc ? g->sh[0].cols : g->n;
+  if (!g->multiproc) *col_begin = 0;
+  return SSSP_OK;
+}
+
+int sssp_graph_destroy(sssp_graph* g) {
+  if (g) destroy_graph(g);
+  return SSSP_OK;
+}
+
+int sssp_graph_info(const sssp_graph* g, sssp_solve_stats* st) {
+  if (!g || !st) return fail(SSSP_ERR_BAD_ARG, "null");
+  std::memset(st, 0, sizeof(*st));
+  st->transfer_in_s = g->transfer_in_s;
+  st->matrix_bytes = g->matrix_bytes;
+  st->weight_bytes = g->wbytes;
+  st->ctas = g->sh[0].G;
+  st->shards = g->P;
+  st->packed_key = g->packed;
+  st->iterations = g->max_batch;  // reused: concurrent solve capacity
+  st->relax_checks = g->min_w;    // reused: min finite off-diagonal weight
+  st->mispredicts = g->max_w;     // reused: max finite weight
+  return SSSP_OK;
+}
+
+int sssp_solve(sssp_graph* g, uint64_t source, uint64_t* dist_out, uint64_t* pred_out,
+               uint64_t* visit_order_out, sssp_solve_stats* st) {
+  if (!g) return fail(SSSP_ERR_BAD_ARG, "null handle");
+  int rc = launch(g, &source, 1);
+  if (rc) return rc;
+  sssp_solve_stats local{};
+  rc = finish(g, &local);
+  if (rc) return rc;
+  const double t0 = now_s();
+  rc = copy_out(g, 1, dist_out, pred_out, g->multiproc ? g->sh[0].cols : g->n);
+  if (rc) return rc;
+  if (visit_order_out) {
+    if (!g->sh[0].d_visit) return fail(SSSP_ERR_BAD_ARG, "record_visit_order was not set");
+    std::vector<uint32_t> tmp(local.iterations);
+    CK(cudaSetDevice(g->sh[0].device));
+    CK(cudaMemcpy(tmp.data(), g->sh[0].d_visit, local.iterations * 4, cudaMemcpyDeviceToHost));
+    for (uint64_t i = 0; i < local.iterations; ++i) visit_order_out[i] = tmp[i];
+  }
+  local.transfer_out_s = now_s() - t0;
+  if (st) *st = local;
+  return SSSP_OK;
+}
+
+int sssp_solve_batch(sssp_graph* g, const uint64_t* sources, uint32_t k, uint64_t* dist_out,
+                     uint64_t* pred_out, sssp_solve_stats* st) {
+  if (!g) return fail(SSSP_ERR_BAD_ARG, "null handle");
+  sssp_solve_stats total{};
+  const uint64_t row_len = g->multiproc ? g->sh[0].cols : g->n;
+  for (uint32_t i0 = 0; i0 < k; i0 += g->max_batch) {
+    const uint32_t kk = std::min<uint32_t>(g->max_batch, k - i0);
+    int rc = launch(g, sources + i0, kk);
+    if (rc) return rc;
+    sssp_solve_stats part{};
+    rc = finish(g, &part);
+    if (rc) return rc;
+    const double t0 = now_s();
+    rc = copy_out(g, kk, dist_out ? dist_out + (uint64_t)i0 * row_len : nullptr,
+                  pred_out ? pred_out + (uint64_t)i0 * row_len : nullptr, row_len);
+    if (rc) return rc;
+    total.transfer_out_s += now_s() - t0;
+    total.rounds_s += part.rounds_s;
+    total.iterations += part.iterations;
+    total.relax_checks += part.relax_checks;
+    total.mispredicts += part.mispredicts;
+    total.transfer_in_s = part.transfer_in_s;
+    total.matrix_bytes = part.matrix_bytes;
+    total.weight_bytes = part.weight_bytes;
+    total.ctas = part.ctas;
+    total.shards = part.shards;
+    total.packed_key = part.packed_key;
+  }
+  if (st) *st = total;
+  return SSSP_OK;
+}
+
+int sssp_enqueue(sssp_graph* g, const uint64_t* sources, uint32_t k) {
+  if (!g) return fail(SSSP_ERR_BAD_ARG, "null handle");
+  if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is already pending");
+  return launch(g, sources, k);
+}
+
+int sssp_finish(sssp_graph* g, sssp_solve_stats* st) {
+  if (!g) return fail(SSSP_ERR_BAD_ARG, "null handle");
+  return finish(g, st);
+}
+
+int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round) {
+  if (!g || rounds == 0) return fail(SSSP_ERR_BAD_ARG, "bad probe arguments");
+  if (g->multiproc && !g->connected) return fail(SSSP_ERR_BAD_ARG, "shard not connected");
+  if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
+  using ProbeFn = void (*)(const ScanParams, uint32_t, uint64_t*);
+  const uint32_t np = g->sh[0].NP;
+  ProbeFn fn = np == 2 ? exchange_probe_kernel<2> : np == 4 ? exchange_probe_kernel<4>
+                                                            : exchange_probe_kernel<16>;
+  std::vector<uint64_t*> d_ns(g->sh.size(), nullptr);
+  std::vector<cudaEvent_t> reset_ev;
+  if (!g->multiproc) {
+    g->exch_base = 0;
+    for (auto& s : g->sh) {
+      CK(cudaSetDevice(s.device));
+      CK(cudaMemsetAsync(s.d_slots, 0, g->slot_stride * sizeof(uint64_t), s.stream));
+      cudaEvent_t e;
+      CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+      CK(cudaEventRecord(e, s.stream));
+      reset_ev.push_back(e);
+    }
+  }
+  for (size_t i = 0; i < g->sh.size(); ++i) {
+    Shard& s = g->sh[i];
+    CK(cudaSetDevice(s.device));
+    for (cudaEvent_t e : reset_ev) CK(cudaStreamWaitEvent(s.stream, e, 0));
+    CK(cudaMalloc(&d_ns[i], sizeof(uint64_t)));
+    CK(cudaMemsetAsync(s.d_info, 0, 4 * sizeof(uint64_t), s.stream));
+    ScanParams p{};
+    p.G = s.G;
+    p.vbits = g->vbits;
+    p.shard = s.k;
+    p.nshards = g->P;
+    p.slots = s.d_slots;
+    for (uint32_t j = 0; j < g->P && j < (uint32_t)kMaxShards; ++j)
+      p.peer_slots[j] = g->multiproc ? s.peer[j] : g->sh[j].d_slots;
+    p.slot_stride = g->slot_stride;
+    p.bstride = (uint32_t)g->bstride;
+    p.exch_base = g->exch_base;
+    p.info = s.d_info;
+    p.timeout_ns = g->opt.timeout_ms * 1000000ull;
+    fn<<<s.G, 32, 0, s.stream>>>(p, rounds, d_ns[i]);
+    CK(cudaGetLastError());
+  }
+  double worst = 0;
+  uint64_t last = 0;
+  for (size_t i = 0; i < g->sh.size(); ++i) {
+    Shard& s = g->sh[i];
+    CK(cudaSetDevice(s.device));
+    CK(cudaStreamSynchronize(s.stream));
+    uint64_t ns = 0, info[4];
+    CK(cudaMemcpy(&ns, d_ns[i], sizeof(ns), cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(info, s.d_info, sizeof(info), cudaMemcpyDeviceToHost));
+    cudaFree(d_ns[i]);
+    if (ns == ~0ull) return fail(SSSP_ERR_TIMEOUT, "probe watchdog fired");
+    worst = std::max(worst, ns * 1e-9 / rounds);
+    last = std::max(last, info[1]);
+  }
+  for (cudaEvent_t e : reset_ev) cudaEventDestroy(e);
+  if (g->multiproc) g->exch_base = last + 1;
+  *seconds_per_round = worst;
+  return SSSP_OK;
+}
+
+void* sssp_stream(sssp_graph* g, int local) {
+  if (!g || local < 0 || (size_t)local >= g->sh.size()) return nullptr;
+  return g->sh[(size_t)local].stream;
+}
+
+}  // extern "C"

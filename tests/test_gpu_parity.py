@@ -1,0 +1,280 @@
+"""Parity of the B200 path (C ABI via ctypes) against the CPU oracle.
+
+Bit-exact dist[] AND pred[] (ShortestPathResult operator==, result.hpp:18)
+versus dijkstra_serial (serial.hpp:26-68) restated in oracle/sssp_oracle.c,
+which tests/test_oracle.py pins to the reference's own compiled code.
+Cases mirror the reference suite: test_serial.cpp:11-75,
+test_partitioned.cpp:135-228, test_dataparallel.cpp:144-154 and the
+acceptance sweep (acceptance.cpp:42-80).
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+INF = 0xFFFFFFFFFFFFFFFF
+
+
+def serial(oracle_c, g, s):
+    d, p = oracle_c.serial(g.adj, g.n, s)
+    return d, p
+
+
+def assert_same(res, d, p, ctx=""):
+    if not (np.array_equal(res.dist, d) and np.array_equal(res.pred, p)):
+        bad = np.nonzero((res.dist != d) | (res.pred != p))[0]
+        i = int(bad[0])
+        raise AssertionError(f"{ctx}: {len(bad)} mismatches, first v={i}: gpu=({res.dist[i]},"
+                             f"{res.pred[i]}) oracle=({d[i]},{p[i]})")
+
+
+def four(gpu, directed):
+    return gpu.graph_from_edges(4, [(0, 1, 2), (0, 2, 4), (1, 2, 1), (1, 3, 3), (2, 3, 5)],
+                                directed)
+
+
+def test_four_vertex_example(gpu):
+    # test_serial.cpp:11-19
+    r = gpu.dijkstra(four(gpu, False), 0)
+    assert r.dist.tolist() == [0, 2, 3, 5]
+    assert r.pred.tolist() == [INF, 0, 1, 1]
+    assert r.source == 0
+
+
+def test_four_vertex_visit_order(gpu):
+    # test_serial.cpp:69-75
+    with gpu.DeviceGraph(four(gpu, False), visit_order=True) as dg:
+        r = dg.solve(0, visit_order=True)
+    assert r.stats["visit_order"].tolist() == [0, 1, 2, 3]
+
+
+def test_directed_sink_reaches_nothing(gpu):
+    # test_serial.cpp:21-26
+    r = gpu.dijkstra(four(gpu, True), 3)
+    assert r.dist.tolist() == [INF, INF, INF, 0]
+    assert r.pred.tolist() == [INF] * 4
+
+
+def test_single_vertex(gpu):
+    # test_serial.cpp:28-33
+    r = gpu.dijkstra(gpu.Graph.no_edges(1), 0)
+    assert r.dist.tolist() == [0] and r.pred.tolist() == [INF]
+
+
+def test_source_out_of_range(gpu):
+    # test_serial.cpp:35-38 (std::invalid_argument)
+    g = gpu.Graph.no_edges(3)
+    with gpu.DeviceGraph(g) as dg:
+        with pytest.raises(ValueError):
+            dg.solve(3)
+
+
+def test_zero_weight_tie_fixture(gpu):
+    # test_dataparallel.cpp:144-154 graph; serial pred = [2, 2, NONE, 1]
+    g = gpu.graph_from_edges(4, [(2, 0, 5), (2, 1, 5), (0, 1, 0), (1, 3, 2)], False)
+    r = gpu.dijkstra(g, 2)
+    assert r.dist.tolist() == [5, 5, 0, 7]
+    assert r.pred.tolist() == [2, 2, INF, 1]
+
+
+def test_isolated_source(gpu):
+    # test_partitioned.cpp:198-204
+    g = gpu.Graph.no_edges(5, True)
+    g.adj[1 * 5 + 2] = 4
+    r = gpu.dijkstra(g, 0)
+    assert r.dist.tolist() == [0, INF, INF, INF, INF]
+
+
+def random_tie_graph(rng, n, wmax, density, directed):
+    adj = np.full((n, n), INF, dtype=np.uint64)
+    mask = rng.random((n, n)) < density
+    w = rng.integers(0, wmax + 1, size=(n, n), dtype=np.uint64)
+    adj[mask] = w[mask]
+    if not directed:
+        iu = np.triu_indices(n, 1)
+        adj[(iu[1], iu[0])] = adj[iu]
+    np.fill_diagonal(adj, 0)
+    return adj
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_tie_heavy_sweep(gpu, oracle_c, seed):
+    """Weights in {0..3} (zero-weight ties), random density, both directions."""
+    rng = np.random.default_rng(1000 + seed)
+    with_graphs = 0
+    for i in range(40):
+        n = int(rng.integers(1, 300))
+        directed = bool(i % 2)
+        adj = random_tie_graph(rng, n, 3, float(rng.choice([0.01, 0.05, 0.2, 0.6, 1.0])), directed)
+        g = gpu.Graph(n, directed, adj)
+        s = int(rng.integers(0, n))
+        r = gpu.dijkstra(g, s)
+        d, p = serial(oracle_c, g, s)
+        assert_same(r, d, p, f"seed={seed} i={i} n={n}")
+        with_graphs += 1
+    assert with_graphs == 40
+
+
+def test_acceptance_sweep_graphs(gpu, oracle_c):
+    """acceptance.cpp:42-80: 400 graphs, dense/sparse x dir/undir, n in 7..200,
+    rng 20240601 -- full ShortestPathResult equality with serial."""
+    rng = oracle_c.rng(20240601)
+    checked = 0
+    for dense in (False, True):
+        for directed in (False, True):
+            for _ in range(100):
+                n = 7 + rng() % 194
+                seed = rng()
+                adj = (oracle_c.dense(n, seed, directed) if dense else
+                       oracle_c.sparse(n, seed, directed))
+                s = rng() % n
+                g = gpu.Graph(n, directed, adj)
+                r = gpu.dijkstra(g, s)
+                d, p = serial(oracle_c, g, s)
+                assert_same(r, d, p, f"dense={dense} directed={directed} n={n}")
+                checked += 1
+    assert checked == 400
+
+
+@pytest.mark.parametrize("kind", ["sparse", "dense"])
+def test_config1_n1000(gpu, oracle_c, kind):
+    """BASELINE config 1: n=1000 generate_{sparse,dense}(1000, 42), s=0."""
+    g = (gpu.generate_sparse if kind == "sparse" else gpu.generate_dense)(1000, 42)
+    r = gpu.dijkstra(g, 0)
+    d, p = serial(oracle_c, g, 0)
+    assert_same(r, d, p, kind)
+    assert oracle_c.validate(g.adj, g.n, 0, r.dist, r.pred) == 0
+
+
+@pytest.mark.parametrize("flags", [0, 1, 2, 3])
+def test_prefetch_flags_are_semantic_noops(gpu, oracle_c, flags):
+    g = gpu.generate_dense(3000, 7)
+    d, p = serial(oracle_c, g, 5)
+    with gpu.DeviceGraph(g, flags=flags) as dg:
+        assert_same(dg.solve(5), d, p, f"flags={flags}")
+
+
+@pytest.mark.parametrize("n", [2, 31, 127, 128, 129, 255, 4095, 4097, 9000])
+@pytest.mark.parametrize("ctas", [0, 1, 3, 7])
+def test_layout_edges(gpu, oracle_c, n, ctas):
+    """n around the 128-column CTA slice and odd CTA counts (padding columns)."""
+    rng = np.random.default_rng(n * 31 + ctas)
+    adj = random_tie_graph(rng, n, 2, min(1.0, 8.0 / n + 0.01), False)
+    g = gpu.Graph(n, False, adj)
+    s = int(rng.integers(0, n))
+    d, p = serial(oracle_c, g, s)
+    try:
+        dg = gpu.DeviceGraph(g, ctas=ctas)
+    except gpu.SsspError as e:  # too many columns for that few CTAs
+        assert ctas and n > ctas * 2048, str(e)
+        return
+    with dg:
+        assert_same(dg.solve(s), d, p, f"n={n} ctas={ctas}")
+
+
+@pytest.mark.parametrize("wmax,wbytes", [(254, 1), (255, 2), (40000, 2), (65534, 2),
+                                         (65535, 4), (3_000_000, 4)])
+def test_weight_encodings(gpu, oracle_c, wmax, wbytes):
+    rng = np.random.default_rng(wmax)
+    n = 700
+    adj = np.full((n, n), INF, dtype=np.uint64)
+    mask = rng.random((n, n)) < 0.02
+    adj[mask] = rng.integers(0, wmax + 1, size=int(mask.sum()), dtype=np.uint64)
+    adj[0, 1] = wmax  # make sure the max is present
+    np.fill_diagonal(adj, 0)
+    g = gpu.Graph(n, True, adj)
+    d, p = serial(oracle_c, g, 0)
+    with gpu.DeviceGraph(g) as dg:
+        info = dg.info()
+        assert info["weight_bytes"] == wbytes
+        assert_same(dg.solve(0), d, p, f"wmax={wmax}")
+
+
+def test_unpacked_key_path(gpu, oracle_c):
+    """Distances too wide for the single-redux packed key use the 2-stage redux."""
+    rng = np.random.default_rng(5)
+    n = 3000
+    adj = random_tie_graph(rng, n, 1, 0.01, True)
+    big = rng.integers(0, 1_000_000, size=(n, n), dtype=np.uint64)
+    adj = np.where(adj == INF, adj, adj * big)
+    np.fill_diagonal(adj, 0)
+    g = gpu.Graph(n, True, adj)
+    d, p = serial(oracle_c, g, 0)
+    with gpu.DeviceGraph(g) as dg:
+        assert dg.info()["packed_key"] == 0
+        assert_same(dg.solve(0), d, p, "unpacked")
+
+
+def test_weight_range_errors_are_loud(gpu):
+    g = gpu.Graph.no_edges(3, True)
+    g.adj[1] = 0xFFFFFFFF  # kMaxWeight is a legal finite weight (weight.hpp:18)
+    with pytest.raises(gpu.SsspError):
+        gpu.DeviceGraph(g)
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_logical_shards_bit_identical(gpu, oracle_c, P):
+    """P column shards on one GPU run the multi-GPU exchange protocol (peer
+    stores into every shard's array); result == serial (test_partitioned.cpp
+    :149-165, 184-196)."""
+    for n, seed in [(1000, 3), (2049, 4)]:
+        g = gpu.generate_sparse(n, seed) if seed % 2 else gpu.generate_dense(n, seed)
+        d, p = serial(oracle_c, g, 7)
+        r = gpu.dijkstra_partitioned(g, 7, P)
+        assert_same(r, d, p, f"P={P} n={n}")
+
+
+def test_shards_p_greater_than_n(gpu, oracle_c):
+    # test_partitioned.cpp:149-165 includes p > n (padding-only shards)
+    g = four(gpu, False)
+    d, p = serial(oracle_c, g, 0)
+    assert_same(gpu.dijkstra_partitioned(g, 0, 7), d, p, "p>n")
+
+
+def test_batch_sources(gpu, oracle_c):
+    g = gpu.generate_dense(2000, 11)
+    sources = list(range(0, 2000, 31))
+    with gpu.DeviceGraph(g) as dg:
+        res = dg.solve_batch(sources)
+    for s, r in zip(sources, res):
+        d, p = serial(oracle_c, g, s)
+        assert_same(r, d, p, f"s={s}")
+
+
+def test_repeated_solves_are_deterministic(gpu):
+    g = gpu.generate_sparse(5000, 8)
+    with gpu.DeviceGraph(g) as dg:
+        a = dg.solve(0)
+        b = dg.solve(0)
+        c = dg.solve(17)
+        d = dg.solve(0)
+    assert a == b == d and not (a == c)
+
+
+def test_visit_order_matches_serial(gpu, oracle_c):
+    g = gpu.generate_sparse(3000, 9, directed=True)
+    d, p, vo = oracle_c.serial(g.adj, g.n, 0, visit_order=True)
+    finite = int(np.count_nonzero(d != INF))
+    with gpu.DeviceGraph(g, visit_order=True) as dg:
+        r = dg.solve(0, visit_order=True)
+    assert r.stats["iterations"] == finite
+    assert np.array_equal(r.stats["visit_order"], vo[:finite])
+
+
+def test_config2_n16384_bernoulli(gpu, oracle_c):
+    """BASELINE config 2: n=16384, Bernoulli(0.5), undirected, s=0."""
+    g = gpu.generate_bernoulli(16384, 0.5, 16384)
+    r = gpu.dijkstra(g, 0)
+    d, p = serial(oracle_c, g, 0)
+    assert_same(r, d, p, "config2")
+
+
+def test_config3_n32768_dense(gpu, oracle_c):
+    """BASELINE config 3 on one GPU: generate_dense(32768, 32768), s=0."""
+    g = gpu.generate_dense(32768, 32768)
+    with gpu.DeviceGraph(g) as dg:
+        r = dg.solve(0)
+        st = r.stats
+    d, p = serial(oracle_c, g, 0)
+    assert_same(r, d, p, "config3")
+    assert st["iterations"] == 32768 and st["weight_bytes"] == 1
