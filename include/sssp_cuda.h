@@ -47,20 +47,25 @@ typedef enum {
   SSSP_ERR_UNSUPPORTED = 8   /* configuration not supported on this device */
 } sssp_status;
 
-/* Election/relaxation engine of a solve. */
+/* How the n-round persistent scan kernel exchanges each round's election.
+ * Both are bit-identical to dijkstra_serial; they differ in latency. */
 typedef enum {
-  SSSP_ENGINE_AUTO = 0, /* the n-round persistent scan kernel (north-star path) */
-  SSSP_ENGINE_SCAN = 1  /* same, explicitly */
+  SSSP_ENGINE_AUTO = 0,    /* = CLUSTER */
+  SSSP_ENGINE_GRID = 1,    /* single-warp CTAs across the GPU, exchange through L2 */
+  SSSP_ENGINE_CLUSTER = 2  /* one thread-block cluster per solve, exchange through DSMEM */
 } sssp_engine;
 
 typedef struct {
   int engine;             /* sssp_engine */
-  uint32_t ctas_per_shard;/* 0 = auto (<= SM count); CTAs of one solve on one shard */
+  uint32_t ctas_per_shard;/* 0 = auto; CTAs of one solve on one shard (cluster engine:
+                             the cluster size, <= 16; grid engine: <= SM count) */
   uint32_t flags;         /* bit0: runner-up row prefetch, bit1: owner L2 row prefetch;
                              SSSP_FLAGS_DEFAULT when the options pointer is NULL */
   uint32_t max_batch;     /* concurrent solves a batch launch may run (0 = auto) */
   uint64_t timeout_ms;    /* exchange watchdog (0 = 60000) */
   int record_visit_order; /* 1: keep the elected vertex of every round */
+  uint32_t replicas;      /* grid engine: copies of the L2 exchange array (0 = 1) */
+  uint32_t warps_per_cta; /* cluster engine: 4, 8 or 16 (0 = 8) */
 } sssp_options;
 
 #define SSSP_FLAGS_DEFAULT 3u

@@ -204,15 +204,21 @@ def generate_bernoulli(n: int, p: float, seed: int, directed: bool = False,
     return Graph(n, directed, out) if cols is None else out.reshape(n, cols[1])
 
 
+ENGINES = {"auto": 0, "grid": 1, "cluster": 2}
+
+
 def _options(flags: Optional[int], ctas: int, max_batch: int, timeout_ms: int,
-             visit_order: bool) -> Options:
+             visit_order: bool, replicas: int = 0, engine: str = "auto",
+             warps: int = 0) -> Options:
     o = Options()
-    o.engine = 0
+    o.engine = ENGINES[engine]
+    o.warps_per_cta = warps
     o.ctas_per_shard = ctas
     o.flags = _native.SSSP_FLAGS_DEFAULT if flags is None else flags
     o.max_batch = max_batch
     o.timeout_ms = timeout_ms
     o.record_visit_order = int(visit_order)
+    o.replicas = replicas
     return o
 
 
@@ -224,9 +230,11 @@ class DeviceGraph:
 
     def __init__(self, g: Graph, devices: Sequence[int] = (0,), *, flags: Optional[int] = None,
                  ctas: int = 0, max_batch: int = 0, timeout_ms: int = 0,
-                 visit_order: bool = False):
+                 visit_order: bool = False, replicas: int = 0, engine: str = "auto",
+                 warps: int = 0):
         self.n = g.n
-        self._opt = _options(flags, ctas, max_batch, timeout_ms, visit_order)
+        self._opt = _options(flags, ctas, max_batch, timeout_ms, visit_order, replicas, engine,
+                             warps)
         devs = (ctypes.c_int * len(devices))(*devices)
         h = ctypes.c_void_p()
         check(lib.sssp_graph_create(_p64(g.adj), g.n, int(g.directed), devs, len(devices),
@@ -315,9 +323,9 @@ class ShardGraph(DeviceGraph):
 
     def __init__(self, block: np.ndarray, n: int, world: int, rank: int, max_weight: int,
                  device: int = 0, *, flags: Optional[int] = None, ctas: int = 0,
-                 timeout_ms: int = 0):
+                 timeout_ms: int = 0, replicas: int = 0, engine: str = "auto", warps: int = 0):
         self.n = n
-        self._opt = _options(flags, ctas, 1, timeout_ms, False)
+        self._opt = _options(flags, ctas, 1, timeout_ms, False, replicas, engine, warps)
         blk = np.ascontiguousarray(block, dtype=np.uint64)
         ld = blk.shape[1] if blk.ndim == 2 else max(1, blk.size // max(1, n))
         h = ctypes.c_void_p()

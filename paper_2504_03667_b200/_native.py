@@ -42,6 +42,8 @@ class Options(ctypes.Structure):
         ("max_batch", ctypes.c_uint32),
         ("timeout_ms", ctypes.c_uint64),
         ("record_visit_order", ctypes.c_int),
+        ("replicas", ctypes.c_uint32),
+        ("warps_per_cta", ctypes.c_uint32),
     ]
 
 

@@ -1,0 +1,428 @@
+// cluster_kernel.cuh -- the cluster-resident persistent Dijkstra kernel.
+//
+// Same algorithm, layout and key protocol as scan_kernel.cuh (read that
+// header first), but one solve lives in ONE thread-block cluster of C CTAs
+// x NW warps (C <= 16, non-portable size) and the per-round election is
+// exchanged through distributed shared memory instead of L2:
+//
+//  * participant q = cta_rank*NW + warp owns local columns {s*Q + q}, Q = C*NW
+//    (the cyclic layout of scan_kernel.cuh with G = Q);
+//  * every warp reduces its (dist, vertex) key with redux.sync and stores the
+//    tagged key into slot q of EVERY CTA's shared-memory exchange array
+//    (mapa + st.shared::cluster: one DSMEM store per destination CTA);
+//  * every warp polls its own CTA's array with ld.shared (no L2 round trip)
+//    until all Q keys carry this round's tag, and reduces them itself.
+//
+// A DSMEM store + local poll costs a few hundred cycles where the grid-wide
+// L2 exchange of scan_kernel.cuh measured ~1 us per round (profiles/), so a
+// 16-SM cluster beats the 128-SM grid on every configured size, and
+// independent solves (batched sources) simply occupy more clusters without
+// any inter-cluster synchronisation.
+//
+// With P > 1 shards (one per GPU) the cluster minimum of the local columns
+// is published to every shard's global mailbox by P2P store (NVLink), and the
+// global winner is the minimum over the P mailbox keys: the allreduce_minloc
+// of partitioned.hpp:94-101.
+#pragma once
+
+#include "scan_kernel.cuh"
+
+namespace sssp_b200 {
+
+__device__ __forceinline__ uint32_t cluster_ctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ uint32_t cluster_nctarank() {
+  uint32_t r;
+  asm volatile("mov.u32 %0, %%cluster_nctarank;" : "=r"(r));
+  return r;
+}
+
+__device__ __forceinline__ void cluster_sync_all() {
+  asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::
+                   : "memory");
+}
+
+__device__ __forceinline__ void st_dsmem(uint32_t local_addr, uint32_t cta, uint64_t v) {
+  uint32_t remote;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(remote) : "r"(local_addr), "r"(cta));
+  asm volatile("st.relaxed.cluster.shared::cluster.u64 [%0], %1;" ::"r"(remote), "l"(v) : "memory");
+}
+
+__device__ __forceinline__ uint64_t ld_smem_pair(uint32_t addr, uint64_t& hi) {
+  uint64_t lo;
+  asm volatile("ld.relaxed.cluster.shared::cta.v2.u64 {%0, %1}, [%2];"
+               : "=l"(lo), "=l"(hi)
+               : "r"(addr)
+               : "memory");
+  return lo;
+}
+
+// Per-lane column state.  PACKED (the common case, chosen on the host when
+// (n*max_w + 1) < 2^(32-SB)) keeps ONE 32-bit register per column:
+//   ek = ((dist << SB) | slot) + 1   unvisited, finite dist
+//   ek = 0xFFFFFFFF                  unvisited, dist = INF
+//   ek = 0                           visited (elected)
+// so that  relax    : improve iff  w != INF  and  cand + 1 < ek   (a visited
+//                     column can never improve: 0 is the minimum), and
+//          election : min over (ek - 1) puts visited columns (0 - 1 = MAX)
+//                     last and orders the rest by (dist, slot) = (dist, vertex).
+// The +1 keeps the encoding monotone; finite keys stay below 2^32 - 2^SB.
+// Without PACKED, dist and a visited mask are kept apart and the election is
+// a 2-stage redux (dist, then slot).
+template <typename W, int EPL, int NW, bool PACKED>
+__global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanParams p) {
+  using Row = RowSlice<W, EPL>;
+  constexpr int NP = NW / 4;  // key pairs per lane: Q <= 16*NW = 64*NP
+  constexpr uint32_t WINF = WInf<W>::v;
+  constexpr uint32_t DINF = 0xFFFFFFFFu;
+  constexpr uint32_t L = 32u * EPL;
+  constexpr uint32_t SB = (L == 128 ? 7 : L == 256 ? 8 : L == 512 ? 9 : 10);
+  constexpr uint32_t QMAX = 16u * NW;
+  static_assert(NW >= 4 && NW % 4 == 0, "NW must be a multiple of 4");
+  static_assert((1u << SB) == L, "L must be a power of two");
+
+  extern __shared__ uint32_t s_pred[];  // [NW][L], dynamic (up to 64 KB)
+  __shared__ __align__(16) uint64_t s_keys[2][QMAX];
+
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t cr = cluster_ctarank();
+  const uint32_t csize = cluster_nctarank();
+  const uint32_t Q = p.G;             // = csize * NW, a power of two
+  const uint32_t qbits = 31u - __clz(Q);
+  const uint32_t solve = blockIdx.x / csize;
+  const uint32_t q = cr * NW + warp;
+  const uint32_t tb = 32u - p.vbits;
+  const uint64_t tagmask = (1ull << tb) - 1ull;
+  const uint32_t vmask_all = (p.vbits >= 32) ? 0xFFFFFFFFu : ((1u << p.vbits) - 1u);
+  const bool multi = p.nshards > 1;
+  const W* const adj = static_cast<const W*>(p.adj) + (size_t)q * L;
+  const uint32_t row_bytes = (uint32_t)(p.row_stride * sizeof(W));
+  const bool pf_reg = (p.flags & kFlagPrefetchReg) != 0;
+  const bool pf_l2 = (p.flags & kFlagPrefetchL2) != 0;
+  uint32_t* const pred = s_pred + warp * L;
+  uint64_t* const dout = p.dist_out + (size_t)solve * p.loc_n;
+  uint64_t* const pout = p.pred_out + (size_t)solve * p.loc_n;
+  // lane's slot of element e is  ebase(e) | lbase  (disjoint bit fields)
+  const uint32_t lbase = (uint32_t)lane * Row::VEC;
+
+  // ---- init (serial.hpp:32-36)
+  const uint32_t source = p.sources[solve];
+  uint32_t ek[EPL];  // PACKED state
+  uint32_t d[EPL];   // !PACKED state
+  uint64_t vis = 0;
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const uint32_t s = Row::slot(e, lane);
+    const uint32_t vl = (s << qbits) | q;
+    const bool pad = vl >= p.loc_n || p.col_base + vl >= p.n;
+    const bool src = !pad && p.col_base + vl == source;
+    if constexpr (PACKED) {
+      ek[e] = pad ? 0u : src ? s + 1u : DINF;
+    } else {
+      d[e] = src ? 0u : DINF;
+      if (pad) vis |= (1ull << e);
+    }
+  }
+  for (uint32_t i = lane; i < L; i += 32) pred[i] = 0xFFFFFFFFu;
+  for (uint32_t i = threadIdx.x; i < 2 * QMAX; i += NW * 32) (&s_keys[0][0])[i] = 0;
+  cluster_sync_all();  // every exchange array is zeroed before anyone publishes
+
+  uint32_t u = source, du = 0;
+  uint64_t E = p.exch_base;
+  uint64_t iters = 0, mispredicts = 0;
+  uint32_t pred_u = 0xFFFFFFFFu, last_l2 = 0xFFFFFFFFu;
+  Row cur, nxt;
+  cur.load(adj + (size_t)u * p.row_stride, lane);
+  uint64_t ks[2 * NP];
+#pragma unroll
+  for (int j = 0; j < 2 * NP; ++j) ks[j] = ~0ull;
+  uint64_t best_key = 0;
+  const uint64_t t_start = globaltimer();
+  bool failed = false;
+  const uint32_t keys_base = (uint32_t)__cvta_generic_to_shared(&s_keys[0][0]);
+
+  while (true) {
+    // ---- the owner of u marks it visited and records its final distance
+    {
+      const uint32_t ul = u - p.col_base;
+      if (u >= p.col_base && ul < p.loc_n && (ul & (Q - 1)) == q) {
+        const uint32_t su = ul >> qbits;
+        if ((uint32_t)lane == ((su / Row::VEC) & 31u)) {
+          const uint32_t eu = (su / (32u * Row::VEC)) * Row::VEC + su % Row::VEC;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e)
+            if ((uint32_t)e == eu) {
+              if constexpr (PACKED) ek[e] = 0u;
+              else vis |= (1ull << e);
+            }
+          dout[ul] = du;
+        }
+      }
+    }
+    // ---- relax row u (serial.hpp:51-60; strict '<' keeps the earliest parent)
+    if constexpr (PACKED) {
+      const uint32_t dus1 = (du << SB) + 1u + lbase;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const uint32_t w = cur.elem(e);
+        const uint32_t nk = w * L + dus1 + (Row::slot(e, 0));
+        if (w != WINF && nk < ek[e]) {
+          ek[e] = nk;
+          pred[Row::slot(e, 0) | lbase] = u;
+        }
+      }
+    } else {
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const uint32_t w = cur.elem(e);
+        const uint32_t nd = du + w;
+        if (w != WINF && nd < d[e] && !((vis >> e) & 1ull)) {
+          d[e] = nd;
+          pred[Row::slot(e, 0) | lbase] = u;
+        }
+      }
+    }
+    ++iters;
+    if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
+      p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
+
+    // ---- warp election (serial.hpp:42-48)
+    uint32_t bd, bs;
+    if constexpr (PACKED) {
+      uint32_t k = 0xFFFFFFFFu;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) k = min(k, ek[e] - 1u);
+      k = __reduce_min_sync(0xFFFFFFFFu, k);
+      const bool none = k >= 0xFFFFFFFEu || (k >> SB) == (DINF >> SB);
+      bd = none ? DINF : (k >> SB);
+      bs = k & (L - 1u);
+    } else {
+      bd = DINF;
+      bs = 0xFFFFFFFFu;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const bool live = !((vis >> e) & 1ull) && d[e] != DINF;
+        if (live && d[e] < bd) {
+          bd = d[e];
+          bs = Row::slot(e, lane);
+        }
+      }
+      warp_lexmin(bd, bs);
+    }
+    const uint32_t bv = (bd == DINF) ? vmask_all : (p.col_base + ((bs << qbits) | q));
+
+    // ---- publish into every CTA's exchange array (DSMEM)
+    ++E;
+    const uint32_t buf = (uint32_t)(E & 1ull);
+    const uint64_t want = E & tagmask;
+    const uint64_t key = ((uint64_t)bd << 32) | ((uint64_t)(bv & vmask_all) << tb) | want;
+    const uint32_t my_slot_addr = keys_base + (buf * QMAX + q) * 8u;
+    if ((uint32_t)lane < csize) st_dsmem(my_slot_addr, (uint32_t)lane, key);
+
+    // ---- off the critical path: L2 prefetch of my new local best's row, and
+    // the runner-up of the previous round's keys into registers.
+    if (pf_l2 && bd != DINF && bv != last_l2) {
+      if (lane == 0)
+        prefetch_l2_bulk(static_cast<const W*>(p.adj) + (size_t)bv * p.row_stride, row_bytes);
+      last_l2 = bv;
+    }
+    if (pf_reg) {
+      uint64_t r = ~0ull;
+#pragma unroll
+      for (int j = 0; j < 2 * NP; ++j) r = (ks[j] != best_key && ks[j] < r) ? ks[j] : r;
+      uint32_t a = (uint32_t)(r >> 32), b = (uint32_t)r;
+      warp_lexmin(a, b);
+      if (a != DINF && iters > 1) {
+        pred_u = b >> tb;
+        nxt.load(adj + (size_t)pred_u * p.row_stride, lane);
+      } else {
+        pred_u = 0xFFFFFFFFu;
+      }
+    }
+
+    // ---- gather from my own shared memory
+    {
+      const uint32_t arr = keys_base + buf * QMAX * 8u;
+      const uint32_t want32 = (uint32_t)want;
+      const uint32_t tm32 = (uint32_t)tagmask;
+      uint32_t polls = 0;
+      while (true) {
+        bool ok = true;
+#pragma unroll
+        for (int j = 0; j < NP; ++j) {
+          const uint32_t i = 2u * lane + 64u * j;
+          if (i < Q) {  // Q is even (NW >= 4)
+            uint64_t hi;
+            const uint64_t lo = ld_smem_pair(arr + i * 8u, hi);
+            ks[2 * j] = lo;
+            ks[2 * j + 1] = hi;
+            ok &= (((uint32_t)lo & tm32) == want32) & (((uint32_t)hi & tm32) == want32);
+          } else {
+            ks[2 * j] = ks[2 * j + 1] = ~0ull;
+          }
+        }
+        if (__all_sync(0xFFFFFFFFu, ok)) break;
+        if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) {
+          failed = true;
+          break;
+        }
+      }
+    }
+    if (failed) break;
+    best_key = min_key<NP>(ks);
+
+    // ---- P > 1: exchange the cluster minimum between shards (P2P mailbox)
+    if (multi) {
+      if (q == 0 && (uint32_t)lane < p.nshards)
+        st_slot(p.peer_slots[lane] + (uint64_t)solve * p.slot_stride + (uint64_t)buf * p.bstride +
+                    p.shard,
+                best_key, true);
+      const uint64_t* mb = p.slots + (uint64_t)solve * p.slot_stride + (uint64_t)buf * p.bstride;
+      uint64_t mk = ~0ull;
+      uint32_t polls = 0;
+      while (true) {
+        mk = (uint32_t)lane < p.nshards ? ld_slot(mb + lane, true) : ~0ull;
+        const bool ok = (uint32_t)lane >= p.nshards || (mk & tagmask) == want;
+        if (__all_sync(0xFFFFFFFFu, ok)) break;
+        if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) {
+          failed = true;
+          break;
+        }
+      }
+      if (failed) break;
+      uint32_t a = (uint32_t)(mk >> 32), b = (uint32_t)mk;
+      warp_lexmin(a, b);
+      best_key = ((uint64_t)a << 32) | b;
+    }
+
+    du = (uint32_t)(best_key >> 32);
+    if (du == DINF) break;
+    u = (uint32_t)(best_key & 0xFFFFFFFFull) >> tb;
+    if (pf_reg && u == pred_u) {
+      cur = nxt;
+    } else {
+      if (pf_reg) ++mispredicts;
+      cur.load(adj + (size_t)u * p.row_stride, lane);
+    }
+  }
+
+  // ---- write back: unvisited columns are unreachable; pred from smem
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const uint32_t s = Row::slot(e, lane);
+    const uint32_t vl = (s << qbits) | q;
+    if (vl < p.loc_n && p.col_base + vl < p.n) {
+      bool visited;
+      if constexpr (PACKED) visited = ek[e] == 0u;
+      else visited = (vis >> e) & 1ull;
+      if (!visited) dout[vl] = ~0ull;
+      const uint32_t pr = pred[s];
+      pout[vl] = pr == 0xFFFFFFFFu ? ~0ull : (uint64_t)pr;
+    }
+  }
+  uint64_t* inf = p.info + (size_t)solve * 4;
+  if (failed && lane == 0) atomicOr((unsigned long long*)(inf + 2), 1ull);
+  if (q == 0 && lane == 0) {
+    inf[0] = iters;
+    inf[1] = E;
+    inf[3] = mispredicts;
+  }
+  cluster_sync_all();  // no CTA leaves while a peer could still address its smem
+}
+
+// t_sync microbenchmark for the cluster exchange (same code, no relax).
+template <int NW>
+__global__ void __launch_bounds__(NW * 32, 1) cluster_probe_kernel(const ScanParams p,
+                                                                  uint32_t rounds,
+                                                                  uint64_t* out_ns) {
+  constexpr int NP = NW / 4;
+  constexpr uint32_t QMAX = 16u * NW;
+  __shared__ __align__(16) uint64_t s_keys[2][QMAX];
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t cr = cluster_ctarank();
+  const uint32_t csize = cluster_nctarank();
+  const uint32_t Q = p.G;
+  const uint32_t solve = blockIdx.x / csize;
+  const uint32_t q = cr * NW + warp;
+  const uint32_t tb = 32u - p.vbits;
+  const uint64_t tagmask = (1ull << tb) - 1ull;
+  const bool multi = p.nshards > 1;
+  for (uint32_t i = threadIdx.x; i < 2 * QMAX; i += NW * 32) (&s_keys[0][0])[i] = 0;
+  cluster_sync_all();
+  const uint32_t keys_base = (uint32_t)__cvta_generic_to_shared(&s_keys[0][0]);
+  uint64_t ks[2 * NP];
+  uint64_t E = p.exch_base, acc = 0;
+  const uint64_t t0 = globaltimer();
+  bool failed = false;
+  for (uint32_t r = 0; r < rounds && !failed; ++r) {
+    ++E;
+    const uint32_t buf = (uint32_t)(E & 1ull);
+    const uint64_t want = E & tagmask;
+    const uint32_t dist = (r * 2654435761u + q * 40503u) >> 20;
+    const uint64_t key = ((uint64_t)dist << 32) | ((uint64_t)(p.shard * Q + q) << tb) | want;
+    if ((uint32_t)lane < csize) st_dsmem(keys_base + (buf * QMAX + q) * 8u, (uint32_t)lane, key);
+    const uint32_t arr = keys_base + buf * QMAX * 8u;
+    uint32_t polls = 0;
+    while (true) {
+      bool ok = true;
+#pragma unroll
+      for (int j = 0; j < NP; ++j) {
+        const uint32_t i = 2u * lane + 64u * j;
+        if (i < Q) {
+          uint64_t hi;
+          const uint64_t lo = ld_smem_pair(arr + i * 8u, hi);
+          ks[2 * j] = lo;
+          ok &= (lo & tagmask) == want;
+          ks[2 * j + 1] = i + 1 < Q ? hi : ~0ull;
+          if (i + 1 < Q) ok &= (hi & tagmask) == want;
+        } else {
+          ks[2 * j] = ks[2 * j + 1] = ~0ull;
+        }
+      }
+      if (__all_sync(0xFFFFFFFFu, ok)) break;
+      if ((++polls & 1023u) == 0 && globaltimer() - t0 > p.timeout_ns) {
+        failed = true;
+        break;
+      }
+    }
+    if (failed) break;
+    uint64_t best = min_key<NP>(ks);
+    if (multi) {
+      if (q == 0 && (uint32_t)lane < p.nshards)
+        st_slot(p.peer_slots[lane] + (uint64_t)solve * p.slot_stride + (uint64_t)buf * p.bstride +
+                    p.shard,
+                best, true);
+      const uint64_t* mb = p.slots + (uint64_t)solve * p.slot_stride + (uint64_t)buf * p.bstride;
+      uint32_t polls2 = 0;
+      uint64_t mk;
+      while (true) {
+        mk = (uint32_t)lane < p.nshards ? ld_slot(mb + lane, true) : ~0ull;
+        const bool ok = (uint32_t)lane >= p.nshards || (mk & tagmask) == want;
+        if (__all_sync(0xFFFFFFFFu, ok)) break;
+        if ((++polls2 & 1023u) == 0 && globaltimer() - t0 > p.timeout_ns) {
+          failed = true;
+          break;
+        }
+      }
+      uint32_t a = (uint32_t)(mk >> 32), b = (uint32_t)mk;
+      warp_lexmin(a, b);
+      best = ((uint64_t)a << 32) | b;
+    }
+    acc += best >> 32;
+  }
+  if (q == 0 && lane == 0) {
+    out_ns[solve] = failed ? ~0ull : globaltimer() - t0;
+    p.info[solve * 4 + 1] = E;
+    p.info[solve * 4 + 0] = acc;
+  }
+  cluster_sync_all();
+}
+
+}  // namespace sssp_b200

@@ -1,0 +1,54 @@
+// kernels_cluster.cu -- instances of the cluster engine (cluster_kernel.cuh).
+#include "cluster_kernel.cuh"
+#include "dispatch.h"
+
+namespace sssp_b200 {
+namespace {
+
+template <typename W, int EPL, bool PK>
+KernelFn pick_nw(int nw) {
+  switch (nw) {
+    case 4: return cluster_scan_kernel<W, EPL, 4, PK>;
+    case 8: return cluster_scan_kernel<W, EPL, 8, PK>;
+    case 16: return cluster_scan_kernel<W, EPL, 16, PK>;
+  }
+  return nullptr;
+}
+
+template <typename W, bool PK>
+KernelFn pick_epl(int epl, int nw) {
+  switch (epl) {
+    case 4: return pick_nw<W, 4, PK>(nw);
+    case 8: return pick_nw<W, 8, PK>(nw);
+    case 16: return pick_nw<W, 16, PK>(nw);
+    case 32: return pick_nw<W, 32, PK>(nw);
+  }
+  return nullptr;
+}
+
+template <bool PK>
+KernelFn pick_w(int wbytes, int epl, int nw) {
+  switch (wbytes) {
+    case 1: return pick_epl<uint8_t, PK>(epl, nw);
+    case 2: return pick_epl<uint16_t, PK>(epl, nw);
+    case 4: return pick_epl<uint32_t, PK>(epl, nw);
+  }
+  return nullptr;
+}
+
+}  // namespace
+
+KernelFn get_cluster_kernel(int wbytes, int epl, int nw, bool packed) {
+  return packed ? pick_w<true>(wbytes, epl, nw) : pick_w<false>(wbytes, epl, nw);
+}
+
+ProbeFn get_cluster_probe(int nw) {
+  switch (nw) {
+    case 4: return cluster_probe_kernel<4>;
+    case 8: return cluster_probe_kernel<8>;
+    case 16: return cluster_probe_kernel<16>;
+  }
+  return nullptr;
+}
+
+}  // namespace sssp_b200

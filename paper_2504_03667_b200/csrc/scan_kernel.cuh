@@ -52,8 +52,9 @@ struct ScanParams {
   uint32_t flags;           // kFlag* below
   uint64_t* slots;          // local exchange array, [nsolve][2][P*G]
   uint64_t* peer_slots[kMaxShards];  // every shard's exchange array (self included)
-  uint64_t slot_stride;     // words per solve in an exchange array (= 2*bstride)
-  uint32_t bstride;         // words per buffer (P*G rounded up to even)
+  uint64_t slot_stride;     // words per solve in an exchange array (= 2*nrep*bstride)
+  uint32_t bstride;         // words per replica (P*G rounded up to 16 = one 128 B line)
+  uint32_t nrep;            // replicas of every buffer; CTA c polls replica c % nrep
   uint64_t exch_base;       // first exchange index of this launch
   const uint32_t* sources;  // [nsolve] global source ids
   uint32_t nsolve;
@@ -186,17 +187,20 @@ struct RowSlice {
 
 
 
-// Flag-in-data publish: lane j < P stores the key into shard j's exchange
-// array (NVLink P2P store for a remote shard); single shard: lane 0 only.
+// Flag-in-data publish: lane j stores the key into replica j % nrep of shard
+// j / nrep's exchange array (an NVLink P2P store for a remote shard).
 __device__ __forceinline__ void publish_key(const ScanParams& p, uint64_t* my_slots,
                                             uint32_t solve, uint32_t c, int lane, uint32_t buf,
                                             uint64_t key, bool multi) {
-  const uint64_t slot_off = (uint64_t)buf * p.bstride + (uint64_t)p.shard * p.G + c;
-  if (multi) {
-    if ((uint32_t)lane < p.nshards)
-      st_slot(p.peer_slots[lane] + (uint64_t)solve * p.slot_stride + slot_off, key, true);
-  } else if (lane == 0) {
-    st_slot(my_slots + slot_off, key, false);
+  // Every buffer is replicated nrep times so that at most ceil(G/nrep)
+  // pollers share an L2 line (one line hammered by all G pollers serialises
+  // in its L2 slice and was the dominant cost of a round).
+  const uint64_t slot_off = (uint64_t)buf * p.nrep * p.bstride + (uint64_t)p.shard * p.G + c;
+  const uint32_t fan = p.nshards * p.nrep;
+  for (uint32_t j = lane; j < fan; j += 32) {
+    const uint32_t dst = j / p.nrep, rep = j - dst * p.nrep;
+    uint64_t* base = multi ? p.peer_slots[dst] + (uint64_t)solve * p.slot_stride : my_slots;
+    st_slot(base + slot_off + (uint64_t)rep * p.bstride, key, multi);
   }
 }
 
@@ -272,8 +276,8 @@ __global__ void __launch_bounds__(32, 1) exchange_probe_kernel(const ScanParams 
     const uint32_t dist = (r * 2654435761u + c * 40503u) >> 20;
     const uint64_t key = ((uint64_t)dist << 32) | ((uint64_t)(p.shard * p.G + c) << tb) | want;
     publish_key(p, my_slots, solve, c, lane, buf, key, multi);
-    if (!gather_keys<NP>(p, my_slots + (uint64_t)buf * p.bstride, nslot, lane, want, tagmask,
-                         multi, t0, ks)) {
+    if (!gather_keys<NP>(p, my_slots + ((uint64_t)buf * p.nrep + c % p.nrep) * p.bstride, nslot,
+                         lane, want, tagmask, multi, t0, ks)) {
       failed = true;
       break;
     }
@@ -426,8 +430,8 @@ __global__ void __launch_bounds__(32, 1) scan_dijkstra_kernel(const ScanParams p
     }
 
     // ---- gather: poll until every participant's key carries tag E.
-    failed = !gather_keys<NP>(p, my_slots + (uint64_t)buf * p.bstride, nslot, lane, want,
-                              tagmask, multi, t_start, ks);
+    failed = !gather_keys<NP>(p, my_slots + ((uint64_t)buf * p.nrep + c % p.nrep) * p.bstride,
+                              nslot, lane, want, tagmask, multi, t_start, ks);
     if (failed) break;
     best_key = min_key<NP>(ks);
     du = (uint32_t)(best_key >> 32);

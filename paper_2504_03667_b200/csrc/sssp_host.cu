@@ -17,7 +17,7 @@
 #include <vector>
 
 #include "../../include/sssp_cuda.h"
-#include "scan_kernel.cuh"
+#include "dispatch.h"
 
 using namespace sssp_b200;
 
@@ -57,39 +57,6 @@ uint32_t bitlen(uint64_t x) {
 uint64_t pad_vertex_count(uint64_t n, uint64_t p) {
   if (p > n) return p;
   return n + (p - n % p) % p;
-}
-
-using KernelFn = void (*)(const ScanParams);
-
-template <typename W, int EPL>
-KernelFn pick_np(int np) {
-  switch (np) {
-    case 2: return scan_dijkstra_kernel<W, EPL, 2>;
-    case 4: return scan_dijkstra_kernel<W, EPL, 4>;
-    case 16: return scan_dijkstra_kernel<W, EPL, 16>;
-  }
-  return nullptr;
-}
-
-template <typename W>
-KernelFn pick_epl(int epl, int np) {
-  switch (epl) {
-    case 4: return pick_np<W, 4>(np);
-    case 8: return pick_np<W, 8>(np);
-    case 16: return pick_np<W, 16>(np);
-    case 32: return pick_np<W, 32>(np);
-    case 64: return pick_np<W, 64>(np);
-  }
-  return nullptr;
-}
-
-KernelFn pick_kernel(int wbytes, int epl, int np) {
-  switch (wbytes) {
-    case 1: return pick_epl<uint8_t>(epl, np);
-    case 2: return pick_epl<uint16_t>(epl, np);
-    case 4: return pick_epl<uint32_t>(epl, np);
-  }
-  return nullptr;
 }
 
 // Rearranges a chunk of staged rows (natural column order) into the
@@ -140,7 +107,8 @@ struct Shard {
   cudaEvent_t ev0 = nullptr, ev1 = nullptr;
   void* d_adj = nullptr;
   uint64_t row_stride = 0;  // G*L
-  uint32_t G = 0, EPL = 0, L = 0, NP = 0;
+  uint32_t G = 0, EPL = 0, L = 0, NP = 0;  // G = participants (warps) per solve
+  uint32_t C = 1, NW = 1;                   // cluster engine: CTAs per cluster, warps per CTA
   uint32_t k = 0;           // shard index
   uint64_t col_base = 0, loc_n = 0, cols = 0;  // cols = real columns held
   uint64_t* d_slots = nullptr;
@@ -169,6 +137,8 @@ struct sssp_graph {
   uint32_t vbits = 0, sbits = 0, packed = 0;
   uint32_t max_batch = 1;
   uint64_t slot_stride = 0, bstride = 0;
+  uint32_t nrep = 1;
+  bool cluster = true;  // engine: cluster (DSMEM exchange) or grid (L2 exchange)
   uint64_t exch_base = 0;
   double transfer_in_s = 0;
   uint32_t pending = 0;  // solves enqueued and not yet finished
@@ -185,7 +155,7 @@ sssp_options default_options(const sssp_options* o) {
   return d;
 }
 
-// Chooses EPL/G for a shard of loc_n columns with at most gmax CTAs.
+// Grid engine: EPL/G for a shard of loc_n columns with at most gmax CTAs.
 int plan_layout(Shard& s, uint64_t loc_n, uint32_t gmax) {
   static const uint32_t epls[] = {4, 8, 16, 32, 64};
   for (uint32_t epl : epls) {
@@ -196,11 +166,34 @@ int plan_layout(Shard& s, uint64_t loc_n, uint32_t gmax) {
       s.EPL = epl;
       s.L = (uint32_t)L;
       s.G = (uint32_t)std::max<uint64_t>(1, G);
+      s.C = s.G;
+      s.NW = 1;
       s.row_stride = (uint64_t)s.G * s.L;
       return SSSP_OK;
     }
   }
   return SSSP_ERR_UNSUPPORTED;
+}
+
+// Cluster engine: C CTAs (<= cmax) of NW warps, EPL columns per lane; the
+// smallest EPL whose cluster of at most cmax CTAs covers loc_n.
+int plan_cluster_layout(Shard& s, uint64_t loc_n, uint32_t cmax, uint32_t nw) {
+  static const uint32_t epls[] = {4, 8, 16, 32};
+  for (uint32_t epl : epls) {
+    const uint64_t per_cta = (uint64_t)nw * 32 * epl;
+    uint64_t C = std::max<uint64_t>(1, (loc_n + per_cta - 1) / per_cta);
+    while (C & (C - 1)) ++C;  // participants Q = C*NW must be a power of two
+    if (C <= cmax) {
+      s.EPL = epl;
+      s.L = 32 * epl;
+      s.NW = nw;
+      s.C = (uint32_t)C;
+      s.G = s.C * nw;
+      s.row_stride = (uint64_t)s.G * s.L;
+      return SSSP_OK;
+    }
+  }
+  return fail(SSSP_ERR_UNSUPPORTED, "graph too large for one cluster; use more shards or the grid engine");
 }
 
 struct ScanResult {
@@ -374,14 +367,31 @@ int finalize_encoding(sssp_graph* g) {
   const uint64_t total_cols = (uint64_t)g->P * s0.loc_n;
   g->vbits = std::max<uint32_t>(1, bitlen(total_cols));
   if (g->vbits > 29) return fail(SSSP_ERR_UNSUPPORTED, "vertex count exceeds the 29-bit key field");
-  g->bstride = ((uint64_t)g->P * s0.G + 1) & ~1ull;
-  g->slot_stride = 2 * g->bstride;
+  if (g->cluster) {
+    // exchange lives in shared memory; global memory holds only the P-slot
+    // cross-shard mailbox [2][bstride] per solve
+    g->bstride = ((uint64_t)g->P + 15) & ~15ull;
+    g->nrep = 1;
+    g->slot_stride = 2ull * g->bstride;
+    for (auto& s : g->sh) {
+      s.NP = s.NW / 4;
+      s.fn = get_cluster_kernel((int)g->wbytes, (int)s.EPL, (int)s.NW, g->packed != 0);
+      if (!s.fn) return fail(SSSP_ERR_UNSUPPORTED, "no cluster kernel instance for this layout");
+    }
+    return SSSP_OK;
+  }
+  g->bstride = ((uint64_t)g->P * s0.G + 15) & ~15ull;
+  uint32_t rep = g->opt.replicas ? g->opt.replicas : 1u;
+  rep = std::max<uint32_t>(1, std::min<uint32_t>(rep, s0.G));
+  while ((uint64_t)rep * g->P > 64) rep = std::max<uint32_t>(1, rep / 2);
+  g->nrep = rep;
+  g->slot_stride = 2ull * g->nrep * g->bstride;
   const uint64_t nslot = (uint64_t)g->P * s0.G;
   const uint32_t np = nslot <= 128 ? 2 : nslot <= 256 ? 4 : nslot <= 1024 ? 16 : 0;
   if (!np) return fail(SSSP_ERR_UNSUPPORTED, "too many exchange participants");
   for (auto& s : g->sh) {
     s.NP = np;
-    s.fn = pick_kernel((int)g->wbytes, (int)s.EPL, (int)np);
+    s.fn = get_grid_kernel((int)g->wbytes, (int)s.EPL, (int)np);
     if (!s.fn) return fail(SSSP_ERR_UNSUPPORTED, "no kernel instance for this layout");
   }
   return SSSP_OK;
@@ -391,14 +401,39 @@ int finalize_encoding(sssp_graph* g) {
 // (the persistent kernel spins, so all CTAs must be co-resident).
 int compute_max_batch(sssp_graph* g) {
   uint32_t cap = ~0u;
-  // shards sharing a device share its SMs
   for (auto& s : g->sh) {
     CK(cudaSetDevice(s.device));
+    uint32_t same = 0;
+    for (auto& t : g->sh) same += (t.device == s.device) ? 1 : 0;
+    if (g->cluster) {
+      if (s.C > 8) CK(cudaFuncSetAttribute(s.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+      cudaLaunchConfig_t cfg{};
+      const size_t dsm = (size_t)s.NW * s.L * 4;
+      CK(cudaFuncSetAttribute(s.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+      cfg.gridDim = dim3(s.C);
+      cfg.blockDim = dim3(s.NW * 32);
+      cfg.dynamicSmemBytes = dsm;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = s.C;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int clusters = 0;
+      CK(cudaOccupancyMaxActiveClusters(&clusters, (void*)s.fn, &cfg));
+      if (clusters < 1) return fail(SSSP_ERR_UNSUPPORTED, "cluster shape not schedulable");
+      // Independent single-shard solves need no co-residency (clusters never
+      // wait on each other).  Shards of one solve do: keep every launch resident.
+      if (g->P > 1) {
+        if ((uint32_t)clusters < same) return fail(SSSP_ERR_UNSUPPORTED, "shards do not fit co-resident");
+        cap = std::min<uint32_t>(cap, (uint32_t)clusters / same);
+      }
+      continue;
+    }
     int per_sm = 0, sms = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, s.fn, 32, 0));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
-    uint32_t same = 0;
-    for (auto& t : g->sh) same += (t.device == s.device) ? 1 : 0;
     const uint64_t blocks = (uint64_t)per_sm * sms;
     const uint64_t need = (uint64_t)s.G * same;
     if (need > blocks) return fail(SSSP_ERR_UNSUPPORTED, "shards do not fit co-resident");
@@ -428,6 +463,7 @@ int create_shard_objects(sssp_graph* g, uint32_t P, const int* devices, uint32_t
   const uint64_t padded = pad_vertex_count(g->n, P);
   const uint64_t loc_n = padded / P;
   uint32_t gmax = g->opt.ctas_per_shard;
+  g->cluster = g->opt.engine != SSSP_ENGINE_GRID;
   g->sh.resize(nlocal);
   for (uint32_t i = 0; i < nlocal; ++i) {
     Shard& s = g->sh[i];
@@ -439,9 +475,16 @@ int create_shard_objects(sssp_graph* g, uint32_t P, const int* devices, uint32_t
     int sms = 148;
     CK(cudaSetDevice(s.device));
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
-    uint32_t gm = gmax;
-    if (!gm) gm = P == 1 ? (uint32_t)sms : std::max<uint32_t>(4, std::min<uint32_t>(sms, 256 / P));
-    int rc = plan_layout(s, loc_n, gm);
+    int rc;
+    if (g->cluster) {
+      const uint32_t nw = g->opt.warps_per_cta ? g->opt.warps_per_cta : 8;
+      if (nw != 4 && nw != 8 && nw != 16) return fail(SSSP_ERR_BAD_ARG, "warps_per_cta: 4, 8 or 16");
+      rc = plan_cluster_layout(s, loc_n, gmax ? std::min<uint32_t>(gmax, 16) : 16, nw);
+    } else {
+      uint32_t gm = gmax;
+      if (!gm) gm = P == 1 ? (uint32_t)sms : std::max<uint32_t>(4, std::min<uint32_t>(sms, 256 / P));
+      rc = plan_layout(s, loc_n, gm);
+    }
     if (rc) return rc;
     CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&s.ev0));
@@ -470,6 +513,36 @@ void destroy_graph(sssp_graph* g) {
     if (s.stream) cudaStreamDestroy(s.stream);
   }
   delete g;
+}
+
+// Launches k solves of `fn` (cluster engine: k clusters of C CTAs x NW warps;
+// grid engine: k*G single-warp CTAs).  Probe kernels pass rounds/out_ns.
+cudaError_t launch_kernel(sssp_graph* g, Shard& s, void* fn, uint32_t k, const ScanParams& p,
+                          const uint32_t* rounds, int is_probe, uint64_t* out_ns) {
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute at[1];
+  cfg.stream = s.stream;
+  if (g->cluster) {
+    cfg.gridDim = dim3(k * s.C);
+    cfg.blockDim = dim3(s.NW * 32);
+    cfg.dynamicSmemBytes = is_probe ? 0 : (size_t)s.NW * s.L * 4;
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = s.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  } else {
+    cfg.gridDim = dim3(k * s.G);
+    cfg.blockDim = dim3(32);
+  }
+  if (is_probe) {
+    uint32_t r = *rounds;
+    void* args[] = {(void*)&p, (void*)&r, (void*)&out_ns};
+    return cudaLaunchKernelExC(&cfg, fn, args);
+  }
+  void* args[] = {(void*)&p};
+  return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
 // Enqueues one launch of k solves on every local shard.
@@ -521,6 +594,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
       p.peer_slots[j] = g->multiproc ? s.peer[j] : g->sh[j].d_slots;
     p.slot_stride = g->slot_stride;
     p.bstride = (uint32_t)g->bstride;
+    p.nrep = g->nrep;
     p.exch_base = g->exch_base;
     p.sources = s.d_sources;
     p.nsolve = k;
@@ -530,8 +604,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
     p.info = s.d_info;
     p.timeout_ns = g->opt.timeout_ms * 1000000ull;
     CK(cudaEventRecord(s.ev0, s.stream));
-    s.fn<<<k * s.G, 32, 0, s.stream>>>(p);
-    CK(cudaGetLastError());
+    CK(launch_kernel(g, s, (void*)s.fn, k, p, nullptr, 0, nullptr));
     CK(cudaEventRecord(s.ev1, s.stream));
   }
   for (cudaEvent_t e : reset_ev) cudaEventDestroy(e);
@@ -571,7 +644,7 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     st->mispredicts = mis;
     st->matrix_bytes = g->matrix_bytes;
     st->weight_bytes = g->wbytes;
-    st->ctas = g->sh[0].G;
+    st->ctas = g->cluster ? g->sh[0].C : g->sh[0].G;
     st->shards = g->P;
     st->packed_key = g->packed;
   }
@@ -793,7 +866,7 @@ int sssp_graph_info(const sssp_graph* g, sssp_solve_stats* st) {
   st->transfer_in_s = g->transfer_in_s;
   st->matrix_bytes = g->matrix_bytes;
   st->weight_bytes = g->wbytes;
-  st->ctas = g->sh[0].G;
+  st->ctas = g->cluster ? g->sh[0].C : g->sh[0].G;
   st->shards = g->P;
   st->packed_key = g->packed;
   st->iterations = g->max_batch;  // reused: concurrent solve capacity
@@ -872,10 +945,11 @@ int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round) {
   if (!g || rounds == 0) return fail(SSSP_ERR_BAD_ARG, "bad probe arguments");
   if (g->multiproc && !g->connected) return fail(SSSP_ERR_BAD_ARG, "shard not connected");
   if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
-  using ProbeFn = void (*)(const ScanParams, uint32_t, uint64_t*);
   const uint32_t np = g->sh[0].NP;
-  ProbeFn fn = np == 2 ? exchange_probe_kernel<2> : np == 4 ? exchange_probe_kernel<4>
-                                                            : exchange_probe_kernel<16>;
+  ProbeFn fn = g->cluster ? get_cluster_probe((int)g->sh[0].NW) : get_grid_probe((int)np);
+  if (!fn) return fail(SSSP_ERR_UNSUPPORTED, "no probe instance");
+  if (g->cluster && g->sh[0].C > 8)
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
   std::vector<uint64_t*> d_ns(g->sh.size(), nullptr);
   std::vector<cudaEvent_t> reset_ev;
   if (!g->multiproc) {
@@ -905,11 +979,11 @@ int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round) {
       p.peer_slots[j] = g->multiproc ? s.peer[j] : g->sh[j].d_slots;
     p.slot_stride = g->slot_stride;
     p.bstride = (uint32_t)g->bstride;
+    p.nrep = g->nrep;
     p.exch_base = g->exch_base;
     p.info = s.d_info;
     p.timeout_ns = g->opt.timeout_ms * 1000000ull;
-    fn<<<s.G, 32, 0, s.stream>>>(p, rounds, d_ns[i]);
-    CK(cudaGetLastError());
+    CK(launch_kernel(g, s, (void*)fn, 1, p, &rounds, 1, d_ns[i]));
   }
   double worst = 0;
   uint64_t last = 0;

@@ -97,8 +97,12 @@ def random_tie_graph(rng, n, wmax, density, directed):
     return adj
 
 
+ENGINES = ["cluster", "grid"]
+
+
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("seed", range(6))
-def test_tie_heavy_sweep(gpu, oracle_c, seed):
+def test_tie_heavy_sweep(gpu, oracle_c, seed, engine):
     """Weights in {0..3} (zero-weight ties), random density, both directions."""
     rng = np.random.default_rng(1000 + seed)
     with_graphs = 0
@@ -108,7 +112,8 @@ def test_tie_heavy_sweep(gpu, oracle_c, seed):
         adj = random_tie_graph(rng, n, 3, float(rng.choice([0.01, 0.05, 0.2, 0.6, 1.0])), directed)
         g = gpu.Graph(n, directed, adj)
         s = int(rng.integers(0, n))
-        r = gpu.dijkstra(g, s)
+        with gpu.DeviceGraph(g, engine=engine) as dg:
+            r = dg.solve(s)
         d, p = serial(oracle_c, g, s)
         assert_same(r, d, p, f"seed={seed} i={i} n={n}")
         with_graphs += 1
@@ -146,17 +151,18 @@ def test_config1_n1000(gpu, oracle_c, kind):
     assert oracle_c.validate(g.adj, g.n, 0, r.dist, r.pred) == 0
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("flags", [0, 1, 2, 3])
-def test_prefetch_flags_are_semantic_noops(gpu, oracle_c, flags):
+def test_prefetch_flags_are_semantic_noops(gpu, oracle_c, flags, engine):
     g = gpu.generate_dense(3000, 7)
     d, p = serial(oracle_c, g, 5)
-    with gpu.DeviceGraph(g, flags=flags) as dg:
+    with gpu.DeviceGraph(g, flags=flags, engine=engine) as dg:
         assert_same(dg.solve(5), d, p, f"flags={flags}")
 
 
 @pytest.mark.parametrize("n", [2, 31, 127, 128, 129, 255, 4095, 4097, 9000])
 @pytest.mark.parametrize("ctas", [0, 1, 3, 7])
-def test_layout_edges(gpu, oracle_c, n, ctas):
+def test_layout_edges_grid(gpu, oracle_c, n, ctas):
     """n around the 128-column CTA slice and odd CTA counts (padding columns)."""
     rng = np.random.default_rng(n * 31 + ctas)
     adj = random_tie_graph(rng, n, 2, min(1.0, 8.0 / n + 0.01), False)
@@ -164,12 +170,31 @@ def test_layout_edges(gpu, oracle_c, n, ctas):
     s = int(rng.integers(0, n))
     d, p = serial(oracle_c, g, s)
     try:
-        dg = gpu.DeviceGraph(g, ctas=ctas)
+        dg = gpu.DeviceGraph(g, ctas=ctas, engine="grid")
     except gpu.SsspError as e:  # too many columns for that few CTAs
         assert ctas and n > ctas * 2048, str(e)
         return
     with dg:
         assert_same(dg.solve(s), d, p, f"n={n} ctas={ctas}")
+
+
+@pytest.mark.parametrize("n", [2, 127, 1025, 4097, 9000, 17000])
+@pytest.mark.parametrize("ctas,warps", [(0, 4), (0, 8), (0, 16), (1, 8), (3, 4), (16, 16)])
+def test_layout_edges_cluster(gpu, oracle_c, n, ctas, warps):
+    """cluster sizes 1..16, 4/8/16 warps, padding participants and columns."""
+    rng = np.random.default_rng(n * 7 + ctas + warps)
+    adj = random_tie_graph(rng, n, 2, min(1.0, 8.0 / n + 0.01), True)
+    g = gpu.Graph(n, True, adj)
+    s = int(rng.integers(0, n))
+    d, p = serial(oracle_c, g, s)
+    try:
+        dg = gpu.DeviceGraph(g, ctas=ctas, warps=warps, engine="cluster")
+    except gpu.SsspError as e:  # cluster sizes are powers of two (Q = C*NW)
+        cmax = 1 << (ctas.bit_length() - 1) if ctas else 16
+        assert n > cmax * warps * 32 * 32, str(e)
+        return
+    with dg:
+        assert_same(dg.solve(s), d, p, f"n={n} ctas={ctas} warps={warps}")
 
 
 @pytest.mark.parametrize("wmax,wbytes", [(254, 1), (255, 2), (40000, 2), (65534, 2),
@@ -212,15 +237,17 @@ def test_weight_range_errors_are_loud(gpu):
         gpu.DeviceGraph(g)
 
 
+@pytest.mark.parametrize("engine", ENGINES)
 @pytest.mark.parametrize("P", [2, 3, 4, 8])
-def test_logical_shards_bit_identical(gpu, oracle_c, P):
+def test_logical_shards_bit_identical(gpu, oracle_c, P, engine):
     """P column shards on one GPU run the multi-GPU exchange protocol (peer
     stores into every shard's array); result == serial (test_partitioned.cpp
     :149-165, 184-196)."""
     for n, seed in [(1000, 3), (2049, 4)]:
         g = gpu.generate_sparse(n, seed) if seed % 2 else gpu.generate_dense(n, seed)
         d, p = serial(oracle_c, g, 7)
-        r = gpu.dijkstra_partitioned(g, 7, P)
+        with gpu.DeviceGraph(g, [0] * P, engine=engine) as dg:
+            r = dg.solve(7)
         assert_same(r, d, p, f"P={P} n={n}")
 
 
@@ -231,10 +258,11 @@ def test_shards_p_greater_than_n(gpu, oracle_c):
     assert_same(gpu.dijkstra_partitioned(g, 0, 7), d, p, "p>n")
 
 
-def test_batch_sources(gpu, oracle_c):
+@pytest.mark.parametrize("engine", ENGINES)
+def test_batch_sources(gpu, oracle_c, engine):
     g = gpu.generate_dense(2000, 11)
     sources = list(range(0, 2000, 31))
-    with gpu.DeviceGraph(g) as dg:
+    with gpu.DeviceGraph(g, engine=engine) as dg:
         res = dg.solve_batch(sources)
     for s, r in zip(sources, res):
         d, p = serial(oracle_c, g, s)
@@ -269,12 +297,26 @@ def test_config2_n16384_bernoulli(gpu, oracle_c):
     assert_same(r, d, p, "config2")
 
 
-def test_config3_n32768_dense(gpu, oracle_c):
-    """BASELINE config 3 on one GPU: generate_dense(32768, 32768), s=0."""
+@pytest.fixture(scope="module")
+def config3(gpu, oracle_c):
     g = gpu.generate_dense(32768, 32768)
-    with gpu.DeviceGraph(g) as dg:
+    d, p = serial(oracle_c, g, 0)
+    return g, d, p
+
+
+@pytest.mark.parametrize("engine", ENGINES)
+def test_config3_n32768_dense(gpu, config3, engine):
+    """BASELINE config 3 on one GPU: generate_dense(32768, 32768), s=0."""
+    g, d, p = config3
+    with gpu.DeviceGraph(g, engine=engine) as dg:
         r = dg.solve(0)
         st = r.stats
-    d, p = serial(oracle_c, g, 0)
     assert_same(r, d, p, "config3")
     assert st["iterations"] == 32768 and st["weight_bytes"] == 1
+
+
+def test_config3_two_logical_shards(gpu, config3):
+    """Config 3 column-partitioned over 2 shards (cluster engine, P2P mailbox)."""
+    g, d, p = config3
+    with gpu.DeviceGraph(g, [0, 0]) as dg:
+        assert_same(dg.solve(0), d, p, "config3 P=2")
