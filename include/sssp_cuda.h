@@ -65,10 +65,10 @@ typedef struct {
   uint64_t timeout_ms;    /* exchange watchdog (0 = 60000) */
   int record_visit_order; /* 1: keep the elected vertex of every round */
   uint32_t replicas;      /* grid engine: copies of the L2 exchange array (0 = 1) */
-  uint32_t warps_per_cta; /* cluster engine: 4, 8 or 16 (0 = 8) */
+  uint32_t warps_per_cta; /* cluster engine: 4, 8 or 16 (0 = 4) */
 } sssp_options;
 
-#define SSSP_FLAGS_DEFAULT 3u
+#define SSSP_FLAGS_DEFAULT 3u /* bit2 (4): speculative relax, off by default */
 
 /* Per-solve statistics; phases mirror the reference's data-parallel timing
  * scope {transfer_in, rounds, transfer_out} (bench.hpp:50-51). */

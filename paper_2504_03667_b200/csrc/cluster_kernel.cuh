@@ -101,7 +101,6 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
   const uint32_t vmask_all = (p.vbits >= 32) ? 0xFFFFFFFFu : ((1u << p.vbits) - 1u);
   const bool multi = p.nshards > 1;
   const W* const adj = static_cast<const W*>(p.adj) + (size_t)q * L;
-  const uint32_t row_bytes = (uint32_t)(p.row_stride * sizeof(W));
   const bool pf_reg = (p.flags & kFlagPrefetchReg) != 0;
   const bool pf_l2 = (p.flags & kFlagPrefetchL2) != 0;
   uint32_t* const pred = s_pred + warp * L;
@@ -135,7 +134,7 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
   uint32_t u = source, du = 0;
   uint64_t E = p.exch_base;
   uint64_t iters = 0, mispredicts = 0;
-  uint32_t pred_u = 0xFFFFFFFFu, last_l2 = 0xFFFFFFFFu;
+  uint32_t pred_u = 0xFFFFFFFFu;
   Row cur, nxt;
   cur.load(adj + (size_t)u * p.row_stride, lane);
   uint64_t ks[2 * NP];
@@ -146,137 +145,32 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
   bool failed = false;
   const uint32_t keys_base = (uint32_t)__cvta_generic_to_shared(&s_keys[0][0]);
 
-  while (true) {
-    // ---- the owner of u marks it visited and records its final distance
-    {
-      const uint32_t ul = u - p.col_base;
-      if (u >= p.col_base && ul < p.loc_n && (ul & (Q - 1)) == q) {
-        const uint32_t su = ul >> qbits;
-        if ((uint32_t)lane == ((su / Row::VEC) & 31u)) {
-          const uint32_t eu = (su / (32u * Row::VEC)) * Row::VEC + su % Row::VEC;
+  // Polls round E's keys (own smem), then with P > 1 exchanges the cluster
+  // minimum through the P2P mailbox.  Returns false if the watchdog fired.
+  auto gather = [&](uint32_t buf, uint64_t want) -> bool {
+    const uint32_t arr = keys_base + buf * QMAX * 8u;
+    const uint32_t want32 = (uint32_t)want;
+    const uint32_t tm32 = (uint32_t)tagmask;
+    uint32_t polls = 0;
+    while (true) {
+      bool ok = true;
 #pragma unroll
-          for (int e = 0; e < EPL; ++e)
-            if ((uint32_t)e == eu) {
-              if constexpr (PACKED) ek[e] = 0u;
-              else vis |= (1ull << e);
-            }
-          dout[ul] = du;
+      for (int j = 0; j < NP; ++j) {
+        const uint32_t i = 2u * lane + 64u * j;
+        if (i < Q) {  // Q is even (NW >= 4)
+          uint64_t hi;
+          const uint64_t lo = ld_smem_pair(arr + i * 8u, hi);
+          ks[2 * j] = lo;
+          ks[2 * j + 1] = hi;
+          ok &= (((uint32_t)lo & tm32) == want32) & (((uint32_t)hi & tm32) == want32);
+        } else {
+          ks[2 * j] = ks[2 * j + 1] = ~0ull;
         }
       }
+      if (__all_sync(0xFFFFFFFFu, ok)) break;
+      if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) return false;
     }
-    // ---- relax row u (serial.hpp:51-60; strict '<' keeps the earliest parent)
-    if constexpr (PACKED) {
-      const uint32_t dus1 = (du << SB) + 1u + lbase;
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) {
-        const uint32_t w = cur.elem(e);
-        const uint32_t nk = w * L + dus1 + (Row::slot(e, 0));
-        if (w != WINF && nk < ek[e]) {
-          ek[e] = nk;
-          pred[Row::slot(e, 0) | lbase] = u;
-        }
-      }
-    } else {
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) {
-        const uint32_t w = cur.elem(e);
-        const uint32_t nd = du + w;
-        if (w != WINF && nd < d[e] && !((vis >> e) & 1ull)) {
-          d[e] = nd;
-          pred[Row::slot(e, 0) | lbase] = u;
-        }
-      }
-    }
-    ++iters;
-    if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
-      p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
-
-    // ---- warp election (serial.hpp:42-48)
-    uint32_t bd, bs;
-    if constexpr (PACKED) {
-      uint32_t k = 0xFFFFFFFFu;
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) k = min(k, ek[e] - 1u);
-      k = __reduce_min_sync(0xFFFFFFFFu, k);
-      const bool none = k >= 0xFFFFFFFEu || (k >> SB) == (DINF >> SB);
-      bd = none ? DINF : (k >> SB);
-      bs = k & (L - 1u);
-    } else {
-      bd = DINF;
-      bs = 0xFFFFFFFFu;
-#pragma unroll
-      for (int e = 0; e < EPL; ++e) {
-        const bool live = !((vis >> e) & 1ull) && d[e] != DINF;
-        if (live && d[e] < bd) {
-          bd = d[e];
-          bs = Row::slot(e, lane);
-        }
-      }
-      warp_lexmin(bd, bs);
-    }
-    const uint32_t bv = (bd == DINF) ? vmask_all : (p.col_base + ((bs << qbits) | q));
-
-    // ---- publish into every CTA's exchange array (DSMEM)
-    ++E;
-    const uint32_t buf = (uint32_t)(E & 1ull);
-    const uint64_t want = E & tagmask;
-    const uint64_t key = ((uint64_t)bd << 32) | ((uint64_t)(bv & vmask_all) << tb) | want;
-    const uint32_t my_slot_addr = keys_base + (buf * QMAX + q) * 8u;
-    if ((uint32_t)lane < csize) st_dsmem(my_slot_addr, (uint32_t)lane, key);
-
-    // ---- off the critical path: L2 prefetch of my new local best's row, and
-    // the runner-up of the previous round's keys into registers.
-    if (pf_l2 && bd != DINF && bv != last_l2) {
-      if (lane == 0)
-        prefetch_l2_bulk(static_cast<const W*>(p.adj) + (size_t)bv * p.row_stride, row_bytes);
-      last_l2 = bv;
-    }
-    if (pf_reg) {
-      uint64_t r = ~0ull;
-#pragma unroll
-      for (int j = 0; j < 2 * NP; ++j) r = (ks[j] != best_key && ks[j] < r) ? ks[j] : r;
-      uint32_t a = (uint32_t)(r >> 32), b = (uint32_t)r;
-      warp_lexmin(a, b);
-      if (a != DINF && iters > 1) {
-        pred_u = b >> tb;
-        nxt.load(adj + (size_t)pred_u * p.row_stride, lane);
-      } else {
-        pred_u = 0xFFFFFFFFu;
-      }
-    }
-
-    // ---- gather from my own shared memory
-    {
-      const uint32_t arr = keys_base + buf * QMAX * 8u;
-      const uint32_t want32 = (uint32_t)want;
-      const uint32_t tm32 = (uint32_t)tagmask;
-      uint32_t polls = 0;
-      while (true) {
-        bool ok = true;
-#pragma unroll
-        for (int j = 0; j < NP; ++j) {
-          const uint32_t i = 2u * lane + 64u * j;
-          if (i < Q) {  // Q is even (NW >= 4)
-            uint64_t hi;
-            const uint64_t lo = ld_smem_pair(arr + i * 8u, hi);
-            ks[2 * j] = lo;
-            ks[2 * j + 1] = hi;
-            ok &= (((uint32_t)lo & tm32) == want32) & (((uint32_t)hi & tm32) == want32);
-          } else {
-            ks[2 * j] = ks[2 * j + 1] = ~0ull;
-          }
-        }
-        if (__all_sync(0xFFFFFFFFu, ok)) break;
-        if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) {
-          failed = true;
-          break;
-        }
-      }
-    }
-    if (failed) break;
     best_key = min_key<NP>(ks);
-
-    // ---- P > 1: exchange the cluster minimum between shards (P2P mailbox)
     if (multi) {
       if (q == 0 && (uint32_t)lane < p.nshards)
         st_slot(p.peer_slots[lane] + (uint64_t)solve * p.slot_stride + (uint64_t)buf * p.bstride +
@@ -284,30 +178,302 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
                 best_key, true);
       const uint64_t* mb = p.slots + (uint64_t)solve * p.slot_stride + (uint64_t)buf * p.bstride;
       uint64_t mk = ~0ull;
-      uint32_t polls = 0;
+      uint32_t polls2 = 0;
       while (true) {
         mk = (uint32_t)lane < p.nshards ? ld_slot(mb + lane, true) : ~0ull;
         const bool ok = (uint32_t)lane >= p.nshards || (mk & tagmask) == want;
         if (__all_sync(0xFFFFFFFFu, ok)) break;
-        if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) {
-          failed = true;
-          break;
-        }
+        if ((++polls2 & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) return false;
       }
-      if (failed) break;
       uint32_t a = (uint32_t)(mk >> 32), b = (uint32_t)mk;
       warp_lexmin(a, b);
       best_key = ((uint64_t)a << 32) | b;
     }
+    return true;
+  };
 
-    du = (uint32_t)(best_key >> 32);
-    if (du == DINF) break;
-    u = (uint32_t)(best_key & 0xFFFFFFFFull) >> tb;
-    if (pf_reg && u == pred_u) {
-      cur = nxt;
-    } else {
-      if (pf_reg) ++mispredicts;
-      cur.load(adj + (size_t)u * p.row_stride, lane);
+  // smallest gathered key strictly greater than `after` (keys are unique)
+  auto next_key = [&](uint64_t after) -> uint64_t {
+    uint64_t r = ~0ull;
+#pragma unroll
+    for (int j = 0; j < 2 * NP; ++j) r = (ks[j] > after && ks[j] < r) ? ks[j] : r;
+    uint32_t a = (uint32_t)(r >> 32), b = (uint32_t)r;
+    warp_lexmin(a, b);
+    return ((uint64_t)a << 32) | b;
+  };
+  // L2-prefetch this warp's slice of a row that is needed two rounds ahead
+  auto prefetch_slice = [&](uint32_t v) {
+    const uint8_t* b = reinterpret_cast<const uint8_t*>(adj + (size_t)v * p.row_stride);
+#pragma unroll
+    for (int k = 0; k < Row::NCH; ++k)
+      asm volatile("prefetch.global.L2 [%0];" ::"l"(b + (size_t)(k * 32 + lane) * Row::CB));
+  };
+
+  if (PACKED && (p.flags & kFlagSpeculate)) {
+    // Speculative loop.  While round E's exchange is in flight, each warp
+    // already relaxes the row of the PREDICTED winner of round E (the
+    // runner-up of round E-1) into a shadow state eks[] and
+    // elects from it.  When round E resolves to exactly that (vertex, dist),
+    // the shadow state is committed and the precomputed key is published at
+    // once, so the relax + election cost hides behind the exchange latency;
+    // otherwise the round is recomputed from the committed state.  Results
+    // are identical either way.
+    uint32_t eks[EPL];
+    uint32_t spec_u = 0xFFFFFFFFu, spec_du = 0, spec_bd = DINF, spec_bv = vmask_all;
+    uint64_t spec_pm = 0;  // columns the speculative relax improved
+    // two-slot row ring: the row for this round's speculation, and the row of
+    // the vertex predicted two rounds ahead (third-best key), in flight
+    Row ra = cur, rb;
+    uint32_t ra_u = u, rb_u = 0xFFFFFFFFu;
+
+    auto owner_of = [&](uint32_t v, uint32_t& ul) -> bool {
+      ul = v - p.col_base;
+      return v >= p.col_base && ul < p.loc_n && (ul & (Q - 1)) == q;
+    };
+    // zero the element of `arr` holding local column ul (owner warp only)
+    auto mark = [&](uint32_t (&arr)[EPL], uint32_t ul) -> bool {
+      const uint32_t su = ul >> qbits;
+      if ((uint32_t)lane != ((su / Row::VEC) & 31u)) return false;
+      const uint32_t eu = (su / (32u * Row::VEC)) * Row::VEC + su % Row::VEC;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e)
+        if ((uint32_t)e == eu) arr[e] = 0u;
+      return true;
+    };
+    auto elect = [&](const uint32_t (&arr)[EPL], uint32_t& bd, uint32_t& bv) {
+      uint32_t k = 0xFFFFFFFFu;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) k = min(k, arr[e] - 1u);
+      k = __reduce_min_sync(0xFFFFFFFFu, k);
+      const bool none = k >= 0xFFFFFFFEu || (k >> SB) == (DINF >> SB);
+      bd = none ? DINF : (k >> SB);
+      bv = none ? vmask_all : (p.col_base + (((k & (L - 1u)) << qbits) | q));
+    };
+
+    // One round.  A = the slot holding the row predicted for this round's
+    // speculation (loaded one round ago), B = the slot this round loads the
+    // two-rounds-ahead row into.  The loop alternates the roles, so every
+    // load targets a fixed register set (a runtime-selected load target would
+    // force the compiler to wait for the load right away).
+    // Returns 0 = continue, 1 = solve finished, 2 = watchdog fired.
+    auto step = [&](Row& A, uint32_t& A_u, Row& B, uint32_t& B_u) -> int {
+      uint32_t bd, bv;
+      const bool hit = (u == spec_u) && (du == spec_du);
+      if (hit) {
+        bd = spec_bd;
+        bv = spec_bv;
+      } else {
+        // ---- recompute this round from the committed state
+        if (u == B_u) {
+          cur = B;
+        } else if (u == A_u) {
+          cur = A;
+        } else {
+          if (iters > 0) ++mispredicts;
+          cur.load(adj + (size_t)u * p.row_stride, lane);
+        }
+        uint32_t ul;
+        if (owner_of(u, ul) && mark(ek, ul)) dout[ul] = du;
+        const uint32_t dus1 = (du << SB) + 1u + lbase;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const uint32_t w = cur.elem(e);
+          const uint32_t nk = w * L + dus1 + (Row::slot(e, 0));
+          if (w != WINF && nk < ek[e]) {
+            ek[e] = nk;
+            pred[Row::slot(e, 0) | lbase] = u;
+          }
+        }
+        elect(ek, bd, bv);
+      }
+
+      // ---- publish (DSMEM) -- the only work between gather and publish on a hit
+      ++E;
+      const uint32_t buf = (uint32_t)(E & 1ull);
+      const uint64_t want = E & tagmask;
+      const uint64_t key = ((uint64_t)bd << 32) | ((uint64_t)(bv & vmask_all) << tb) | want;
+      if ((uint32_t)lane < csize) st_dsmem(keys_base + (buf * QMAX + q) * 8u, (uint32_t)lane, key);
+
+      // ---- commit the speculation's side effects
+      if (hit) {
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) ek[e] = eks[e];
+#pragma unroll
+        for (int e = 0; e < EPL; ++e)
+          if ((spec_pm >> e) & 1ull) pred[Row::slot(e, 0) | lbase] = u;
+        uint32_t ul;
+        if (owner_of(u, ul)) {
+          const uint32_t su = ul >> qbits;
+          if ((uint32_t)lane == ((su / Row::VEC) & 31u)) dout[ul] = du;
+        }
+      }
+      ++iters;
+      if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
+        p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
+      // ---- speculate on the next round: runner-up of the last exchange
+      spec_u = 0xFFFFFFFFu;
+      const uint64_t r2 = next_key(best_key);
+      if (pf_reg && iters > 1 && (uint32_t)(r2 >> 32) != DINF) {
+        spec_u = (uint32_t)(r2 & 0xFFFFFFFFull) >> tb;
+        spec_du = (uint32_t)(r2 >> 32);
+        if (spec_u != A_u && spec_u != B_u) {
+          ++mispredicts;
+          A.load(adj + (size_t)spec_u * p.row_stride, lane);
+          A_u = spec_u;
+        }
+        const Row sr = (spec_u == B_u) ? B : A;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) eks[e] = ek[e];
+        uint32_t ul;
+        if (owner_of(spec_u, ul)) mark(eks, ul);
+        const uint32_t dus1 = (spec_du << SB) + 1u + lbase;
+        uint64_t pm = 0;
+#pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const uint32_t w = sr.elem(e);
+          const uint32_t nk = w * L + dus1 + (Row::slot(e, 0));
+          if (w != WINF && nk < eks[e]) {
+            eks[e] = nk;
+            pm |= 1ull << e;
+          }
+        }
+        spec_pm = pm;
+        elect(eks, spec_bd, spec_bv);
+        // two rounds ahead: the third-best key's row into slot B
+        const uint64_t r3 = next_key(r2);
+        if ((uint32_t)(r3 >> 32) != DINF) {
+          const uint32_t v3 = (uint32_t)(r3 & 0xFFFFFFFFull) >> tb;
+          if (v3 != A_u && v3 != B_u && spec_u != B_u) {
+            B.load(adj + (size_t)v3 * p.row_stride, lane);
+            B_u = v3;
+          }
+        }
+      }
+
+      // ---- gather round E
+      if (!gather(buf, want)) return 2;
+      du = (uint32_t)(best_key >> 32);
+      if (du == DINF) return 1;
+      u = (uint32_t)(best_key & 0xFFFFFFFFull) >> tb;
+      return 0;
+    };
+
+    int st = 0;
+    while (st == 0) {
+      st = step(rb, rb_u, ra, ra_u);
+      if (st == 0) st = step(ra, ra_u, rb, rb_u);
+    }
+    failed = st == 2;
+  } else {
+    while (true) {
+      // ---- the owner of u marks it visited and records its final distance
+      {
+        const uint32_t ul = u - p.col_base;
+        if (u >= p.col_base && ul < p.loc_n && (ul & (Q - 1)) == q) {
+          const uint32_t su = ul >> qbits;
+          if ((uint32_t)lane == ((su / Row::VEC) & 31u)) {
+            const uint32_t eu = (su / (32u * Row::VEC)) * Row::VEC + su % Row::VEC;
+  #pragma unroll
+            for (int e = 0; e < EPL; ++e)
+              if ((uint32_t)e == eu) {
+                if constexpr (PACKED) ek[e] = 0u;
+                else vis |= (1ull << e);
+              }
+            dout[ul] = du;
+          }
+        }
+      }
+      // ---- relax row u (serial.hpp:51-60; strict '<' keeps the earliest parent)
+      if constexpr (PACKED) {
+        const uint32_t dus1 = (du << SB) + 1u + lbase;
+  #pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const uint32_t w = cur.elem(e);
+          const uint32_t nk = w * L + dus1 + (Row::slot(e, 0));
+          if (w != WINF && nk < ek[e]) {
+            ek[e] = nk;
+            pred[Row::slot(e, 0) | lbase] = u;
+          }
+        }
+      } else {
+  #pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const uint32_t w = cur.elem(e);
+          const uint32_t nd = du + w;
+          if (w != WINF && nd < d[e] && !((vis >> e) & 1ull)) {
+            d[e] = nd;
+            pred[Row::slot(e, 0) | lbase] = u;
+          }
+        }
+      }
+      ++iters;
+      if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
+        p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
+
+      // ---- warp election (serial.hpp:42-48)
+      uint32_t bd, bs;
+      if constexpr (PACKED) {
+        uint32_t k = 0xFFFFFFFFu;
+  #pragma unroll
+        for (int e = 0; e < EPL; ++e) k = min(k, ek[e] - 1u);
+        k = __reduce_min_sync(0xFFFFFFFFu, k);
+        const bool none = k >= 0xFFFFFFFEu || (k >> SB) == (DINF >> SB);
+        bd = none ? DINF : (k >> SB);
+        bs = k & (L - 1u);
+      } else {
+        bd = DINF;
+        bs = 0xFFFFFFFFu;
+  #pragma unroll
+        for (int e = 0; e < EPL; ++e) {
+          const bool live = !((vis >> e) & 1ull) && d[e] != DINF;
+          if (live && d[e] < bd) {
+            bd = d[e];
+            bs = Row::slot(e, lane);
+          }
+        }
+        warp_lexmin(bd, bs);
+      }
+      const uint32_t bv = (bd == DINF) ? vmask_all : (p.col_base + ((bs << qbits) | q));
+
+      // ---- publish into every CTA's exchange array (DSMEM)
+      ++E;
+      const uint32_t buf = (uint32_t)(E & 1ull);
+      const uint64_t want = E & tagmask;
+      const uint64_t key = ((uint64_t)bd << 32) | ((uint64_t)(bv & vmask_all) << tb) | want;
+      const uint32_t my_slot_addr = keys_base + (buf * QMAX + q) * 8u;
+      if ((uint32_t)lane < csize) st_dsmem(my_slot_addr, (uint32_t)lane, key);
+
+      // ---- off the critical path, while the exchange is in flight: the
+      // runner-up of the last exchange (the likely next winner, SURVEY.md
+      // §8d) into registers, the third-best row's slice into L2.
+      if (pf_reg) {
+        const uint64_t r2 = next_key(best_key);
+        if ((uint32_t)(r2 >> 32) != DINF && iters > 1) {
+          pred_u = (uint32_t)(r2 & 0xFFFFFFFFull) >> tb;
+          nxt.load(adj + (size_t)pred_u * p.row_stride, lane);
+          if (pf_l2) {
+            const uint64_t r3 = next_key(r2);
+            if ((uint32_t)(r3 >> 32) != DINF) prefetch_slice((uint32_t)(r3 & 0xFFFFFFFFull) >> tb);
+          }
+        } else {
+          pred_u = 0xFFFFFFFFu;
+        }
+      }
+
+      if (!gather(buf, want)) {
+        failed = true;
+        break;
+      }
+
+      du = (uint32_t)(best_key >> 32);
+      if (du == DINF) break;
+      u = (uint32_t)(best_key & 0xFFFFFFFFull) >> tb;
+      if (pf_reg && u == pred_u) {
+        cur = nxt;
+      } else {
+        if (pf_reg) ++mispredicts;
+        cur.load(adj + (size_t)u * p.row_stride, lane);
+      }
     }
   }
 

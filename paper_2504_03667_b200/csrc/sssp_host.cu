@@ -477,7 +477,7 @@ int create_shard_objects(sssp_graph* g, uint32_t P, const int* devices, uint32_t
     CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
     int rc;
     if (g->cluster) {
-      const uint32_t nw = g->opt.warps_per_cta ? g->opt.warps_per_cta : 8;
+      const uint32_t nw = g->opt.warps_per_cta ? g->opt.warps_per_cta : 4;
       if (nw != 4 && nw != 8 && nw != 16) return fail(SSSP_ERR_BAD_ARG, "warps_per_cta: 4, 8 or 16");
       rc = plan_cluster_layout(s, loc_n, gmax ? std::min<uint32_t>(gmax, 16) : 16, nw);
     } else {
