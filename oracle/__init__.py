@@ -145,6 +145,7 @@ class _Ref:
             "ref_last_error": (ctypes.c_char_p, []),
             "ref_generate_dense": (ctypes.c_int, [U64, U64, ctypes.c_int, _u64p]),
             "ref_generate_sparse_edges": (ctypes.c_int, [U64, U64, _u64p]),
+            "ref_graph_from_edges": (ctypes.c_int, [U64, _u64p, U64, ctypes.c_int, _u64p]),
             "ref_parse_edge_list": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_int, _u64p, _u64p,
                                                    U64, _u64p]),
             "ref_dijkstra_serial": (ctypes.c_int, [_u64p, U64, U64, _u64p, _u64p, _u64p, _u64p]),
@@ -170,6 +171,16 @@ class _Ref:
         if self.lib.ref_generate_sparse_edges(n, seed, _p(e)):
             raise ValueError(self.lib.ref_last_error().decode())
         return e.reshape(-1, 3)
+
+    def from_edges(self, n, edges, directed):
+        e = np.ascontiguousarray(np.asarray(edges, np.uint64).reshape(-1, 3))
+        out = np.empty(n * n, np.uint64)
+        if self.lib.ref_graph_from_edges(n, _p(e), len(e), int(directed), _p(out)):
+            raise ValueError(self.lib.ref_last_error().decode())
+        return out
+
+    def sparse(self, n, seed, directed=False):
+        return self.from_edges(n, self.sparse_edges(n, seed), directed)
 
     def parse(self, text, directed, cap=1 << 20):
         n = ctypes.c_uint64()

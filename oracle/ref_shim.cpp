@@ -73,6 +73,23 @@ int ref_generate_sparse_edges(std::uint64_t n, std::uint64_t seed, std::uint64_t
   }
 }
 
+// graph.hpp:73-88 (graph_from_edges) over m (u, v, w) triples
+int ref_graph_from_edges(std::uint64_t n, const std::uint64_t* edges, std::uint64_t m,
+                         int directed, std::uint64_t* adj) {
+  try {
+    sssp::EdgeList el;
+    el.n = n;
+    for (std::uint64_t i = 0; i < m; ++i)
+      el.edges.push_back({edges[3 * i], edges[3 * i + 1], edges[3 * i + 2]});
+    const sssp::Graph g = sssp::graph_from_edges(el, directed != 0);
+    std::memcpy(adj, g.adj.data(), n * n * sizeof(std::uint64_t));
+    return RS_OK;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return RS_BAD_ARG;
+  }
+}
+
 // graph.hpp:172-174 (parse_edge_list, the '-w' switch is `directed`).
 // On success *n_out is set and adj (capacity adj_cap cells) is filled when
 // n*n <= adj_cap; returns RS_ERR with *line_out set on ParseError.
