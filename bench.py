@@ -175,6 +175,8 @@ def main():
     ap.add_argument("--source", type=int, default=0)
     ap.add_argument("--flags", type=int, default=None)
     ap.add_argument("--ctas", type=int, default=0)
+    ap.add_argument("--engine", default="auto", choices=["auto", "cluster", "grid"])
+    ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ref-skip-partitioned", action="store_true")
@@ -215,14 +217,12 @@ def main():
     t_build = time.perf_counter() - t0
 
     if world == 1:
-        dg = P.DeviceGraph(g, (local_rank,), flags=args.flags, ctas=args.ctas)
+        dg = P.DeviceGraph(g, (local_rank,), flags=args.flags, ctas=args.ctas, engine=args.engine,
+                           warps=args.warps)
     else:
-        dg = P.ShardGraph(block, n, world, rank, max_weight=100, device=local_rank,
-                          flags=args.flags, ctas=args.ctas)
-        h = dg.export()
-        handles = [None] * world
-        dist.all_gather_object(handles, h)
-        dg.connect(handles)
+        from paper_2504_03667_b200 import distributed as D
+        dg = D.open_shard(block, n, max_weight=100, device=local_rank, flags=args.flags,
+                          ctas=args.ctas, engine=args.engine)
     info = dg.info()
     t_sync = dg.probe_sync(rounds=min(n, 20000))
 

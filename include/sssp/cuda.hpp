@@ -1,0 +1,147 @@
+// sssp/cuda.hpp -- C++ drop-in for the reference's solve entry points.
+//
+// Add this header next to the reference's proj/include/sssp/*.hpp and link
+// libsssp_cuda.so.  It keeps the reference's own types (sssp::Graph,
+// graph.hpp:33-58; sssp::ShortestPathResult, result.hpp:13-19; VertexId,
+// weight.hpp:9-21) and its error behaviour:
+//
+//   reference                                        drop-in (B200)
+//   dijkstra_serial(g, s)            serial.hpp:65   sssp::cuda::dijkstra(g, s)
+//   dijkstra_serial(g, s, c, &vo)    serial.hpp:26   sssp::cuda::dijkstra(g, s, &vo)
+//   dijkstra_partitioned(g, s, p)    partitioned:184 sssp::cuda::dijkstra_partitioned(g, s, devices)
+//   (repeated solves on one graph)                   sssp::cuda::DeviceGraph
+//
+// Results are bit-identical to dijkstra_serial (dist AND pred), so
+// `sssp::cuda::dijkstra(g, s) == sssp::dijkstra_serial(g, s)` holds.
+// source >= n throws std::invalid_argument (serial.hpp:30); every other
+// failure throws std::runtime_error -- there is no CPU fallback.
+#pragma once
+
+#include <cstdint>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "sssp/graph.hpp"
+#include "sssp/result.hpp"
+#include "sssp/weight.hpp"
+#include "sssp_cuda.h"
+
+namespace sssp::cuda {
+
+// Mirrors DataParallelRun's timing scope {transfer_in, rounds, transfer_out}
+// (dataparallel.hpp:284-296, bench.hpp:50-51).
+struct Phases {
+  double transfer_in_s = 0;
+  double rounds_s = 0;
+  double transfer_out_s = 0;
+};
+
+struct CudaRun {
+  ShortestPathResult result;
+  Phases phases;
+  std::size_t iterations = 0;  // elections executed (vertices reached)
+  sssp_solve_stats stats{};
+};
+
+inline void check(int rc, const char* where) {
+  if (rc == SSSP_OK) return;
+  const std::string msg = std::string(where) + ": " + sssp_status_string(rc) + " (" +
+                          sssp_last_error() + ")";
+  if (rc == SSSP_ERR_BAD_SOURCE) throw std::invalid_argument(msg);
+  throw std::runtime_error(msg);
+}
+
+// A Graph resident in HBM; one GPU, or several column shards (one per entry of
+// `devices`, partition.hpp:31-41).  Not safe for concurrent solves.
+class DeviceGraph {
+ public:
+  explicit DeviceGraph(const Graph& g, std::vector<int> devices = {0},
+                       const sssp_options* opt = nullptr)
+      : n_(g.n) {
+    static_assert(sizeof(Weight) == sizeof(std::uint64_t), "Weight is uint64 (weight.hpp:9)");
+    check(sssp_graph_create(g.adj.data(), g.n, g.directed ? 1 : 0, devices.data(),
+                            static_cast<int>(devices.size()), opt, &h_),
+          "sssp_graph_create");
+  }
+  DeviceGraph(const DeviceGraph&) = delete;
+  DeviceGraph& operator=(const DeviceGraph&) = delete;
+  DeviceGraph(DeviceGraph&& o) noexcept : h_(std::exchange(o.h_, nullptr)), n_(o.n_) {}
+  ~DeviceGraph() {
+    if (h_) sssp_graph_destroy(h_);
+  }
+
+  CudaRun run(VertexId source, std::vector<VertexId>* visit_order = nullptr) {
+    if (source >= n_) throw std::invalid_argument("dijkstra: source out of range");
+    CudaRun r;
+    r.result.source = source;
+    r.result.dist.resize(n_);
+    r.result.pred.resize(n_);
+    std::vector<std::uint64_t> vo(visit_order ? n_ : 0);
+    static_assert(sizeof(VertexId) == sizeof(std::uint64_t), "VertexId is 64-bit (LP64)");
+    check(sssp_solve(h_, source, r.result.dist.data(),
+                     reinterpret_cast<std::uint64_t*>(r.result.pred.data()),
+                     visit_order ? vo.data() : nullptr, &r.stats),
+          "sssp_solve");
+    r.phases = {r.stats.transfer_in_s, r.stats.rounds_s, r.stats.transfer_out_s};
+    r.iterations = r.stats.iterations;
+    if (visit_order) visit_order->assign(vo.begin(), vo.begin() + r.stats.iterations);
+    return r;
+  }
+
+  ShortestPathResult solve(VertexId source) { return run(source).result; }
+
+  std::vector<ShortestPathResult> solve_batch(const std::vector<VertexId>& sources) {
+    for (VertexId s : sources)
+      if (s >= n_) throw std::invalid_argument("dijkstra: source out of range");
+    std::vector<std::uint64_t> src(sources.begin(), sources.end());
+    std::vector<std::uint64_t> dist(src.size() * n_), pred(src.size() * n_);
+    check(sssp_solve_batch(h_, src.data(), static_cast<std::uint32_t>(src.size()), dist.data(),
+                           pred.data(), nullptr),
+          "sssp_solve_batch");
+    std::vector<ShortestPathResult> out(src.size());
+    for (std::size_t i = 0; i < src.size(); ++i) {
+      out[i].source = sources[i];
+      out[i].dist.assign(dist.begin() + i * n_, dist.begin() + (i + 1) * n_);
+      out[i].pred.assign(pred.begin() + i * n_, pred.begin() + (i + 1) * n_);
+    }
+    return out;
+  }
+
+  sssp_graph* handle() const { return h_; }
+
+ private:
+  sssp_graph* h_ = nullptr;
+  std::size_t n_ = 0;
+};
+
+// Drop-in for dijkstra_serial(g, source) (serial.hpp:65-68).
+inline ShortestPathResult dijkstra(const Graph& g, VertexId source,
+                                   std::vector<VertexId>* visit_order = nullptr) {
+  if (source >= g.n) throw std::invalid_argument("dijkstra: source out of range");
+  sssp_options opt{};
+  opt.flags = SSSP_FLAGS_DEFAULT;
+  opt.record_visit_order = visit_order ? 1 : 0;
+  DeviceGraph dg(g, {0}, &opt);
+  return dg.run(source, visit_order).result;
+}
+
+// The same solve with the phase timings of the data-parallel scope.
+inline CudaRun dijkstra_run(const Graph& g, VertexId source) {
+  if (source >= g.n) throw std::invalid_argument("dijkstra: source out of range");
+  DeviceGraph dg(g);
+  return dg.run(source);
+}
+
+// Column-partitioned over one shard per device (partitioned.hpp:184-225);
+// repeat a device id to run several shards on one GPU.
+inline ShortestPathResult dijkstra_partitioned(const Graph& g, VertexId source,
+                                               std::vector<int> devices) {
+  if (devices.empty()) throw std::invalid_argument("dijkstra_partitioned: p >= 1");
+  if (source >= g.n) throw std::invalid_argument("dijkstra_partitioned: source out of range");
+  DeviceGraph dg(g, std::move(devices));
+  return dg.solve(source);
+}
+
+}  // namespace sssp::cuda

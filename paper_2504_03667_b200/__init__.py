@@ -323,9 +323,10 @@ class ShardGraph(DeviceGraph):
 
     def __init__(self, block: np.ndarray, n: int, world: int, rank: int, max_weight: int,
                  device: int = 0, *, flags: Optional[int] = None, ctas: int = 0,
-                 timeout_ms: int = 0, replicas: int = 0, engine: str = "auto", warps: int = 0):
+                 timeout_ms: int = 0, replicas: int = 0, engine: str = "auto", warps: int = 0,
+                 max_batch: int = 1):
         self.n = n
-        self._opt = _options(flags, ctas, 1, timeout_ms, False, replicas, engine, warps)
+        self._opt = _options(flags, ctas, max_batch, timeout_ms, False, replicas, engine, warps)
         blk = np.ascontiguousarray(block, dtype=np.uint64)
         ld = blk.shape[1] if blk.ndim == 2 else max(1, blk.size // max(1, n))
         h = ctypes.c_void_p()

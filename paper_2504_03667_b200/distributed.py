@@ -1,0 +1,70 @@
+"""One process per GPU: the host side of the column-partitioned solve.
+
+The reference's dijkstra_partitioned (partitioned.hpp:184-225) scatters column
+blocks to p workers, runs padded_n rounds of local_min -> allreduce_minloc ->
+relax_owned, then gathers.  Here each torchrun rank owns one shard on its own
+GPU; the per-round allreduce_minloc runs INSIDE the persistent kernels as P2P
+stores into every rank's mailbox (CUDA IPC handles exchanged once through
+torch.distributed), so the only host collectives are the one-time handle
+exchange and the final gather of owned dist/pred slices.
+"""
+from __future__ import annotations
+
+from typing import Optional, Sequence
+
+import numpy as np
+
+from . import ShardGraph, ShortestPathResult, pad_vertex_count
+
+
+def shard_range(n: int, world: int, rank: int) -> tuple:
+    """Real columns [begin, begin+count) of shard `rank` (partition.hpp:31-41;
+    padding columns beyond n are owned but never materialised)."""
+    loc_n = pad_vertex_count(n, world) // world
+    begin = rank * loc_n
+    return begin, max(0, min(loc_n, n - begin))
+
+
+def exchange_handles(handle: bytes, group=None) -> list:
+    """All-gathers every rank's exchange-buffer IPC handle, in rank order."""
+    import torch.distributed as dist
+    out = [None] * dist.get_world_size(group)
+    dist.all_gather_object(out, handle, group=group)
+    return out
+
+
+def gather_result(source: int, n: int, local_dist: np.ndarray, local_pred: np.ndarray,
+                  group=None) -> ShortestPathResult:
+    """Reassembles the owned slices of every rank (partitioned.hpp:208-223)."""
+    import torch.distributed as dist
+    world = dist.get_world_size(group)
+    parts = [None] * world
+    dist.all_gather_object(parts, (dist.get_rank(group), local_dist.tobytes(), local_pred.tobytes()),
+                           group=group)
+    dist_out = np.empty(n, np.uint64)
+    pred_out = np.empty(n, np.uint64)
+    for r, db, pb in parts:
+        b, c = shard_range(n, world, r)
+        dist_out[b:b + c] = np.frombuffer(db, np.uint64)
+        pred_out[b:b + c] = np.frombuffer(pb, np.uint64)
+    return ShortestPathResult(source, dist_out, pred_out)
+
+
+def open_shard(block: np.ndarray, n: int, max_weight: int, device: int, group=None,
+               **kw) -> ShardGraph:
+    """Creates this rank's shard from its column block and connects it to the
+    other ranks' shards."""
+    import torch.distributed as dist
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    sg = ShardGraph(block, n, world, rank, max_weight, device, **kw)
+    sg.connect(exchange_handles(sg.export(), group))
+    return sg
+
+
+def dijkstra_distributed(block: np.ndarray, n: int, source: int, max_weight: int, device: int,
+                         group=None, **kw) -> ShortestPathResult:
+    """Collective: every rank passes its n x count column block (shard_range)
+    and receives the full ShortestPathResult."""
+    with open_shard(block, n, max_weight, device, group, **kw) as sg:
+        r = sg.solve(source)
+    return gather_result(source, n, r.dist, r.pred, group)

@@ -320,3 +320,17 @@ def test_config3_two_logical_shards(gpu, config3):
     g, d, p = config3
     with gpu.DeviceGraph(g, [0, 0]) as dg:
         assert_same(dg.solve(0), d, p, "config3 P=2")
+
+
+def test_cpp_dropin_against_reference_binary(gpu):
+    """include/sssp/cuda.hpp compiled with the reference headers
+    (oracle/_ref/test_dropin): cuda::dijkstra(g,s) == dijkstra_serial(g,s)."""
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref",
+                       "test_dropin")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/test_dropin not built (needs /root/reference at build time)")
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr
+    assert "PASS" in out.stdout
