@@ -47,12 +47,17 @@ typedef enum {
   SSSP_ERR_UNSUPPORTED = 8   /* configuration not supported on this device */
 } sssp_status;
 
-/* How the n-round persistent scan kernel exchanges each round's election.
- * Both are bit-identical to dijkstra_serial; they differ in latency. */
+/* Solve engines -- all bit-identical to dijkstra_serial.
+ * GRID / CLUSTER run the reference's n rounds in one persistent kernel and
+ * differ in how a round's election is exchanged.  BUCKET settles a whole
+ * distance class per step and is exact only when every finite off-diagonal
+ * weight is >= 1; AUTO picks BUCKET when that holds (single shard), else
+ * CLUSTER. */
 typedef enum {
-  SSSP_ENGINE_AUTO = 0,    /* = CLUSTER */
+  SSSP_ENGINE_AUTO = 0,
   SSSP_ENGINE_GRID = 1,    /* single-warp CTAs across the GPU, exchange through L2 */
-  SSSP_ENGINE_CLUSTER = 2  /* one thread-block cluster per solve, exchange through DSMEM */
+  SSSP_ENGINE_CLUSTER = 2, /* one thread-block cluster per solve, exchange through DSMEM */
+  SSSP_ENGINE_BUCKET = 3   /* distance-class steps, push/pull over B200 HBM */
 } sssp_engine;
 
 typedef struct {
@@ -76,7 +81,7 @@ typedef struct {
   double transfer_in_s;   /* graph upload (narrow + permute + H2D) of the handle */
   double rounds_s;        /* kernel time, CUDA events on the launch stream */
   double transfer_out_s;  /* D2H of dist/pred */
-  uint64_t iterations;    /* elections executed (= vertices reached) */
+  uint64_t iterations;    /* vertices settled (= elections executed / vertices reached) */
   uint64_t relax_checks;  /* iterations * columns scanned (OpCounters analogue) */
   uint64_t mispredicts;   /* rounds whose row was not prefetched */
   uint64_t matrix_bytes;  /* device bytes of the stored matrix (all local shards) */
@@ -84,6 +89,9 @@ typedef struct {
   uint32_t ctas;          /* CTAs per solve per shard */
   uint32_t shards;        /* P */
   uint32_t packed_key;    /* 1 if the single-redux packed local key is in use */
+  uint32_t engine;        /* sssp_engine that ran */
+  uint32_t classes;       /* BUCKET: distance classes (steps) */
+  uint64_t rows_read;     /* matrix rows streamed (scan: = iterations) */
 } sssp_solve_stats;
 
 typedef struct sssp_graph sssp_graph;

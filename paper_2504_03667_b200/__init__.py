@@ -204,7 +204,7 @@ def generate_bernoulli(n: int, p: float, seed: int, directed: bool = False,
     return Graph(n, directed, out) if cols is None else out.reshape(n, cols[1])
 
 
-ENGINES = {"auto": 0, "grid": 1, "cluster": 2}
+ENGINES = {"auto": 0, "grid": 1, "cluster": 2, "bucket": 3}
 
 
 def _options(flags: Optional[int], ctas: int, max_batch: int, timeout_ms: int,

@@ -60,6 +60,9 @@ class Stats(ctypes.Structure):
         ("ctas", ctypes.c_uint32),
         ("shards", ctypes.c_uint32),
         ("packed_key", ctypes.c_uint32),
+        ("engine", ctypes.c_uint32),
+        ("classes", ctypes.c_uint32),
+        ("rows_read", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:

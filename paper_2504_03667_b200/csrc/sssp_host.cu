@@ -17,6 +17,7 @@
 #include <vector>
 
 #include "../../include/sssp_cuda.h"
+#include "bucket_kernel.cuh"
 #include "dispatch.h"
 
 using namespace sssp_b200;
@@ -120,6 +121,12 @@ struct Shard {
   uint32_t* h_sources = nullptr;  // pinned
   uint64_t* h_info = nullptr;     // pinned
   uint64_t* peer[kMaxShards] = {};
+  // bucket engine (bucket_kernel.cuh)
+  void* d_adjT = nullptr;        // transpose in position order (nullptr: symmetric or absent)
+  const void* pull_src = nullptr;// d_adjT, or d_adj when the matrix is symmetric
+  uint32_t* d_bitmap = nullptr;  // [2][row_stride/32]
+  uint32_t* d_ctrl = nullptr;    // [8]
+  uint32_t bT = 0, bG = 0;       // positions per CTA, CTAs
   bool peer_ipc[kMaxShards] = {};
   KernelFn fn = nullptr;
 };
@@ -138,7 +145,8 @@ struct sssp_graph {
   uint32_t max_batch = 1;
   uint64_t slot_stride = 0, bstride = 0;
   uint32_t nrep = 1;
-  bool cluster = true;  // engine: cluster (DSMEM exchange) or grid (L2 exchange)
+  bool cluster = true;  // scan engine: cluster (DSMEM exchange) or grid (L2 exchange)
+  bool bucket = false;  // distance-class engine available and selected (min weight >= 1)
   uint64_t exch_base = 0;
   double transfer_in_s = 0;
   uint32_t pending = 0;  // solves enqueued and not yet finished
@@ -444,6 +452,101 @@ int compute_max_batch(sssp_graph* g) {
   return SSSP_OK;
 }
 
+// The distance-class engine is exact iff every finite off-diagonal weight is
+// >= 1 (bucket_kernel.cuh); it runs on single-shard graphs with the cluster
+// layout (power-of-two participant count).  It needs the matrix transpose for
+// PULL steps: none when the matrix is symmetric, else a second device copy
+// when it fits (otherwise PUSH only).
+int prepare_bucket(sssp_graph* g) {
+  const int want = g->opt.engine;
+  if (want == SSSP_ENGINE_GRID || want == SSSP_ENGINE_CLUSTER) return SSSP_OK;
+  const bool exact = g->min_w >= 1;
+  // the visit-order debug output is produced by the round-by-round engines
+  const bool shape = g->P == 1 && g->cluster && g->n > 1 && !g->opt.record_visit_order;
+  if (want == SSSP_ENGINE_BUCKET && !(exact && shape))
+    return fail(SSSP_ERR_UNSUPPORTED,
+                exact ? "bucket engine needs one shard" : "bucket engine needs min weight >= 1");
+  if (!(exact && shape)) return SSSP_OK;
+  Shard& s = g->sh[0];
+  CK(cudaSetDevice(s.device));
+  const uint32_t Q = s.G, L = s.L;
+  if ((Q & (Q - 1)) || (L & (L - 1))) return SSSP_OK;
+  // tile T: 256 B of each row per CTA, widened until the grid is co-resident
+  void* fn = g->wbytes == 1 ? (void*)bucket_kernel<uint8_t>
+             : g->wbytes == 2 ? (void*)bucket_kernel<uint16_t> : (void*)bucket_kernel<uint32_t>;
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
+  uint32_t T = 256 / g->wbytes;
+  while (true) {
+    if (T > s.row_stride) T = (uint32_t)s.row_stride;
+    const size_t cpt = 16 / g->wbytes, ksz = g->wbytes == 1 ? 4 : 8;
+    const size_t smem = (size_t)T * 8 + ((T + 31) / 32) * 4 + kBucketChunk * 4 + kBucketThreads * cpt * ksz;
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBucketThreads, smem));
+    const uint64_t G = s.row_stride / T;
+    if (per_sm > 0 && G <= (uint64_t)per_sm * sms && T * g->wbytes / 16 <= kBucketThreads) {
+      s.bT = T;
+      s.bG = (uint32_t)G;
+      break;
+    }
+    if (T * g->wbytes >= 4096 || T >= s.row_stride)
+      return fail(SSSP_ERR_UNSUPPORTED, "bucket grid does not fit co-resident");
+    T *= 2;
+  }
+  CK(cudaMalloc(&s.d_bitmap, 2 * (s.row_stride / 32) * sizeof(uint32_t)));
+  CK(cudaMalloc(&s.d_ctrl, 8 * sizeof(uint32_t)));
+  // transpose (position order) and a symmetry check
+  size_t free_b = 0, total_b = 0;
+  CK(cudaMemGetInfo(&free_b, &total_b));
+  const uint64_t mbytes = g->n * s.row_stride * g->wbytes;
+  s.pull_src = nullptr;
+  if (mbytes + (256ull << 20) < free_b) {
+    CK(cudaMalloc(&s.d_adjT, mbytes));
+    const dim3 grid((unsigned)(s.row_stride / 64), (unsigned)(s.row_stride / 64));
+    const uint32_t qb = bitlen(Q) - 1, lb = bitlen(L) - 1;
+    if (s.row_stride % 64 == 0) {
+      if (g->wbytes == 1)
+        transpose_positions_kernel<uint8_t><<<grid, 256, 0, s.stream>>>(
+            (const uint8_t*)s.d_adj, (uint8_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
+      else if (g->wbytes == 2)
+        transpose_positions_kernel<uint16_t><<<grid, 256, 0, s.stream>>>(
+            (const uint16_t*)s.d_adj, (uint16_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
+      else
+        transpose_positions_kernel<uint32_t><<<grid, 256, 0, s.stream>>>(
+            (const uint32_t*)s.d_adj, (uint32_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
+      CK(cudaGetLastError());
+      uint32_t* d_flag = nullptr;
+      CK(cudaMalloc(&d_flag, 4));
+      CK(cudaMemsetAsync(d_flag, 0, 4, s.stream));
+      const uint64_t elems = g->n * s.row_stride;
+      if (g->wbytes == 1)
+        compare_rows_kernel<uint8_t><<<sms * 8, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, (const uint8_t*)s.d_adjT, elems, d_flag);
+      else if (g->wbytes == 2)
+        compare_rows_kernel<uint16_t><<<sms * 8, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, (const uint16_t*)s.d_adjT, elems, d_flag);
+      else
+        compare_rows_kernel<uint32_t><<<sms * 8, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, (const uint32_t*)s.d_adjT, elems, d_flag);
+      uint32_t asym = 1;
+      CK(cudaMemcpyAsync(&asym, d_flag, 4, cudaMemcpyDeviceToHost, s.stream));
+      CK(cudaStreamSynchronize(s.stream));
+      cudaFree(d_flag);
+      if (!asym) {  // symmetric: row v of A is column v
+        cudaFree(s.d_adjT);
+        s.d_adjT = nullptr;
+        s.pull_src = s.d_adj;
+      } else {
+        s.pull_src = s.d_adjT;
+        g->matrix_bytes += mbytes;
+      }
+    } else {
+      cudaFree(s.d_adjT);
+      s.d_adjT = nullptr;
+    }
+  }
+  g->bucket = true;
+  return SSSP_OK;
+}
+
 int setup_common(sssp_graph* g) {
   int rc = finalize_encoding(g);
   if (rc) return rc;
@@ -455,7 +558,7 @@ int setup_common(sssp_graph* g) {
     if (rc) return rc;
     g->matrix_bytes += g->n * s.row_stride * g->wbytes;
   }
-  return SSSP_OK;
+  return prepare_bucket(g);
 }
 
 int create_shard_objects(sssp_graph* g, uint32_t P, const int* devices, uint32_t nlocal,
@@ -506,6 +609,9 @@ void destroy_graph(sssp_graph* g) {
     cudaFree(s.d_info);
     cudaFree(s.d_sources);
     cudaFree(s.d_visit);
+    cudaFree(s.d_adjT);
+    cudaFree(s.d_bitmap);
+    cudaFree(s.d_ctrl);
     if (s.h_sources) cudaFreeHost(s.h_sources);
     if (s.h_info) cudaFreeHost(s.h_info);
     if (s.ev0) cudaEventDestroy(s.ev0);
@@ -552,6 +658,39 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
   if (k == 0 || k > g->max_batch) return fail(SSSP_ERR_BAD_ARG, "bad batch size");
   for (uint32_t i = 0; i < k; ++i)
     if (sources[i] >= g->n) return fail(SSSP_ERR_BAD_SOURCE, "dijkstra: source out of range");
+  if (g->bucket) {
+    Shard& s = g->sh[0];
+    CK(cudaSetDevice(s.device));
+    CK(cudaEventRecord(s.ev0, s.stream));
+    void* fn = g->wbytes == 1 ? (void*)bucket_kernel<uint8_t>
+               : g->wbytes == 2 ? (void*)bucket_kernel<uint16_t> : (void*)bucket_kernel<uint32_t>;
+    const size_t cpt = 16 / g->wbytes, ksz = g->wbytes == 1 ? 4 : 8;
+    const size_t smem = (size_t)s.bT * 8 + ((s.bT + 31) / 32) * 4 + kBucketChunk * 4 +
+                        kBucketThreads * cpt * ksz;
+    for (uint32_t i = 0; i < k; ++i) {
+      BucketParams bp{};
+      bp.adj = s.d_adj;
+      bp.adjT = s.pull_src;
+      bp.row_stride = s.row_stride;
+      bp.n = (uint32_t)g->n;
+      bp.Q = s.G;
+      bp.L = s.L;
+      bp.qbits = bitlen(s.G) - 1;
+      bp.lbits = bitlen(s.L) - 1;
+      bp.T = s.bT;
+      bp.source = (uint32_t)sources[i];
+      bp.bitmap = s.d_bitmap;
+      bp.ctrl = s.d_ctrl;
+      bp.dist_out = s.d_dist + (uint64_t)i * s.loc_n;
+      bp.pred_out = s.d_pred + (uint64_t)i * s.loc_n;
+      bp.info = s.d_info + (uint64_t)i * 4;
+      void* args[] = {&bp};
+      CK(cudaLaunchCooperativeKernel(fn, dim3(s.bG), dim3(kBucketThreads), args, smem, s.stream));
+    }
+    CK(cudaEventRecord(s.ev1, s.stream));
+    g->pending = k;
+    return SSSP_OK;
+  }
   // Single process: reset the exchange buffers of every shard first, and make
   // every launch wait for all resets (a peer may publish into our buffers as
   // soon as its kernel starts).
@@ -617,7 +756,7 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
   const uint32_t k = g->pending;
   if (k == 0) return fail(SSSP_ERR_BAD_ARG, "nothing enqueued");
   double rounds = 0;
-  uint64_t iters = 0, last = 0, mis = 0;
+  uint64_t iters = 0, last = 0, mis = 0, classes = 0, rows = 0;
   bool timeout = false;
   for (auto& s : g->sh) {
     CK(cudaSetDevice(s.device));
@@ -628,6 +767,12 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
     rounds = std::max(rounds, ms * 1e-3);
     for (uint32_t i = 0; i < k; ++i) {
+      if (g->bucket) {
+        iters += s.h_info[4 * i];
+        classes += s.h_info[4 * i + 1];
+        rows += s.h_info[4 * i + 2] + s.h_info[4 * i + 3];
+        continue;
+      }
       iters += s.k == g->sh[0].k ? s.h_info[4 * i] : 0;
       last = std::max(last, s.h_info[4 * i + 1]);
       timeout |= s.h_info[4 * i + 2] != 0;
@@ -640,8 +785,11 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     st->transfer_in_s = g->transfer_in_s;
     st->rounds_s = rounds;
     st->iterations = iters;
-    st->relax_checks = iters * g->sh[0].row_stride * g->P;
+    st->relax_checks = (g->bucket ? rows : iters) * g->sh[0].row_stride * g->P;
     st->mispredicts = mis;
+    st->engine = g->bucket ? SSSP_ENGINE_BUCKET : g->cluster ? SSSP_ENGINE_CLUSTER : SSSP_ENGINE_GRID;
+    st->classes = (uint32_t)classes;
+    st->rows_read = g->bucket ? rows : iters;
     st->matrix_bytes = g->matrix_bytes;
     st->weight_bytes = g->wbytes;
     st->ctas = g->cluster ? g->sh[0].C : g->sh[0].G;
@@ -869,6 +1017,7 @@ int sssp_graph_info(const sssp_graph* g, sssp_solve_stats* st) {
   st->ctas = g->cluster ? g->sh[0].C : g->sh[0].G;
   st->shards = g->P;
   st->packed_key = g->packed;
+  st->engine = g->bucket ? SSSP_ENGINE_BUCKET : g->cluster ? SSSP_ENGINE_CLUSTER : SSSP_ENGINE_GRID;
   st->iterations = g->max_batch;  // reused: concurrent solve capacity
   st->relax_checks = g->min_w;    // reused: min finite off-diagonal weight
   st->mispredicts = g->max_w;     // reused: max finite weight

@@ -1,0 +1,110 @@
+"""The distance-class (bucket) engine: bit-identical to dijkstra_serial
+whenever every finite off-diagonal weight is >= 1 (bucket_kernel.cuh), and
+never selected otherwise.  Covers push and pull steps, symmetric (pull from
+the matrix) and asymmetric (pull from the transpose) graphs, many classes,
+all weight encodings and batches."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+INF = 0xFFFFFFFFFFFFFFFF
+
+
+def rand_graph(rng, n, wlo, whi, density, directed):
+    adj = np.full((n, n), INF, dtype=np.uint64)
+    m = rng.random((n, n)) < density
+    adj[m] = rng.integers(wlo, whi + 1, size=int(m.sum()), dtype=np.uint64)
+    if not directed:
+        iu = np.triu_indices(n, 1)
+        adj[(iu[1], iu[0])] = adj[iu]
+    np.fill_diagonal(adj, 0)
+    return adj
+
+
+def check(gpu, oracle_c, g, s, **kw):
+    d, p = oracle_c.serial(g.adj, g.n, s)
+    with gpu.DeviceGraph(g, **kw) as dg:
+        info = dg.info()
+        r = dg.solve(s)
+    ok = np.array_equal(r.dist, d) and np.array_equal(r.pred, p)
+    if not ok:
+        bad = np.nonzero((r.dist != d) | (r.pred != p))[0]
+        i = int(bad[0])
+        raise AssertionError(f"n={g.n} s={s}: {len(bad)} mismatches, v={i} gpu=({r.dist[i]},"
+                             f"{r.pred[i]}) want=({d[i]},{p[i]}) engine={info['engine']}")
+    return info, r
+
+
+@pytest.mark.parametrize("seed", range(8))
+def test_bucket_tie_heavy_positive_weights(gpu, oracle_c, seed):
+    rng = np.random.default_rng(300 + seed)
+    for i in range(25):
+        n = int(rng.integers(2, 400))
+        directed = bool(i % 2)
+        g = gpu.Graph(n, directed, rand_graph(rng, n, 1, 3, float(rng.choice([0.005, 0.02, 0.1, 0.5, 1.0])),
+                                             directed))
+        info, r = check(gpu, oracle_c, g, int(rng.integers(0, n)), engine="bucket")
+        assert info["engine"] == 3
+
+
+def test_auto_selects_bucket_only_when_exact(gpu, oracle_c):
+    rng = np.random.default_rng(7)
+    g = gpu.Graph(300, False, rand_graph(rng, 300, 1, 5, 0.1, False))
+    info, _ = check(gpu, oracle_c, g, 0)
+    assert info["engine"] == 3
+    g0 = gpu.Graph(300, False, rand_graph(rng, 300, 0, 5, 0.1, False))  # zero weights
+    info, _ = check(gpu, oracle_c, g0, 0)
+    assert info["engine"] == 2
+    with pytest.raises(gpu.SsspError):
+        gpu.DeviceGraph(g0, engine="bucket")
+
+
+@pytest.mark.parametrize("kind", ["dense", "sparse", "sparse_directed", "bern_directed"])
+def test_bucket_generated_graphs(gpu, oracle_c, kind):
+    for n, seed in [(1000, 42), (2049, 5), (5000, 11)]:
+        if kind == "dense":
+            g = gpu.generate_dense(n, seed)
+        elif kind == "sparse":
+            g = gpu.generate_sparse(n, seed)
+        elif kind == "sparse_directed":
+            g = gpu.generate_sparse(n, seed, directed=True)
+        else:
+            g = gpu.generate_bernoulli(n, 0.01, seed, directed=True)
+        for s in (0, n // 3, n - 1):
+            info, r = check(gpu, oracle_c, g, s, engine="bucket")
+            assert r.stats["engine"] == 3 and r.stats["classes"] >= 1
+
+
+@pytest.mark.parametrize("wmax,wbytes", [(254, 1), (3000, 2), (70000, 4)])
+def test_bucket_weight_encodings(gpu, oracle_c, wmax, wbytes):
+    rng = np.random.default_rng(wmax)
+    for directed in (False, True):
+        g = gpu.Graph(600, directed, rand_graph(rng, 600, 1, wmax, 0.05, directed))
+        info, _ = check(gpu, oracle_c, g, 3, engine="bucket")
+        assert info["weight_bytes"] == wbytes
+
+
+def test_bucket_batch_and_repeat(gpu, oracle_c):
+    g = gpu.generate_dense(3000, 17)
+    srcs = [0, 1, 999, 2999, 1500]
+    with gpu.DeviceGraph(g, engine="bucket") as dg:
+        res = dg.solve_batch(srcs)
+        again = dg.solve(999)
+    for s, r in zip(srcs, res):
+        d, p = oracle_c.serial(g.adj, g.n, s)
+        assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p)
+    assert again == res[2]
+
+
+def test_bucket_unreachable_and_isolated(gpu, oracle_c):
+    g = gpu.Graph.no_edges(700, True)
+    g.adj[5 * 700 + 6] = 3
+    g.adj[6 * 700 + 9] = 1
+    check(gpu, oracle_c, g, 5, engine="bucket")
+    check(gpu, oracle_c, g, 0, engine="bucket")
+
+
+def test_bucket_config3(gpu, oracle_c):
+    g = gpu.generate_dense(32768, 32768)
+    info, r = check(gpu, oracle_c, g, 0, engine="bucket")
+    assert r.stats["classes"] == 4
