@@ -48,10 +48,11 @@ struct BucketParams {
   uint32_t T;           // positions per CTA
   uint32_t source;
   uint32_t* bitmap;     // [2][row_stride / 32] (B_d by position)
-  uint32_t* ctrl;       // [0..1] dmin[parity], [2..3] bcount, [4..5] ucount, [6] steps
+  uint32_t* ctrl;       // [2 parities][3][G]: per-tile lmin, candidate count, unsettled count
   uint64_t* dist_out;   // [n]
   uint64_t* pred_out;   // [n]
   uint64_t* info;       // [4]: settled vertices, classes (steps), rows pushed, rows pulled
+  uint64_t* trace;      // optional [64]: %globaltimer after every grid barrier (CTA 0)
 };
 
 __device__ __forceinline__ uint32_t pos_to_vid(uint32_t pos, uint32_t Q, uint32_t lbits,
@@ -80,6 +81,11 @@ struct BucketKey<uint16_t> {
 template <>
 struct BucketKey<uint32_t> : BucketKey<uint16_t> {};
 
+__device__ __forceinline__ void smem_min(uint32_t* a, uint32_t v) { atomicMin(a, v); }
+__device__ __forceinline__ void smem_min(uint64_t* a, uint64_t v) {
+  atomicMin(reinterpret_cast<unsigned long long*>(a), (unsigned long long)v);
+}
+
 template <typename K>
 __device__ __forceinline__ K warp_min_key(K k) {
   if constexpr (sizeof(K) == 4) {
@@ -92,10 +98,24 @@ __device__ __forceinline__ K warp_min_key(K k) {
 }
 
 constexpr int kBucketThreads = 256;
+
+__host__ __device__ constexpr uint32_t bucket_round4(uint32_t x) { return (x + 3u) & ~3u; }
+
+// dynamic shared memory of bucket_kernel (keeps every region 16 B aligned)
+__host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t T, uint32_t G, uint32_t words,
+                                                       uint32_t wbytes);
 constexpr int kBucketChunk = kBucketThreads * 32;  // ids of one pass over 256 bitmap words
 
-// Dynamic smem: dist[T] u32 | pred[T] u32 | settled[T/32] u32 | chunk[kBucketChunk] u32
-//               | combine[kBucketThreads * (16/sizeof(W))] keys
+// Dynamic smem: dist[T] u32 | pred[T] u32 | settled[T/32] u32 | lmin[G] u32 |
+//               bitmap[row_stride/32] u32 | chunk[kBucketChunk] u32 |
+//               combine[kBucketThreads * CPT] keys
+//
+// One grid barrier per class.  Before the barrier that ends step s every CTA
+// publishes, for its own tile: its minimum unsettled dist (lmin), the bitmap
+// of its unsettled columns at that minimum (the class candidates), and its
+// counts.  After the barrier every CTA derives d = min(lmin); the candidates
+// of the tiles with lmin == d form B_d -- no second barrier is needed to
+// build the class.
 template <typename W>
 __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketParams p) {
   namespace cg = cooperative_groups;
@@ -107,22 +127,67 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
   cg::grid_group grid = cg::this_grid();
 
   extern __shared__ __align__(16) uint32_t smem[];
-  const uint32_t T = p.T;
+  const uint32_t T = p.T, G = gridDim.x;
+  const uint32_t TW = T / 32;  // bitmap words per tile
+  const uint32_t words = (uint32_t)(p.row_stride / 32);
   uint32_t* sdist = smem;
   uint32_t* spred = sdist + T;
   uint32_t* ssettled = spred + T;
-  uint32_t* schunk = ssettled + (T + 31) / 32;
+  uint32_t* slmin = ssettled + bucket_round4(TW);
+  uint32_t* sbm = slmin + bucket_round4(G);  // B_d bitmap (all positions), staged per class
+  uint32_t* schunk = sbm + bucket_round4(words);
   K* scomb = reinterpret_cast<K*>(schunk + kBucketChunk);
   __shared__ uint32_t s_red[kBucketThreads / 32];
   __shared__ uint32_t s_cnt[2];
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t p0 = blockIdx.x * T;  // first position of this CTA's tile
-  const uint32_t words = (uint32_t)(p.row_stride / 32);
+  const uint32_t me = blockIdx.x;
+  const uint32_t p0 = me * T;
+  const uint32_t tbits = 31u - __clz(T);  // T is a power of two
   const W* adj = static_cast<const W*>(p.adj);
   const W* adjT = static_cast<const W*>(p.adjT);
   const uint32_t TPR = T * sizeof(W) / 16;  // threads per row slice
   const uint32_t RG = kBucketThreads / TPR; // row groups
+  // global per-step arrays: ctrl = [2][3][G] (lmin, candidates, unsettled)
+  uint32_t* const glob = p.ctrl;
+
+  uint32_t ntr = 0;
+  auto stamp = [&]() {
+    if (p.trace && me == 0 && tid == 0 && ntr < 64) p.trace[ntr++] = globaltimer();
+  };
+
+  // Publishes this tile's minimum, candidate bitmap and counts for step `s`.
+  auto publish = [&](uint32_t par) {
+    uint32_t m = DINF, uns = 0;
+    for (uint32_t col = tid; col < T; col += kBucketThreads)
+      if (!((ssettled[col >> 5] >> (col & 31)) & 1u)) {
+        m = min(m, sdist[col]);
+        ++uns;
+      }
+    m = __reduce_min_sync(0xFFFFFFFFu, m);
+    uns = __reduce_add_sync(0xFFFFFFFFu, uns);
+    if (lane == 0) s_red[warp] = m;
+    if (tid < 2) s_cnt[tid] = 0;
+    __syncthreads();
+    if (lane == 0) atomicAdd(&s_cnt[1], uns);
+    for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) m = min(m, s_red[w2]);
+    uint32_t* bm = p.bitmap + par * words + me * TW;
+    for (uint32_t i = tid; i < TW; i += kBucketThreads) {
+      uint32_t cm = 0;
+      const uint32_t sm = ssettled[i];
+      if (m != DINF)
+        for (uint32_t b = 0; b < 32; ++b)
+          if (!((sm >> b) & 1u) && sdist[i * 32 + b] == m) cm |= 1u << b;
+      bm[i] = cm;
+      if (cm) atomicAdd(&s_cnt[0], __popc(cm));
+    }
+    __syncthreads();
+    if (tid == 0) {
+      glob[(par * 3 + 0) * G + me] = m;
+      glob[(par * 3 + 1) * G + me] = s_cnt[0];
+      glob[(par * 3 + 2) * G + me] = s_cnt[1];
+    }
+  };
 
   // ---- init: dist = INF, pred = NONE, padding settled (serial.hpp:32-36)
   for (uint32_t i = tid; i < T; i += kBucketThreads) {
@@ -130,66 +195,68 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
     sdist[i] = v == p.source ? 0u : DINF;
     spred[i] = 0xFFFFFFFFu;
   }
-  for (uint32_t i = tid; i < (T + 31) / 32; i += kBucketThreads) {
+  for (uint32_t i = tid; i < TW; i += kBucketThreads) {
     uint32_t m = 0;
-    for (uint32_t b = 0; b < 32 && i * 32 + b < T; ++b)
+    for (uint32_t b = 0; b < 32; ++b)
       if (pos_to_vid(p0 + i * 32 + b, p.Q, p.lbits, p.qbits) >= p.n) m |= 1u << b;
     ssettled[i] = m;
   }
-  if (blockIdx.x == 0 && tid == 0) {
-    p.ctrl[0] = 0;  // class 0 = the source
-    p.ctrl[1] = DINF;
-    p.ctrl[2] = p.ctrl[3] = p.ctrl[4] = p.ctrl[5] = 0;
-  }
-  for (uint32_t i = blockIdx.x * kBucketThreads + tid; i < 2 * words; i += gridDim.x * kBucketThreads)
-    p.bitmap[i] = 0;
+  __syncthreads();
+  publish(0);
   grid.sync();
+  stamp();
 
   uint64_t pushed = 0, pulled = 0, settled = 0;
   uint32_t step = 0;
   while (true) {
     const uint32_t par = step & 1u, nxt = par ^ 1u;
-    const uint32_t d = *(volatile uint32_t*)&p.ctrl[par];
-    if (d == DINF) break;
-    // ---- phase A: settle B_d = {unsettled, dist == d}; count B_d and the rest
-    if (tid < 2) s_cnt[tid] = 0;
+    // ---- the class: d = min over tiles, B_d = candidates of the tiles at d
+    uint32_t d = DINF, bcount = 0, uns = 0;
+    for (uint32_t c = tid; c < G; c += kBucketThreads) {
+      const uint32_t lm = __ldcg(&glob[(par * 3 + 0) * G + c]);
+      slmin[c] = lm;
+      d = min(d, lm);
+    }
+    d = __reduce_min_sync(0xFFFFFFFFu, d);
+    if (lane == 0) s_red[warp] = d;
     __syncthreads();
-    uint32_t* bm = p.bitmap + par * words;
-    for (uint32_t i = tid; i < (T + 31) / 32; i += kBucketThreads) {
-      uint32_t setm = 0, uns = 0;
-      const uint32_t sm = ssettled[i];
-      for (uint32_t b = 0; b < 32 && i * 32 + b < T; ++b) {
-        if ((sm >> b) & 1u) continue;
-        if (sdist[i * 32 + b] == d) setm |= 1u << b;
-        else ++uns;
-      }
-      if (setm) {
-        ssettled[i] = sm | setm;
-        atomicOr(&bm[(p0 >> 5) + i], setm);  // T is a multiple of 32: word-aligned tiles
-        atomicAdd(&s_cnt[0], __popc(setm));
-      }
-      if (uns) atomicAdd(&s_cnt[1], uns);
+    for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) d = min(d, s_red[w2]);
+    if (d == DINF) break;  // uniform: every CTA reads the same values
+    for (uint32_t c = tid; c < G; c += kBucketThreads) {
+      if (slmin[c] == d) bcount += __ldcg(&glob[(par * 3 + 1) * G + c]);
+      uns += __ldcg(&glob[(par * 3 + 2) * G + c]);
+    }
+    bcount = __reduce_add_sync(0xFFFFFFFFu, bcount);
+    uns = __reduce_add_sync(0xFFFFFFFFu, uns);
+    __syncthreads();  // s_red reuse
+    if (lane == 0) {
+      s_red[warp] = bcount;
     }
     __syncthreads();
-    if (tid == 0) {
-      if (s_cnt[0]) atomicAdd(&p.ctrl[2 + par], s_cnt[0]);
-      if (s_cnt[1]) atomicAdd(&p.ctrl[4 + par], s_cnt[1]);
+    bcount = 0;
+    for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) bcount += s_red[w2];
+    __syncthreads();
+    if (lane == 0) s_red[warp] = uns;
+    __syncthreads();
+    uns = 0;
+    for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) uns += s_red[w2];
+    const uint32_t ucount = uns - bcount;  // unsettled after settling B_d
+    // stage B_d (candidates of the tiles at d) in shared memory: every
+    // later bitmap lookup of this class hits smem, not a few hot L2 lines
+    {
+      const uint32_t* bm = p.bitmap + par * words;
+      for (uint32_t i = tid; i < words; i += kBucketThreads)
+        sbm[i] = slmin[i / TW] == d ? __ldcg(&bm[i]) : 0u;
     }
-    if (blockIdx.x == 0 && tid == 0) {  // reset the next step's reductions
-      p.ctrl[nxt] = DINF;
-      p.ctrl[2 + nxt] = 0;
-      p.ctrl[4 + nxt] = 0;
-    }
-    for (uint32_t i = blockIdx.x * kBucketThreads + tid; i < words; i += gridDim.x * kBucketThreads)
-      p.bitmap[nxt * words + i] = 0;
-    grid.sync();
-
-    const uint32_t bcount = *(volatile uint32_t*)&p.ctrl[2 + par];
-    const uint32_t ucount = *(volatile uint32_t*)&p.ctrl[4 + par];
+    __syncthreads();
+    // settle my candidates if my tile is in the class
+    for (uint32_t i = tid; i < TW; i += kBucketThreads) ssettled[i] |= sbm[me * TW + i];
+    __syncthreads();
     ++step;
     settled += bcount;
     if (ucount == 0) break;  // nothing left to relax (the last class needs no rows)
     const bool pull = adjT != nullptr && ucount < bcount;
+    const uint32_t dk = d;
 
     if (!pull) {
       // ---- PUSH: stream the rows of B_d (ascending ids), per-column min key
@@ -198,13 +265,11 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
       K best[CPT];
 #pragma unroll
       for (int j = 0; j < CPT; ++j) best[j] = KT::kNone;
-      // enumerate set bits of the whole bitmap in order, kBucketChunk at a time
-      uint32_t wbase = 0;
-      while (wbase < words) {
-        // take up to kBucketThreads bitmap words, prefix-sum their popcounts
+      for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads) {
         const uint32_t wi = wbase + tid;
-        const uint32_t bw = wi < words ? __ldcg(&bm[wi]) : 0u;
-        uint32_t c = __popc(bw);
+        const uint32_t bw = wi < words ? sbm[wi] : 0u;
+        if (!__syncthreads_or(bw != 0)) continue;
+        const uint32_t c = __popc(bw);
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -219,44 +284,48 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
           tot += s_red[w2];
         }
         uint32_t o = wofs + incl - c;
-        for (uint32_t m = bw; m; m &= m - 1) {
-          const uint32_t pos = wi * 32 + (__ffs(m) - 1);
-          schunk[o++] = pos_to_vid(pos, p.Q, p.lbits, p.qbits);  // < kBucketChunk: 256*32 bits
-        }
+        for (uint32_t m = bw; m; m &= m - 1)
+          schunk[o++] = pos_to_vid(wi * 32 + (__ffs(m) - 1), p.Q, p.lbits, p.qbits);
         __syncthreads();
-        // relax the rows of this chunk (ascending vertex ids)
-#pragma unroll 4
-        for (uint32_t r = rg; r < tot; r += RG) {
-          const uint32_t u = schunk[r];
-          const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(
-              reinterpret_cast<const uint8_t*>(adj + (size_t)u * p.row_stride + p0) + ct * 16));
-          const uint32_t wd[4] = {v4.x, v4.y, v4.z, v4.w};
+        // batches of 8 rows: all 8 loads are issued before any is consumed
+        for (uint32_t r0 = rg; r0 < tot; r0 += 8 * RG) {
+          uint32_t ub[8];
+          uint4 vb[8];
 #pragma unroll
-          for (int j = 0; j < CPT; ++j) {
-            const uint32_t word = wd[(j * sizeof(W)) / 4];
-            const uint32_t w = sizeof(W) == 4 ? word : (word >> (((j * sizeof(W)) % 4) * 8)) & WINF;
-            if (w != WINF) {
-              const K k = KT::make(w, u);
+          for (int m = 0; m < 8; ++m) {
+            const uint32_t r = r0 + m * RG;
+            ub[m] = r < tot ? schunk[r] : 0xFFFFFFFFu;
+            if (r < tot)
+              vb[m] = __ldg(reinterpret_cast<const uint4*>(
+                  reinterpret_cast<const uint8_t*>(adj + (size_t)ub[m] * p.row_stride + p0) + ct * 16));
+          }
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            if (ub[m] == 0xFFFFFFFFu) break;
+            const uint32_t wd[4] = {vb[m].x, vb[m].y, vb[m].z, vb[m].w};
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+              const uint32_t word = wd[(j * sizeof(W)) / 4];
+              const uint32_t w = sizeof(W) == 4 ? word : (word >> (((j * sizeof(W)) % 4) * 8)) & WINF;
+              const K k = KT::make(w, ub[m]);  // INF weights make keys above every finite one
               best[j] = k < best[j] ? k : best[j];
             }
           }
         }
         __syncthreads();
-        wbase += kBucketThreads;
       }
-      // combine the RG row groups per column
 #pragma unroll
       for (int j = 0; j < CPT; ++j) scomb[tid * CPT + j] = best[j];
       __syncthreads();
       for (uint32_t col = tid; col < T; col += kBucketThreads) {
         const uint32_t cth = col / CPT, j = col % CPT;
         K k = KT::kNone;
-        for (uint32_t g = 0; g < RG; ++g) {
-          const K x = scomb[(g * TPR + cth) * CPT + j];
+        for (uint32_t g2 = 0; g2 < RG; ++g2) {
+          const K x = scomb[(g2 * TPR + cth) * CPT + j];
           k = x < k ? x : k;
         }
-        if (k != KT::kNone) {
-          const uint32_t cand = d + KT::w(k);
+        if (KT::w(k) != WINF && k != KT::kNone) {
+          const uint32_t cand = dk + KT::w(k);
           if (cand < sdist[col]) {  // settled columns hold dist <= d < cand
             sdist[col] = cand;
             spred[col] = KT::u(k);
@@ -265,34 +334,74 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
       }
       __syncthreads();
     } else {
-      // ---- PULL: one warp per unsettled column v of this tile; stream row v
-      // of the transpose, keep only positions in B_d
+      // ---- PULL: stream column v (row v of the transpose) of every unsettled
+      // column of this tile, masked by B_d.  The (column, 16 B chunk) items are
+      // spread over all threads with 8 loads in flight each, so the tile's
+      // columns are read concurrently and evenly.
       pulled += ucount;
-      for (uint32_t col = warp; col < T; col += kBucketThreads / 32) {
-        if ((ssettled[col >> 5] >> (col & 31)) & 1u) continue;
-        const uint32_t v = pos_to_vid(p0 + col, p.Q, p.lbits, p.qbits);
-        const uint8_t* row = reinterpret_cast<const uint8_t*>(adjT + (size_t)v * p.row_stride);
-        K k = KT::kNone;
-        for (uint32_t off = lane * 16; off < p.row_stride * sizeof(W); off += 32 * 16) {
-          const uint32_t pos0 = off / sizeof(W);
-          const uint32_t bits = (__ldcg(&bm[pos0 >> 5]) >> (pos0 & 31)) & ((1u << CPT) - 1u);
-          if (!bits) continue;
-          const uint4 v4 = __ldg(reinterpret_cast<const uint4*>(row + off));
-          const uint32_t wd[4] = {v4.x, v4.y, v4.z, v4.w};
+      K* sk = scomb;                            // per unsettled column running key
+      uint32_t* slist = schunk;                 // unsettled columns of this tile
+      __shared__ uint32_t s_nu;
+      if (tid == 0) s_nu = 0;
+      __syncthreads();
+      for (uint32_t col = tid; col < T; col += kBucketThreads)
+        if (!((ssettled[col >> 5] >> (col & 31)) & 1u)) {
+          const uint32_t i = atomicAdd(&s_nu, 1u);
+          slist[i] = col;
+          sk[i] = KT::kNone;
+        }
+      __syncthreads();
+      const uint32_t nu = s_nu;
+      const uint32_t cbits = 31u - __clz((uint32_t)(p.row_stride * sizeof(W) / 16));  // chunks/row
+      const uint32_t total = nu << cbits;
+      uint32_t cur = 0xFFFFFFFFu;
+      K run = KT::kNone;
+      for (uint32_t it0 = tid; it0 < total; it0 += kBucketThreads * 8) {
+        uint4 v4[8];
+        uint32_t bits[8], ci[8];
 #pragma unroll
-          for (int j = 0; j < CPT; ++j) {
-            if (!((bits >> j) & 1u)) continue;
-            const uint32_t word = wd[(j * sizeof(W)) / 4];
-            const uint32_t w = sizeof(W) == 4 ? word : (word >> (((j * sizeof(W)) % 4) * 8)) & WINF;
-            if (w != WINF) {
-              const K kk = KT::make(w, pos_to_vid(pos0 + j, p.Q, p.lbits, p.qbits));
-              k = kk < k ? kk : k;
-            }
+        for (int m = 0; m < 8; ++m) {
+          const uint32_t item = it0 + m * kBucketThreads;
+          ci[m] = 0xFFFFFFFFu;
+          bits[m] = 0;
+          if (item < total) {
+            ci[m] = item >> cbits;
+            const uint32_t chunk = item & ((1u << cbits) - 1u);
+            const uint32_t pos0 = chunk * CPT;
+            const uint32_t v = pos_to_vid(p0 + slist[ci[m]], p.Q, p.lbits, p.qbits);
+            bits[m] = (sbm[pos0 >> 5] >> (pos0 & 31)) & ((1u << CPT) - 1u);
+            v4[m] = __ldg(reinterpret_cast<const uint4*>(
+                reinterpret_cast<const uint8_t*>(adjT + (size_t)v * p.row_stride) + chunk * 16));
           }
         }
-        k = warp_min_key<K>(k);
-        if (lane == 0 && k != KT::kNone) {
-          const uint32_t cand = d + KT::w(k);
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          if (ci[m] == 0xFFFFFFFFu) break;
+          if (ci[m] != cur) {
+            if (cur != 0xFFFFFFFFu && run != KT::kNone) smem_min(&sk[cur], run);
+            cur = ci[m];
+            run = KT::kNone;
+          }
+          const uint32_t pos0 = ((it0 + m * kBucketThreads) & ((1u << cbits) - 1u)) * CPT;
+          // consecutive positions of one participant: vertex ids step by Q
+          const uint32_t vid0 = pos_to_vid(pos0, p.Q, p.lbits, p.qbits);
+          const uint32_t wd[4] = {v4[m].x, v4[m].y, v4[m].z, v4[m].w};
+#pragma unroll
+          for (int c = 0; c < CPT; ++c) {
+            const uint32_t word = wd[(c * sizeof(W)) / 4];
+            const uint32_t w = sizeof(W) == 4 ? word : (word >> (((c * sizeof(W)) % 4) * 8)) & WINF;
+            const K kk = ((bits[m] >> c) & 1u) ? KT::make(w, vid0 + c * p.Q) : KT::kNone;
+            run = kk < run ? kk : run;
+          }
+        }
+      }
+      if (cur != 0xFFFFFFFFu && run != KT::kNone) smem_min(&sk[cur], run);
+      __syncthreads();
+      for (uint32_t i = tid; i < nu; i += kBucketThreads) {
+        const K k = sk[i];
+        const uint32_t col = slist[i];
+        if (k != KT::kNone && KT::w(k) != WINF) {
+          const uint32_t cand = dk + KT::w(k);
           if (cand < sdist[col]) {
             sdist[col] = cand;
             spred[col] = KT::u(k);
@@ -301,18 +410,10 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
       }
       __syncthreads();
     }
-    // ---- the next class: min dist over unsettled columns (grid-wide)
-    uint32_t m = DINF;
-    for (uint32_t col = tid; col < T; col += kBucketThreads)
-      if (!((ssettled[col >> 5] >> (col & 31)) & 1u)) m = min(m, sdist[col]);
-    m = __reduce_min_sync(0xFFFFFFFFu, m);
-    if (lane == 0) s_red[warp] = m;
-    __syncthreads();
-    if (tid == 0) {
-      for (uint32_t w2 = 1; w2 < kBucketThreads / 32; ++w2) m = min(m, s_red[w2]);
-      if (m != DINF) atomicMin(&p.ctrl[nxt], m);
-    }
+    // ---- publish the next class's candidates, one barrier per class
+    publish(nxt);
     grid.sync();
+    stamp();
   }
 
   // ---- write back (positions -> vertex ids)
@@ -323,12 +424,19 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
       p.pred_out[v] = spred[i] == 0xFFFFFFFFu ? ~0ull : (uint64_t)spred[i];
     }
   }
-  if (blockIdx.x == 0 && tid == 0) {
+  if (me == 0 && tid == 0) {
     p.info[0] = settled;
     p.info[1] = step;
     p.info[2] = pushed;
     p.info[3] = pulled;
   }
+}
+
+__host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t T, uint32_t G, uint32_t words,
+                                                       uint32_t wbytes) {
+  return 4ull * (2ull * T + bucket_round4(T / 32) + bucket_round4(G) + bucket_round4(words) +
+                 kBucketChunk) +
+         (size_t)kBucketThreads * (16 / wbytes) * (wbytes == 1 ? 4 : 8);
 }
 
 }  // namespace sssp_b200

@@ -11,6 +11,7 @@
 #include <atomic>
 #include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <thread>
@@ -127,6 +128,7 @@ struct Shard {
   uint32_t* d_bitmap = nullptr;  // [2][row_stride/32]
   uint32_t* d_ctrl = nullptr;    // [8]
   uint32_t bT = 0, bG = 0;       // positions per CTA, CTAs
+  uint64_t* d_trace = nullptr;   // debug (SSSP_BUCKET_TRACE)
   bool peer_ipc[kMaxShards] = {};
   KernelFn fn = nullptr;
 };
@@ -471,16 +473,19 @@ int prepare_bucket(sssp_graph* g) {
   CK(cudaSetDevice(s.device));
   const uint32_t Q = s.G, L = s.L;
   if ((Q & (Q - 1)) || (L & (L - 1))) return SSSP_OK;
-  // tile T: 256 B of each row per CTA, widened until the grid is co-resident
+  // tile T: 128 B of each row per CTA, widened until the grid is co-resident
   void* fn = g->wbytes == 1 ? (void*)bucket_kernel<uint8_t>
              : g->wbytes == 2 ? (void*)bucket_kernel<uint16_t> : (void*)bucket_kernel<uint32_t>;
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
-  uint32_t T = 256 / g->wbytes;
+  uint32_t T = 128 / g->wbytes;
   while (true) {
     if (T > s.row_stride) T = (uint32_t)s.row_stride;
     const size_t cpt = 16 / g->wbytes, ksz = g->wbytes == 1 ? 4 : 8;
-    const size_t smem = (size_t)T * 8 + ((T + 31) / 32) * 4 + kBucketChunk * 4 + kBucketThreads * cpt * ksz;
+    const uint64_t G0 = s.row_stride / T;
+    const size_t smem = bucket_smem_bytes(T, (uint32_t)G0, (uint32_t)(s.row_stride / 32), g->wbytes);
+    (void)cpt;
+    (void)ksz;
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBucketThreads, smem));
@@ -495,7 +500,7 @@ int prepare_bucket(sssp_graph* g) {
     T *= 2;
   }
   CK(cudaMalloc(&s.d_bitmap, 2 * (s.row_stride / 32) * sizeof(uint32_t)));
-  CK(cudaMalloc(&s.d_ctrl, 8 * sizeof(uint32_t)));
+  CK(cudaMalloc(&s.d_ctrl, 2 * 3 * (size_t)s.bG * sizeof(uint32_t)));
   // transpose (position order) and a symmetry check
   size_t free_b = 0, total_b = 0;
   CK(cudaMemGetInfo(&free_b, &total_b));
@@ -612,6 +617,7 @@ void destroy_graph(sssp_graph* g) {
     cudaFree(s.d_adjT);
     cudaFree(s.d_bitmap);
     cudaFree(s.d_ctrl);
+    cudaFree(s.d_trace);
     if (s.h_sources) cudaFreeHost(s.h_sources);
     if (s.h_info) cudaFreeHost(s.h_info);
     if (s.ev0) cudaEventDestroy(s.ev0);
@@ -665,8 +671,9 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
     void* fn = g->wbytes == 1 ? (void*)bucket_kernel<uint8_t>
                : g->wbytes == 2 ? (void*)bucket_kernel<uint16_t> : (void*)bucket_kernel<uint32_t>;
     const size_t cpt = 16 / g->wbytes, ksz = g->wbytes == 1 ? 4 : 8;
-    const size_t smem = (size_t)s.bT * 8 + ((s.bT + 31) / 32) * 4 + kBucketChunk * 4 +
-                        kBucketThreads * cpt * ksz;
+    const size_t smem = bucket_smem_bytes(s.bT, s.bG, (uint32_t)(s.row_stride / 32), g->wbytes);
+    (void)cpt;
+    (void)ksz;
     for (uint32_t i = 0; i < k; ++i) {
       BucketParams bp{};
       bp.adj = s.d_adj;
@@ -684,6 +691,11 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
       bp.dist_out = s.d_dist + (uint64_t)i * s.loc_n;
       bp.pred_out = s.d_pred + (uint64_t)i * s.loc_n;
       bp.info = s.d_info + (uint64_t)i * 4;
+      if (getenv("SSSP_BUCKET_TRACE")) {  // debug: per-barrier timestamps to stderr
+        if (!s.d_trace) CK(cudaMalloc(&s.d_trace, 64 * 8));
+        CK(cudaMemsetAsync(s.d_trace, 0, 64 * 8, s.stream));
+        bp.trace = s.d_trace;
+      }
       void* args[] = {&bp};
       CK(cudaLaunchCooperativeKernel(fn, dim3(s.bG), dim3(kBucketThreads), args, smem, s.stream));
     }
@@ -781,6 +793,13 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
   }
   g->pending = 0;
   if (g->multiproc) g->exch_base = last + 1;
+  if (g->bucket && g->sh[0].d_trace) {
+    uint64_t tr[64];
+    CK(cudaMemcpy(tr, g->sh[0].d_trace, sizeof(tr), cudaMemcpyDeviceToHost));
+    fprintf(stderr, "bucket trace (us since init barrier):");
+    for (int i = 1; i < 64 && tr[i]; ++i) fprintf(stderr, " %.2f", (tr[i] - tr[0]) * 1e-3);
+    fprintf(stderr, "\n");
+  }
   if (st) {
     st->transfer_in_s = g->transfer_in_s;
     st->rounds_s = rounds;
