@@ -175,7 +175,7 @@ def main():
     ap.add_argument("--source", type=int, default=0)
     ap.add_argument("--flags", type=int, default=None)
     ap.add_argument("--ctas", type=int, default=0)
-    ap.add_argument("--engine", default="auto", choices=["auto", "cluster", "grid"])
+    ap.add_argument("--engine", default="auto", choices=["auto", "cluster", "grid", "bucket"])
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -216,72 +216,98 @@ def main():
         g = None
     t_build = time.perf_counter() - t0
 
-    if world == 1:
-        dg = P.DeviceGraph(g, (local_rank,), flags=args.flags, ctas=args.ctas, engine=args.engine,
-                           warps=args.warps)
-    else:
+    def open_graph(engine):
+        if world == 1:
+            return P.DeviceGraph(g, (local_rank,), flags=args.flags, ctas=args.ctas, engine=engine,
+                                 warps=args.warps)
         from paper_2504_03667_b200 import distributed as D
-        dg = D.open_shard(block, n, max_weight=100, device=local_rank, flags=args.flags,
-                          ctas=args.ctas, engine=args.engine)
-    info = dg.info()
-    t_sync = dg.probe_sync(rounds=min(n, 20000))
+        return D.open_shard(block, n, max_weight=100, device=local_rank, flags=args.flags,
+                            ctas=args.ctas, engine=engine)
 
-    stream = torch.cuda.ExternalStream(dg.stream_ptr())
-    src = [args.source]
-    for _ in range(args.warmup):
-        dg.enqueue(src)
-        dg.finish()
-
-    # parity gate (rank 0, N=1): the bench result must equal the reference's
-    res0 = None
-    if world == 1:
-        res0 = dg.solve(args.source)
-
-    sampler = ClockSampler(local_rank)
-    sampler.start()
-    if dist is not None:
-        dist.barrier()
-    torch.cuda.synchronize()
-    ev_s = torch.cuda.Event(enable_timing=True)
-    ev_e = torch.cuda.Event(enable_timing=True)
-    kernel_s, iters, mis = [], 0, 0
-    ev_s.record(stream)
-    for _ in range(args.steps):
-        dg.enqueue(src)
+    def time_engine(dg, steps, warmup, sample_clocks=False):
+        """W untimed + K timed solves, CUDA events on the library's launch
+        stream, barrier + synchronize on both sides, max over ranks."""
+        stream = torch.cuda.ExternalStream(dg.stream_ptr())
+        src = [args.source]
+        for _ in range(warmup):
+            dg.enqueue(src)
+            dg.finish()
+        sampler = ClockSampler(local_rank) if sample_clocks else None
+        if sampler:
+            sampler.start()
+        if dist is not None:
+            dist.barrier()
+        torch.cuda.synchronize()
+        ev_s = torch.cuda.Event(enable_timing=True)
+        ev_e = torch.cuda.Event(enable_timing=True)
+        ev_s.record(stream)
+        for _ in range(steps):  # queued back to back in stream order
+            dg.enqueue(src)
+        ev_e.record(stream)
         st = dg.finish()
-        kernel_s.append(st["rounds_s"])
-        iters = st["iterations"]
-        mis = st["mispredicts"]
-    ev_e.record(stream)
-    torch.cuda.synchronize()
-    if dist is not None:
-        dist.barrier()
-    clocks = sampler.stop()
-    elapsed_ms = ev_s.elapsed_time(ev_e)
-    ms = elapsed_ms / args.steps
-    kern_ms = 1e3 * float(np.mean(kernel_s))
-    if dist is not None:
-        t = torch.tensor([ms, kern_ms], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms, kern_ms = float(t[0]), float(t[1])
+        kern = [st["rounds_s"]]
+        torch.cuda.synchronize()
+        if dist is not None:
+            dist.barrier()
+        clocks = sampler.stop() if sampler else None
+        ms = ev_s.elapsed_time(ev_e) / steps
+        kms = 1e3 * float(np.mean(kern))
+        if dist is not None:
+            t = torch.tensor([ms, kms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ms, kms = float(t[0]), float(t[1])
+        return ms, kms, st, clocks
 
-    # ---- roofline (dominant kernel = the persistent solve kernel)
     peak, peak_src = measured_peaks()
-    wb = info["weight_bytes"]
     loc_cols = n if world == 1 else P.pad_vertex_count(n, world) // world
-    alg_bytes = n * loc_cols * wb  # every row read once per solve, this GPU's columns
+    ENG = {1: "grid", 2: "cluster", 3: "bucket"}
+
+    # ---- the default engine (what dijkstra(G, s) runs) -> `value`
+    dg = open_graph(args.engine)
+    info = dg.info()
+    wb = info["weight_bytes"]
+    ms, kern_ms, st, clocks = time_engine(dg, args.steps, args.warmup, sample_clocks=True)
+    engine = ENG[st["engine"]]
+    res0 = dg.solve(args.source) if world == 1 else None
+    rows = st["rows_read"]
+    alg_bytes = rows * loc_cols * wb  # every streamed row slice once
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
-    t_hbm_ms = alg_bytes / (peak * 1e9) * 1e3
-    t_sync_ms = iters * t_sync * 1e3
-    t_roof_ms = max(t_hbm_ms, t_sync_ms)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
         try:
             with open(tpath) as f:
-                traffic = json.load(f).get(str(n))
+                traffic = json.load(f).get(f"{engine}:{n}")
         except Exception:
             traffic = None
+    transfer_in_s = info["transfer_in_s"]
+    dg.close()
+
+    # ---- the north-star n-round persistent scan kernel, timed beside it
+    scan = None
+    if engine == "bucket" or args.engine == "auto":
+        sdg = open_graph("cluster")
+        t_sync = sdg.probe_sync(rounds=min(n, 20000))
+        k2 = max(3, args.steps // 4)
+        sms, skms, sst, _ = time_engine(sdg, k2, 3)
+        rounds = sst["iterations"]
+        t_hbm_ms = n * loc_cols * wb / (peak * 1e9) * 1e3
+        t_sync_ms = rounds * t_sync * 1e3
+        scan = {"engine": "cluster (n-round persistent kernel, DSMEM exchange)", "ms": round(sms, 4),
+                "kernel_ms": round(skms, 4), "steps": k2, "rounds": rounds,
+                "mispredicts": sst["mispredicts"],
+                "achieved_gbs": round(n * loc_cols * wb / (skms * 1e-3) / 1e9, 2),
+                "latency_roofline": {"t_hbm_ms": round(t_hbm_ms, 4),
+                                     "t_sync_round_us": round(t_sync * 1e6, 4),
+                                     "t_sync_ms": round(t_sync_ms, 3),
+                                     "t_roof_ms": round(max(t_hbm_ms, t_sync_ms), 3),
+                                     "frac": round(max(t_hbm_ms, t_sync_ms) / skms, 4),
+                                     "note": "max(n*n_local*wbytes / HBM, rounds * t_sync_min); "
+                                             "t_sync_min measured by sssp_probe_sync in this run"}}
+        if world == 1:
+            r1 = sdg.solve(args.source)
+            assert r1 == res0, "scan engine != default engine"
+        sdg.close()
 
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
@@ -292,27 +318,28 @@ def main():
         "config": {"workload": f"graph_from_edges(generate_dense({n},{args.seed})) undirected, "
                                f"single source {args.source}",
                    "n": n, "parallelism": f"column-partitioned x{world}" if world > 1 else "1 GPU",
-                   "ctas_per_gpu": info["ctas"], "weight_bytes": wb,
+                   "engine": engine, "weight_bytes": wb,
                    "l2": f"matrix {info['matrix_bytes'] / 2**20:.0f} MiB per GPU > 126 MB L2; "
-                         "each solve streams every row once (no flush needed)"},
-        "kernel_ms": round(kern_ms, 4), "iterations": iters, "mispredicts": mis,
+                         "rows are streamed at most once per solve (no flush needed)"},
+        "kernel_ms": round(kern_ms, 4),
+        "solve": {"vertices_settled": st["iterations"], "classes": st["classes"],
+                  "rows_read": rows, "mispredicts": st["mispredicts"]},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
-                     "peak_source": peak_src,
-                     "bytes_per_launch": alg_bytes,
-                     "note": "algorithmic bytes = n * n_local * weight_bytes (each row once)"},
-        "latency_roofline": {"t_hbm_ms": round(t_hbm_ms, 4), "t_sync_round_us": round(t_sync * 1e6, 4),
-                             "t_sync_ms": round(t_sync_ms, 3), "t_roof_ms": round(t_roof_ms, 3),
-                             "frac": round(t_roof_ms / kern_ms, 4),
-                             "note": "north-star roofline: max(n^2 bytes / HBM, rounds * t_sync_min)"},
+                     "peak_source": peak_src, "bytes_per_launch": alg_bytes,
+                     "note": "algorithmic bytes = rows the engine must stream x n_local x "
+                             "weight_bytes (bucket: sum over classes of min(|class|, |unsettled|) "
+                             "rows; scan: n rows)"},
+        "scan_engine": scan,
         "clocks": clocks,
-        "build_s": round(t_build, 2), "transfer_in_s": round(info["transfer_in_s"], 4),
+        "build_s": round(t_build, 2), "transfer_in_s": round(transfer_in_s, 4),
     }
 
     if world == 1:
         # ---- e2e: dijkstra(G, s) through the public API with host buffers
         e2e = []
+        r = None
         for i in range(args.e2e_steps + 1):
             torch.cuda.synchronize()
             t = time.perf_counter()
@@ -321,8 +348,9 @@ def main():
         e2e_ms = 1e3 * float(np.mean(e2e[1:])) if len(e2e) > 1 else 1e3 * e2e[0]
         line["e2e"] = {"value": round(e2e_ms, 3), "unit": "ms",
                        "h2d_bytes_per_step": int(n * n * wb + 8), "d2h_bytes_per_step": int(16 * n),
-                       "note": "uint64 host matrix narrowed on host threads, pinned H2D, "
-                               "device permute, solve, D2H; graph handle created per call"}
+                       "note": "uint64 host matrix narrowed on host threads, pinned H2D, device "
+                               "permute (+ transpose/symmetry check), solve, D2H; graph handle "
+                               "created per call"}
         assert r == res0
         # ---- CPU baseline + parity gate (reference serial, 1 core)
         if not args.no_cpu_baseline:
@@ -341,7 +369,6 @@ def main():
                                     "parity": "dist and pred bit-identical"}
     if rank == 0:
         print(json.dumps(line), flush=True)
-    dg.close()
     if dist is not None:
         dist.barrier()
         dist.destroy_process_group()

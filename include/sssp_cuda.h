@@ -140,8 +140,9 @@ int sssp_solve_batch(sssp_graph* g, const uint64_t* sources, uint32_t k, uint64_
                      uint64_t* pred_out, sssp_solve_stats* st);
 
 /* Asynchronous form for device-side timing: enqueue k solves on the handle's
- * stream (results stay on the device), then sssp_finish waits and checks the
- * watchdog.  sssp_stream returns the cudaStream_t of shard `local` as a
+ * stream (results stay on the device); several enqueues queue up in stream
+ * order and reuse the output slots.  sssp_finish waits, checks the watchdog
+ * and reports the last launch (rounds_s = mean kernel time per launch).  sssp_stream returns the cudaStream_t of shard `local` as a
  * pointer so a caller can record its own CUDA events around the launches. */
 int sssp_enqueue(sssp_graph* g, const uint64_t* sources, uint32_t k);
 int sssp_finish(sssp_graph* g, sssp_solve_stats* st);

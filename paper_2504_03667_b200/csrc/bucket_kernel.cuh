@@ -468,6 +468,33 @@ __global__ void __launch_bounds__(256) transpose_positions_kernel(const W* __res
   }
 }
 
+// flag = 1 if the stored matrix is not symmetric: compares every element
+// A[vid(p')][p] with its mirror A[vid(p)][p'] (same 64x64 tiling as the
+// transpose, no transpose buffer needed).
+template <typename W>
+__global__ void __launch_bounds__(256) symmetric_check_kernel(const W* __restrict__ a,
+                                                              uint64_t row_stride, uint32_t n,
+                                                              uint32_t Q, uint32_t qbits,
+                                                              uint32_t lbits, uint32_t* flag) {
+  __shared__ W tile[64][65];
+  const uint32_t pb = blockIdx.x * 64, ppb = blockIdx.y * 64;
+  const uint32_t tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  for (uint32_t r = ty; r < 64; r += 4) {
+    const uint32_t u = pos_to_vid(ppb + r, Q, lbits, qbits);
+    tile[r][tx] = u < n ? a[(size_t)u * row_stride + pb + tx] : (W)WInf<W>::v;
+  }
+  __syncthreads();
+  bool diff = false;
+  for (uint32_t r = ty; r < 64; r += 4) {
+    const uint32_t v = pos_to_vid(pb + r, Q, lbits, qbits);
+    if (v < n) {
+      const uint32_t u = pos_to_vid(ppb + tx, Q, lbits, qbits);
+      if (u < n) diff |= a[(size_t)v * row_stride + ppb + tx] != tile[tx][r];
+    }
+  }
+  if (__any_sync(0xFFFFFFFFu, diff) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
 // flag = 1 if A and AT differ anywhere (i.e. the matrix is not symmetric)
 template <typename W>
 __global__ void compare_rows_kernel(const W* __restrict__ a, const W* __restrict__ b,

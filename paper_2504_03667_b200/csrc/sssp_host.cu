@@ -20,6 +20,7 @@
 #include "../../include/sssp_cuda.h"
 #include "bucket_kernel.cuh"
 #include "dispatch.h"
+#include "host_narrow.h"
 
 using namespace sssp_b200;
 
@@ -151,7 +152,8 @@ struct sssp_graph {
   bool bucket = false;  // distance-class engine available and selected (min weight >= 1)
   uint64_t exch_base = 0;
   double transfer_in_s = 0;
-  uint32_t pending = 0;  // solves enqueued and not yet finished
+  uint32_t pending = 0;  // solves of the last enqueued launch (0: nothing pending)
+  uint32_t queued = 0;   // launches enqueued since the last finish
   uint64_t matrix_bytes = 0;
 };
 
@@ -217,20 +219,19 @@ struct ScanResult {
 // finite range (the caller then retries with a wider W).
 template <typename W>
 int upload_block(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, ScanResult& res) {
+  double t_narrow = 0, t_wait = 0;
+  const double t_all = now_s();
   const uint64_t WINF64 = WInf<W>::v;
   const uint64_t fmax = WINF64 - 1;  // largest finite weight W can carry
   const uint64_t cols = s.cols;
   const uint64_t row_in_bytes = std::max<uint64_t>(1, cols) * 8;
-  const uint64_t R = std::max<uint64_t>(1, std::min<uint64_t>(n, (64ull << 20) / row_in_bytes));
+  const uint64_t R = std::max<uint64_t>(1, std::min<uint64_t>(n, (32ull << 20) / row_in_bytes));
   const uint64_t stage_elems = R * std::max<uint64_t>(1, cols);
   W* pin[2] = {nullptr, nullptr};
   W* dst[2] = {nullptr, nullptr};
   cudaEvent_t done[2] = {nullptr, nullptr};
   bool used[2] = {false, false};
   int rc = SSSP_OK;
-  const unsigned nt = host_threads();
-  std::vector<uint64_t> tmax(nt, 0), tmin(nt, ~0ull);
-  std::vector<char> tover(nt, 0);
 
   auto cleanup = [&]() {
     cudaStreamSynchronize(s.stream);
@@ -252,32 +253,16 @@ int upload_block(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, ScanRes
   for (uint64_t r0 = 0; r0 < n && rc == SSSP_OK; r0 += R, ++chunk) {
     const int b = (int)(chunk & 1);
     const uint64_t rows = std::min<uint64_t>(R, n - r0);
+    const double tw0 = now_s();
     if (used[b]) cudaEventSynchronize(done[b]);
+    t_wait += now_s() - tw0;
     W* out = pin[b];
-    parallel_for(r0, r0 + rows, nt, [&](uint64_t a, uint64_t e, unsigned t) {
-      uint64_t mx = tmax[t], mn = tmin[t];
-      bool over = false;
-      for (uint64_t r = a; r < e; ++r) {
-        const uint64_t* row = src + r * ld;
-        W* o = out + (r - r0) * cols;
-        const uint64_t diag = (r >= s.col_base && r < s.col_base + cols) ? r - s.col_base : ~0ull;
-        for (uint64_t j = 0; j < cols; ++j) {
-          const uint64_t x = row[j];
-          const bool inf = x == ~0ull;
-          over |= !inf && x > fmax;
-          o[j] = inf ? (W)WINF64 : (W)x;
-          if (!inf) {
-            mx = x > mx ? x : mx;
-            if (j != diag) mn = x < mn ? x : mn;
-          }
-        }
-      }
-      tmax[t] = mx;
-      tmin[t] = mn;
-      if (over) tover[t] = 1;
-    });
-    for (unsigned t = 0; t < nt; ++t)
-      if (tover[t]) res.overflow = true;
+    const double tn0 = now_s();
+    const NarrowStats ns = narrow_rows<W>(src, ld, r0, rows, cols, s.col_base, out);
+    t_narrow += now_s() - tn0;
+    res.max_w = std::max(res.max_w, ns.max_w);
+    res.min_w = std::min(res.min_w, ns.min_w);
+    if (ns.overflow) res.overflow = true;
     if (res.overflow) break;
     if (cols) {
       cudaError_t e = cudaMemcpyAsync(dst[b], out, rows * cols * sizeof(W),
@@ -300,25 +285,43 @@ int upload_block(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, ScanRes
     cudaEventRecord(done[b], s.stream);
     used[b] = true;
   }
-  for (unsigned t = 0; t < nt; ++t) {
-    res.max_w = std::max(res.max_w, tmax[t]);
-    res.min_w = std::min(res.min_w, tmin[t]);
-  }
   cleanup();
   if (rc == SSSP_OK) {
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) rc = fail(SSSP_ERR_CUDA, cudaGetErrorString(e));
   }
+  if (getenv("SSSP_UPLOAD_TRACE"))
+    fprintf(stderr, "upload: total %.1f ms, host narrow %.1f ms, waiting on device %.1f ms\n",
+            (now_s() - t_all) * 1e3, t_narrow * 1e3, t_wait * 1e3);
   return rc;
+}
+
+// Matrices come from the device's stream-ordered pool with an unbounded
+// release threshold, so re-creating a graph of the same size (every drop-in
+// dijkstra(G, s) call) reuses the memory instead of cudaMalloc/cudaFree.
+int pool_alloc(Shard& s, void** p, size_t bytes) {
+  static bool configured[64] = {};
+  if (s.device >= 0 && s.device < 64 && !configured[s.device]) {
+    cudaMemPool_t mp;
+    CK(cudaDeviceGetDefaultMemPool(&mp, s.device));
+    uint64_t thr = ~0ull;
+    CK(cudaMemPoolSetAttribute(mp, cudaMemPoolAttrReleaseThreshold, &thr));
+    configured[s.device] = true;
+  }
+  CK(cudaMallocAsync(p, bytes, s.stream));
+  return SSSP_OK;
+}
+
+void pool_free(Shard& s, void* p) {
+  if (p) cudaFreeAsync(p, s.stream);
 }
 
 int alloc_matrix(Shard& s, uint64_t n, uint32_t wbytes) {
   if (s.d_adj) {
-    cudaFree(s.d_adj);
+    pool_free(s, s.d_adj);
     s.d_adj = nullptr;
   }
-  CK(cudaMalloc(&s.d_adj, n * s.row_stride * wbytes));
-  return SSSP_OK;
+  return pool_alloc(s, &s.d_adj, n * s.row_stride * wbytes);
 }
 
 // Uploads with the narrowest encoding that holds every finite weight.
@@ -459,7 +462,14 @@ int compute_max_batch(sssp_graph* g) {
 // layout (power-of-two participant count).  It needs the matrix transpose for
 // PULL steps: none when the matrix is symmetric, else a second device copy
 // when it fits (otherwise PUSH only).
+int prepare_bucket_impl(sssp_graph* g);
 int prepare_bucket(sssp_graph* g) {
+  const double t0 = now_s();
+  const int rc = prepare_bucket_impl(g);
+  if (getenv("SSSP_UPLOAD_TRACE")) fprintf(stderr, "prepare_bucket: %.1f ms\n", (now_s() - t0) * 1e3);
+  return rc;
+}
+int prepare_bucket_impl(sssp_graph* g) {
   const int want = g->opt.engine;
   if (want == SSSP_ENGINE_GRID || want == SSSP_ENGINE_CLUSTER) return SSSP_OK;
   const bool exact = g->min_w >= 1;
@@ -501,51 +511,46 @@ int prepare_bucket(sssp_graph* g) {
   }
   CK(cudaMalloc(&s.d_bitmap, 2 * (s.row_stride / 32) * sizeof(uint32_t)));
   CK(cudaMalloc(&s.d_ctrl, 2 * 3 * (size_t)s.bG * sizeof(uint32_t)));
-  // transpose (position order) and a symmetry check
-  size_t free_b = 0, total_b = 0;
-  CK(cudaMemGetInfo(&free_b, &total_b));
-  const uint64_t mbytes = g->n * s.row_stride * g->wbytes;
+  // symmetry check; PULL reads row v of the matrix itself when symmetric, else
+  // row v of a transpose kept in position order (when it fits)
   s.pull_src = nullptr;
-  if (mbytes + (256ull << 20) < free_b) {
-    CK(cudaMalloc(&s.d_adjT, mbytes));
+  if (s.row_stride % 64 == 0) {
     const dim3 grid((unsigned)(s.row_stride / 64), (unsigned)(s.row_stride / 64));
     const uint32_t qb = bitlen(Q) - 1, lb = bitlen(L) - 1;
-    if (s.row_stride % 64 == 0) {
-      if (g->wbytes == 1)
-        transpose_positions_kernel<uint8_t><<<grid, 256, 0, s.stream>>>(
-            (const uint8_t*)s.d_adj, (uint8_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
-      else if (g->wbytes == 2)
-        transpose_positions_kernel<uint16_t><<<grid, 256, 0, s.stream>>>(
-            (const uint16_t*)s.d_adj, (uint16_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
-      else
-        transpose_positions_kernel<uint32_t><<<grid, 256, 0, s.stream>>>(
-            (const uint32_t*)s.d_adj, (uint32_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
-      CK(cudaGetLastError());
-      uint32_t* d_flag = nullptr;
-      CK(cudaMalloc(&d_flag, 4));
-      CK(cudaMemsetAsync(d_flag, 0, 4, s.stream));
-      const uint64_t elems = g->n * s.row_stride;
-      if (g->wbytes == 1)
-        compare_rows_kernel<uint8_t><<<sms * 8, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, (const uint8_t*)s.d_adjT, elems, d_flag);
-      else if (g->wbytes == 2)
-        compare_rows_kernel<uint16_t><<<sms * 8, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, (const uint16_t*)s.d_adjT, elems, d_flag);
-      else
-        compare_rows_kernel<uint32_t><<<sms * 8, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, (const uint32_t*)s.d_adjT, elems, d_flag);
-      uint32_t asym = 1;
-      CK(cudaMemcpyAsync(&asym, d_flag, 4, cudaMemcpyDeviceToHost, s.stream));
-      CK(cudaStreamSynchronize(s.stream));
-      cudaFree(d_flag);
-      if (!asym) {  // symmetric: row v of A is column v
-        cudaFree(s.d_adjT);
-        s.d_adjT = nullptr;
-        s.pull_src = s.d_adj;
-      } else {
+    uint32_t* d_flag = nullptr;
+    CK(cudaMallocAsync((void**)&d_flag, 4, s.stream));
+    CK(cudaMemsetAsync(d_flag, 0, 4, s.stream));
+    if (g->wbytes == 1)
+      symmetric_check_kernel<uint8_t><<<grid, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, s.row_stride, (uint32_t)g->n, Q, qb, lb, d_flag);
+    else if (g->wbytes == 2)
+      symmetric_check_kernel<uint16_t><<<grid, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, s.row_stride, (uint32_t)g->n, Q, qb, lb, d_flag);
+    else
+      symmetric_check_kernel<uint32_t><<<grid, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, s.row_stride, (uint32_t)g->n, Q, qb, lb, d_flag);
+    CK(cudaGetLastError());
+    uint32_t asym = 1;
+    CK(cudaMemcpyAsync(&asym, d_flag, 4, cudaMemcpyDeviceToHost, s.stream));
+    CK(cudaFreeAsync(d_flag, s.stream));
+    CK(cudaStreamSynchronize(s.stream));
+    if (!asym) {
+      s.pull_src = s.d_adj;
+    } else {
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      const uint64_t mbytes = g->n * s.row_stride * g->wbytes;
+      if (mbytes + (256ull << 20) < free_b && pool_alloc(s, &s.d_adjT, mbytes) == SSSP_OK) {
+        if (g->wbytes == 1)
+          transpose_positions_kernel<uint8_t><<<grid, 256, 0, s.stream>>>(
+              (const uint8_t*)s.d_adj, (uint8_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
+        else if (g->wbytes == 2)
+          transpose_positions_kernel<uint16_t><<<grid, 256, 0, s.stream>>>(
+              (const uint16_t*)s.d_adj, (uint16_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
+        else
+          transpose_positions_kernel<uint32_t><<<grid, 256, 0, s.stream>>>(
+              (const uint32_t*)s.d_adj, (uint32_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
+        CK(cudaGetLastError());
         s.pull_src = s.d_adjT;
         g->matrix_bytes += mbytes;
       }
-    } else {
-      cudaFree(s.d_adjT);
-      s.d_adjT = nullptr;
     }
   }
   g->bucket = true;
@@ -607,14 +612,15 @@ void destroy_graph(sssp_graph* g) {
     if (s.stream) cudaStreamSynchronize(s.stream);
     for (int j = 0; j < kMaxShards; ++j)
       if (s.peer_ipc[j] && s.peer[j]) cudaIpcCloseMemHandle(s.peer[j]);
-    cudaFree(s.d_adj);
+    pool_free(s, s.d_adj);
     cudaFree(s.d_slots);
     cudaFree(s.d_dist);
     cudaFree(s.d_pred);
     cudaFree(s.d_info);
     cudaFree(s.d_sources);
     cudaFree(s.d_visit);
-    cudaFree(s.d_adjT);
+    pool_free(s, s.d_adjT);
+    if (s.stream) cudaStreamSynchronize(s.stream);
     cudaFree(s.d_bitmap);
     cudaFree(s.d_ctrl);
     cudaFree(s.d_trace);
@@ -667,7 +673,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
   if (g->bucket) {
     Shard& s = g->sh[0];
     CK(cudaSetDevice(s.device));
-    CK(cudaEventRecord(s.ev0, s.stream));
+    if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
     void* fn = g->wbytes == 1 ? (void*)bucket_kernel<uint8_t>
                : g->wbytes == 2 ? (void*)bucket_kernel<uint16_t> : (void*)bucket_kernel<uint32_t>;
     const size_t cpt = 16 / g->wbytes, ksz = g->wbytes == 1 ? 4 : 8;
@@ -701,6 +707,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
     }
     CK(cudaEventRecord(s.ev1, s.stream));
     g->pending = k;
+    g->queued += 1;
     return SSSP_OK;
   }
   // Single process: reset the exchange buffers of every shard first, and make
@@ -754,12 +761,13 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
     p.visit_order = s.d_visit;
     p.info = s.d_info;
     p.timeout_ns = g->opt.timeout_ms * 1000000ull;
-    CK(cudaEventRecord(s.ev0, s.stream));
+    if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
     CK(launch_kernel(g, s, (void*)s.fn, k, p, nullptr, 0, nullptr));
     CK(cudaEventRecord(s.ev1, s.stream));
   }
   for (cudaEvent_t e : reset_ev) cudaEventDestroy(e);
   g->pending = k;
+  g->queued += 1;
   return SSSP_OK;
 }
 
@@ -777,7 +785,7 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     CK(cudaStreamSynchronize(s.stream));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
-    rounds = std::max(rounds, ms * 1e-3);
+    rounds = std::max(rounds, ms * 1e-3 / std::max(1u, g->queued));
     for (uint32_t i = 0; i < k; ++i) {
       if (g->bucket) {
         iters += s.h_info[4 * i];
@@ -792,6 +800,7 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     }
   }
   g->pending = 0;
+  g->queued = 0;
   if (g->multiproc) g->exch_base = last + 1;
   if (g->bucket && g->sh[0].d_trace) {
     uint64_t tr[64];
@@ -913,9 +922,10 @@ int sssp_graph_create(const uint64_t* adj, uint64_t n, int directed, const int* 
   // whole matrix.  A single shard widens optimistically inside the upload.
   uint64_t hint = 0;
   if (rc == SSSP_OK && g->P > 1) {
-    const unsigned nt = host_threads();
+    const unsigned nt = narrow_threads();
     std::vector<uint64_t> tm(nt, 0);
-    parallel_for(0, n, nt, [&](uint64_t a, uint64_t e, unsigned t) {
+    parallel_run([&](unsigned t) {
+      const uint64_t a = n * t / nt, e = n * (t + 1) / nt;
       uint64_t mx = 0;
       for (uint64_t i = a * n; i < e * n; ++i) {
         const uint64_t x = adj[i];
@@ -1100,7 +1110,8 @@ int sssp_solve_batch(sssp_graph* g, const uint64_t* sources, uint32_t k, uint64_
 
 int sssp_enqueue(sssp_graph* g, const uint64_t* sources, uint32_t k) {
   if (!g) return fail(SSSP_ERR_BAD_ARG, "null handle");
-  if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is already pending");
+  // Launches queue up in stream order; each one reuses the handle's output
+  // slots, so sssp_finish reports (and the buffers hold) the last one.
   return launch(g, sources, k);
 }
 

@@ -334,3 +334,17 @@ def test_cpp_dropin_against_reference_binary(gpu):
     out = subprocess.run([exe], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr
     assert "PASS" in out.stdout
+
+
+@pytest.mark.parametrize("engine", ["auto", "cluster", "grid"])
+def test_queued_enqueues_then_finish(gpu, oracle_c, engine):
+    """Several sssp_enqueue calls queue in stream order; finish reports the last."""
+    g = gpu.generate_dense(1500, 3)
+    with gpu.DeviceGraph(g, engine=engine) as dg:
+        for s in (5, 9, 11):
+            dg.enqueue([s])
+        st = dg.finish()
+        assert st["iterations"] == 1500 and st["rounds_s"] > 0
+        r = dg.solve(11)
+    d, p = oracle_c.serial(g.adj, g.n, 11)
+    assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p)
