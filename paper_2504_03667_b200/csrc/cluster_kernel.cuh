@@ -502,21 +502,254 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
   cluster_sync_all();  // no CTA leaves while a peer could still address its smem
 }
 
+// Hierarchical variant (flag kFlagHier): each CTA first reduces its NW warp
+// keys through shared memory (one named barrier), and only the C CTA minima
+// are all-gathered over DSMEM -- C stores per CTA per round instead of C*NW,
+// and C keys to poll (ubench: a 16-participant DSMEM all-gather costs ~380
+// cycles vs ~590 for 64).  Participant q = warp*C + cta_rank, so consecutive
+// vertex ids fall on consecutive CTAs and the runner-up CTA minimum is still
+// the likely next winner.  PACKED state only (the host falls back otherwise).
+template <typename W, int EPL, int NW>
+__global__ void __launch_bounds__(NW * 32, 1) cluster_hier_kernel(const ScanParams p) {
+  using Row = RowSlice<W, EPL>;
+  constexpr uint32_t WINF = WInf<W>::v;
+  constexpr uint32_t DINF = 0xFFFFFFFFu;
+  constexpr uint32_t L = 32u * EPL;
+  constexpr uint32_t SB = (L == 128 ? 7 : L == 256 ? 8 : L == 512 ? 9 : 10);
+  static_assert((1u << SB) == L, "L must be a power of two");
+
+  extern __shared__ uint32_t s_pred[];  // [NW][L]
+  __shared__ __align__(16) uint64_t s_keys[2][16];   // CTA minima of the round, by CTA rank
+  __shared__ __align__(16) uint64_t s_wk[2][NW];     // warp keys of this CTA
+
+  const int lane = threadIdx.x & 31;
+  const uint32_t warp = threadIdx.x >> 5;
+  const uint32_t cr = cluster_ctarank();
+  const uint32_t csize = cluster_nctarank();
+  const uint32_t Q = p.G;  // = csize * NW, a power of two
+  const uint32_t qbits = 31u - __clz(Q);
+  const uint32_t solve = blockIdx.x / csize;
+  const uint32_t q = warp * csize + cr;
+  const uint32_t tb = 32u - p.vbits;
+  const uint64_t tagmask = (1ull << tb) - 1ull;
+  const uint32_t vmask_all = (p.vbits >= 32) ? 0xFFFFFFFFu : ((1u << p.vbits) - 1u);
+  const bool multi = p.nshards > 1;
+  const W* const adj = static_cast<const W*>(p.adj) + (size_t)q * L;
+  const bool pf_reg = (p.flags & kFlagPrefetchReg) != 0;
+  const bool pf_l2 = (p.flags & kFlagPrefetchL2) != 0;
+  uint32_t* const pred = s_pred + warp * L;
+  uint64_t* const dout = p.dist_out + (size_t)solve * p.loc_n;
+  uint64_t* const pout = p.pred_out + (size_t)solve * p.loc_n;
+  const uint32_t lbase = (uint32_t)lane * Row::VEC;
+
+  const uint32_t source = p.sources[solve];
+  uint32_t ek[EPL];
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const uint32_t s = Row::slot(e, lane);
+    const uint32_t vl = (s << qbits) | q;
+    const bool pad = vl >= p.loc_n || p.col_base + vl >= p.n;
+    ek[e] = pad ? 0u : (p.col_base + vl == source) ? s + 1u : DINF;
+  }
+  for (uint32_t i = lane; i < L; i += 32) pred[i] = 0xFFFFFFFFu;
+  for (uint32_t i = threadIdx.x; i < 2 * 16; i += NW * 32) (&s_keys[0][0])[i] = 0;
+  cluster_sync_all();
+
+  uint32_t u = source, du = 0;
+  uint64_t E = p.exch_base, iters = 0, mispredicts = 0;
+  uint32_t pred_u = 0xFFFFFFFFu;
+  Row cur, nxt;
+  cur.load(adj + (size_t)u * p.row_stride, lane);
+  uint64_t ck = ~0ull;  // this lane's gathered CTA key (lanes < csize)
+  uint64_t best_key = 0;
+  const uint64_t t_start = globaltimer();
+  bool failed = false;
+  const uint32_t keys_base = (uint32_t)__cvta_generic_to_shared(&s_keys[0][0]);
+
+  auto next_key = [&](uint64_t after) -> uint64_t {
+    const uint64_t r = (ck > after) ? ck : ~0ull;
+    uint32_t a = (uint32_t)(r >> 32), b = (uint32_t)r;
+    warp_lexmin(a, b);
+    return ((uint64_t)a << 32) | b;
+  };
+
+  while (true) {
+    // ---- owner marks u visited, records its final distance
+    {
+      const uint32_t ul = u - p.col_base;
+      if (u >= p.col_base && ul < p.loc_n && (ul & (Q - 1)) == q) {
+        const uint32_t su = ul >> qbits;
+        if ((uint32_t)lane == ((su / Row::VEC) & 31u)) {
+          const uint32_t eu = (su / (32u * Row::VEC)) * Row::VEC + su % Row::VEC;
+#pragma unroll
+          for (int e = 0; e < EPL; ++e)
+            if ((uint32_t)e == eu) ek[e] = 0u;
+          dout[ul] = du;
+        }
+      }
+    }
+    // ---- relax (serial.hpp:51-60)
+    {
+      const uint32_t dus1 = (du << SB) + 1u + lbase;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) {
+        const uint32_t w = cur.elem(e);
+        const uint32_t nk = w * L + dus1 + (Row::slot(e, 0));
+        if (w != WINF && nk < ek[e]) {
+          ek[e] = nk;
+          pred[Row::slot(e, 0) | lbase] = u;
+        }
+      }
+    }
+    ++iters;
+    if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
+      p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
+
+    // ---- warp election, then the CTA minimum through shared memory
+    ++E;
+    const uint32_t buf = (uint32_t)(E & 1ull);
+    const uint64_t want = E & tagmask;
+    {
+      uint32_t k = 0xFFFFFFFFu;
+#pragma unroll
+      for (int e = 0; e < EPL; ++e) k = min(k, ek[e] - 1u);
+      k = __reduce_min_sync(0xFFFFFFFFu, k);
+      const bool none = k >= 0xFFFFFFFEu || (k >> SB) == (DINF >> SB);
+      const uint32_t bd = none ? DINF : (k >> SB);
+      const uint32_t bv = none ? vmask_all : (p.col_base + (((k & (L - 1u)) << qbits) | q));
+      if (lane == 0) s_wk[buf][warp] = ((uint64_t)bd << 32) | ((uint64_t)(bv & vmask_all) << tb);
+    }
+    asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+    if (warp == 0) {
+      uint64_t m = (uint32_t)lane < NW ? s_wk[buf][lane] : ~0ull;
+      uint32_t a = (uint32_t)(m >> 32), b = (uint32_t)m;
+      warp_lexmin(a, b);
+      const uint64_t key = ((uint64_t)a << 32) | b | want;
+      // ---- publish the CTA minimum into every CTA's exchange array (DSMEM)
+      if ((uint32_t)lane < csize) st_dsmem(keys_base + (buf * 16 + cr) * 8u, (uint32_t)lane, key);
+    }
+
+    // ---- off the critical path: runner-up row into registers, third into L2
+    if (pf_reg) {
+      const uint64_t r2 = next_key(best_key);
+      if ((uint32_t)(r2 >> 32) != DINF && iters > 1) {
+        pred_u = (uint32_t)(r2 & 0xFFFFFFFFull) >> tb;
+        nxt.load(adj + (size_t)pred_u * p.row_stride, lane);
+        if (pf_l2) {
+          const uint64_t r3 = next_key(r2);
+          if ((uint32_t)(r3 >> 32) != DINF) {
+            const uint32_t v3 = (uint32_t)(r3 & 0xFFFFFFFFull) >> tb;
+            const uint8_t* b3 = reinterpret_cast<const uint8_t*>(adj + (size_t)v3 * p.row_stride);
+#pragma unroll
+            for (int k2 = 0; k2 < Row::NCH; ++k2)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(b3 + (size_t)(k2 * 32 + lane) * Row::CB));
+          }
+        }
+      } else {
+        pred_u = 0xFFFFFFFFu;
+      }
+    }
+
+    // ---- gather the C CTA minima from my own shared memory
+    {
+      const uint32_t addr = keys_base + (buf * 16 + (uint32_t)lane) * 8u;
+      const uint32_t want32 = (uint32_t)want, tm32 = (uint32_t)tagmask;
+      uint32_t polls = 0;
+      while (true) {
+        uint64_t v = ~0ull;
+        if ((uint32_t)lane < csize)
+          asm volatile("ld.relaxed.cluster.shared::cta.u64 %0, [%1];" : "=l"(v) : "r"(addr) : "memory");
+        const bool ok = (uint32_t)lane >= csize || (((uint32_t)v & tm32) == want32);
+        if (__all_sync(0xFFFFFFFFu, ok)) {
+          ck = (uint32_t)lane < csize ? (v & ~tagmask) : ~0ull;
+          break;
+        }
+        if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) {
+          failed = true;
+          break;
+        }
+      }
+    }
+    if (failed) break;
+    {
+      uint32_t a = (uint32_t)(ck >> 32), b = (uint32_t)ck;
+      warp_lexmin(a, b);
+      best_key = ((uint64_t)a << 32) | b;
+    }
+    if (multi) {
+      const uint64_t tagged = best_key | want;
+      if (q == 0 && (uint32_t)lane < p.nshards)
+        st_slot(p.peer_slots[lane] + (uint64_t)solve * p.slot_stride + (uint64_t)buf * p.bstride +
+                    p.shard,
+                tagged, true);
+      const uint64_t* mb = p.slots + (uint64_t)solve * p.slot_stride + (uint64_t)buf * p.bstride;
+      uint64_t mk = ~0ull;
+      uint32_t polls = 0;
+      while (true) {
+        mk = (uint32_t)lane < p.nshards ? ld_slot(mb + lane, true) : ~0ull;
+        const bool ok = (uint32_t)lane >= p.nshards || (mk & tagmask) == want;
+        if (__all_sync(0xFFFFFFFFu, ok)) break;
+        if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) {
+          failed = true;
+          break;
+        }
+      }
+      if (failed) break;
+      mk = (uint32_t)lane < p.nshards ? (mk & ~tagmask) : ~0ull;
+      uint32_t a = (uint32_t)(mk >> 32), b = (uint32_t)mk;
+      warp_lexmin(a, b);
+      best_key = ((uint64_t)a << 32) | b;
+    }
+    du = (uint32_t)(best_key >> 32);
+    if (du == DINF) break;
+    u = (uint32_t)(best_key & 0xFFFFFFFFull) >> tb;
+    if (pf_reg && u == pred_u) {
+      cur = nxt;
+    } else {
+      if (pf_reg) ++mispredicts;
+      cur.load(adj + (size_t)u * p.row_stride, lane);
+    }
+  }
+
+  __syncwarp();
+#pragma unroll
+  for (int e = 0; e < EPL; ++e) {
+    const uint32_t s = Row::slot(e, lane);
+    const uint32_t vl = (s << qbits) | q;
+    if (vl < p.loc_n && p.col_base + vl < p.n) {
+      if (ek[e] != 0u) dout[vl] = ~0ull;
+      const uint32_t pr = pred[s];
+      pout[vl] = pr == 0xFFFFFFFFu ? ~0ull : (uint64_t)pr;
+    }
+  }
+  uint64_t* inf = p.info + (size_t)solve * 4;
+  if (failed && lane == 0) atomicOr((unsigned long long*)(inf + 2), 1ull);
+  if (q == 0 && lane == 0) {
+    inf[0] = iters;
+    inf[1] = E;
+    inf[3] = mispredicts;
+  }
+  cluster_sync_all();
+}
+
 // t_sync microbenchmark for the cluster exchange (same code, no relax).
-template <int NW>
+// HIER = the hierarchical variant: named barrier, warp 0 publishes the CTA
+// key, every warp polls the C CTA keys.
+template <int NW, bool HIER = false>
 __global__ void __launch_bounds__(NW * 32, 1) cluster_probe_kernel(const ScanParams p,
                                                                   uint32_t rounds,
                                                                   uint64_t* out_ns) {
   constexpr int NP = NW / 4;
   constexpr uint32_t QMAX = 16u * NW;
   __shared__ __align__(16) uint64_t s_keys[2][QMAX];
+  __shared__ __align__(16) uint64_t s_wk[2][NW];
   const int lane = threadIdx.x & 31;
   const uint32_t warp = threadIdx.x >> 5;
   const uint32_t cr = cluster_ctarank();
   const uint32_t csize = cluster_nctarank();
-  const uint32_t Q = p.G;
+  const uint32_t Q = HIER ? csize : p.G;  // participants of the DSMEM exchange
   const uint32_t solve = blockIdx.x / csize;
-  const uint32_t q = cr * NW + warp;
+  const uint32_t q = HIER ? cr : cr * NW + warp;
   const uint32_t tb = 32u - p.vbits;
   const uint64_t tagmask = (1ull << tb) - 1ull;
   const bool multi = p.nshards > 1;
@@ -531,9 +764,22 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_probe_kernel(const ScanPar
     ++E;
     const uint32_t buf = (uint32_t)(E & 1ull);
     const uint64_t want = E & tagmask;
-    const uint32_t dist = (r * 2654435761u + q * 40503u) >> 20;
-    const uint64_t key = ((uint64_t)dist << 32) | ((uint64_t)(p.shard * Q + q) << tb) | want;
-    if ((uint32_t)lane < csize) st_dsmem(keys_base + (buf * QMAX + q) * 8u, (uint32_t)lane, key);
+    const uint32_t dist = (r * 2654435761u + (cr * NW + warp) * 40503u) >> 20;
+    uint64_t key = ((uint64_t)dist << 32) | ((uint64_t)(p.shard * p.G + cr * NW + warp) << tb);
+    if (HIER) {
+      if (lane == 0) s_wk[buf][warp] = key;
+      asm volatile("bar.sync 1, %0;" ::"r"(NW * 32) : "memory");
+      if (warp == 0) {
+        uint64_t m = (uint32_t)lane < NW ? s_wk[buf][lane] : ~0ull;
+        uint32_t a = (uint32_t)(m >> 32), b = (uint32_t)m;
+        warp_lexmin(a, b);
+        key = ((uint64_t)a << 32) | b | want;
+        if ((uint32_t)lane < csize) st_dsmem(keys_base + (buf * QMAX + q) * 8u, (uint32_t)lane, key);
+      }
+    } else {
+      key |= want;
+      if ((uint32_t)lane < csize) st_dsmem(keys_base + (buf * QMAX + q) * 8u, (uint32_t)lane, key);
+    }
     const uint32_t arr = keys_base + buf * QMAX * 8u;
     uint32_t polls = 0;
     while (true) {
@@ -561,7 +807,7 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_probe_kernel(const ScanPar
     if (failed) break;
     uint64_t best = min_key<NP>(ks);
     if (multi) {
-      if (q == 0 && (uint32_t)lane < p.nshards)
+      if (cr == 0 && warp == 0 && (uint32_t)lane < p.nshards)
         st_slot(p.peer_slots[lane] + (uint64_t)solve * p.slot_stride + (uint64_t)buf * p.bstride +
                     p.shard,
                 best, true);
@@ -583,7 +829,7 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_probe_kernel(const ScanPar
     }
     acc += best >> 32;
   }
-  if (q == 0 && lane == 0) {
+  if (cr == 0 && warp == 0 && lane == 0) {
     out_ns[solve] = failed ? ~0ull : globaltimer() - t0;
     p.info[solve * 4 + 1] = E;
     p.info[solve * 4 + 0] = acc;

@@ -15,6 +15,8 @@ ProbeFn get_grid_probe(int np);
 
 // cluster engine (cluster_kernel.cuh): one cluster per solve, DSMEM exchange
 KernelFn get_cluster_kernel(int wbytes, int epl, int nw, bool packed);
-ProbeFn get_cluster_probe(int nw);
+ProbeFn get_cluster_probe(int nw, bool hier);
+// hierarchical cluster variant (CTA pre-reduction, PACKED state only)
+KernelFn get_cluster_hier_kernel(int wbytes, int epl, int nw);
 
 }  // namespace sssp_b200

@@ -42,11 +42,42 @@ KernelFn get_cluster_kernel(int wbytes, int epl, int nw, bool packed) {
   return packed ? pick_w<true>(wbytes, epl, nw) : pick_w<false>(wbytes, epl, nw);
 }
 
-ProbeFn get_cluster_probe(int nw) {
+ProbeFn get_cluster_probe(int nw, bool hier) {
   switch (nw) {
-    case 4: return cluster_probe_kernel<4>;
-    case 8: return cluster_probe_kernel<8>;
-    case 16: return cluster_probe_kernel<16>;
+    case 4: return hier ? cluster_probe_kernel<4, true> : cluster_probe_kernel<4, false>;
+    case 8: return hier ? cluster_probe_kernel<8, true> : cluster_probe_kernel<8, false>;
+    case 16: return hier ? cluster_probe_kernel<16, true> : cluster_probe_kernel<16, false>;
+  }
+  return nullptr;
+}
+
+namespace {
+template <typename W, int EPL>
+KernelFn pick_hier_nw(int nw) {
+  switch (nw) {
+    case 4: return cluster_hier_kernel<W, EPL, 4>;
+    case 8: return cluster_hier_kernel<W, EPL, 8>;
+    case 16: return cluster_hier_kernel<W, EPL, 16>;
+  }
+  return nullptr;
+}
+template <typename W>
+KernelFn pick_hier_epl(int epl, int nw) {
+  switch (epl) {
+    case 4: return pick_hier_nw<W, 4>(nw);
+    case 8: return pick_hier_nw<W, 8>(nw);
+    case 16: return pick_hier_nw<W, 16>(nw);
+    case 32: return pick_hier_nw<W, 32>(nw);
+  }
+  return nullptr;
+}
+}  // namespace
+
+KernelFn get_cluster_hier_kernel(int wbytes, int epl, int nw) {
+  switch (wbytes) {
+    case 1: return pick_hier_epl<uint8_t>(epl, nw);
+    case 2: return pick_hier_epl<uint16_t>(epl, nw);
+    case 4: return pick_hier_epl<uint32_t>(epl, nw);
   }
   return nullptr;
 }

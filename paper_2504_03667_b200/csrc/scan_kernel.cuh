@@ -69,6 +69,7 @@ struct ScanParams {
 constexpr uint32_t kFlagPrefetchReg = 1u;  // runner-up row into registers
 constexpr uint32_t kFlagPrefetchL2 = 2u;   // owner L2 prefetch of local-best rows
 constexpr uint32_t kFlagSpeculate = 4u;    // cluster engine: speculative relax of the runner-up
+constexpr uint32_t kFlagHier = 8u;         // cluster engine: CTA pre-reduction, C-key exchange
 
 template <typename W>
 struct WInf;

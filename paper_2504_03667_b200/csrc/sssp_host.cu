@@ -112,6 +112,7 @@ struct Shard {
   uint64_t row_stride = 0;  // G*L
   uint32_t G = 0, EPL = 0, L = 0, NP = 0;  // G = participants (warps) per solve
   uint32_t C = 1, NW = 1;                   // cluster engine: CTAs per cluster, warps per CTA
+  bool hier = false;                        // cluster engine: hierarchical (CTA pre-reduction)
   uint32_t k = 0;           // shard index
   uint64_t col_base = 0, loc_n = 0, cols = 0;  // cols = real columns held
   uint64_t* d_slots = nullptr;
@@ -388,7 +389,9 @@ int finalize_encoding(sssp_graph* g) {
     g->slot_stride = 2ull * g->bstride;
     for (auto& s : g->sh) {
       s.NP = s.NW / 4;
-      s.fn = get_cluster_kernel((int)g->wbytes, (int)s.EPL, (int)s.NW, g->packed != 0);
+      s.hier = g->packed && (g->opt.flags & kFlagHier) && s.C <= 16;
+      s.fn = s.hier ? get_cluster_hier_kernel((int)g->wbytes, (int)s.EPL, (int)s.NW)
+                    : get_cluster_kernel((int)g->wbytes, (int)s.EPL, (int)s.NW, g->packed != 0);
       if (!s.fn) return fail(SSSP_ERR_UNSUPPORTED, "no cluster kernel instance for this layout");
     }
     return SSSP_OK;
@@ -1125,7 +1128,8 @@ int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round) {
   if (g->multiproc && !g->connected) return fail(SSSP_ERR_BAD_ARG, "shard not connected");
   if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
   const uint32_t np = g->sh[0].NP;
-  ProbeFn fn = g->cluster ? get_cluster_probe((int)g->sh[0].NW) : get_grid_probe((int)np);
+  ProbeFn fn = g->cluster ? get_cluster_probe((int)g->sh[0].NW, g->sh[0].hier)
+                          : get_grid_probe((int)np);
   if (!fn) return fail(SSSP_ERR_UNSUPPORTED, "no probe instance");
   if (g->cluster && g->sh[0].C > 8)
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));

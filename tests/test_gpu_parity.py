@@ -348,3 +348,19 @@ def test_queued_enqueues_then_finish(gpu, oracle_c, engine):
         r = dg.solve(11)
     d, p = oracle_c.serial(g.adj, g.n, 11)
     assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p)
+
+
+@pytest.mark.parametrize("warps", [4, 8, 16])
+@pytest.mark.parametrize("P", [1, 2])
+def test_hierarchical_cluster_variant(gpu, oracle_c, warps, P):
+    """flag 8: CTA pre-reduction + C-key DSMEM exchange (+ P2P mailbox for P>1)."""
+    rng = np.random.default_rng(warps * 10 + P)
+    for i in range(12):
+        n = int(rng.integers(2, 3000))
+        directed = bool(i % 2)
+        adj = random_tie_graph(rng, n, 3, float(rng.choice([0.002, 0.05, 0.5])), directed)
+        g = gpu.Graph(n, directed, adj)
+        s = int(rng.integers(0, n))
+        d, p = serial(oracle_c, g, s)
+        with gpu.DeviceGraph(g, [0] * P, engine="cluster", flags=3 | 8, warps=warps) as dg:
+            assert_same(dg.solve(s), d, p, f"hier n={n} warps={warps} P={P}")
