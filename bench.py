@@ -169,7 +169,7 @@ def main():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--vertices", dest="n", type=int, default=N_DEFAULT)
     ap.add_argument("--seed", type=int, default=SEED_DEFAULT)
     ap.add_argument("--graph", default="dense", choices=["dense", "bernoulli"])
     ap.add_argument("--source", type=int, default=0)
@@ -196,11 +196,17 @@ def main():
 
     if not torch.cuda.is_available():
         raise SystemExit("bench.py needs a CUDA device (there is no CPU path)")
+    # test knobs: run all ranks on one GPU over gloo (the 1-GPU multi-process check)
+    if os.environ.get("SSSP_BENCH_ONE_GPU"):
+        local_rank = 0
     torch.cuda.set_device(local_rank)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if os.environ.get("SSSP_BENCH_ONE_GPU"):
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
 
     n = args.n
     # ---- input (untimed, as in the reference: PAPER.md:35, bench.hpp:43-44)

@@ -65,6 +65,13 @@ def dijkstra_distributed(block: np.ndarray, n: int, source: int, max_weight: int
                          group=None, **kw) -> ShortestPathResult:
     """Collective: every rank passes its n x count column block (shard_range)
     and receives the full ShortestPathResult."""
-    with open_shard(block, n, max_weight, device, group, **kw) as sg:
+    sg = open_shard(block, n, max_weight, device, group, **kw)
+    try:
         r = sg.solve(source)
+    finally:
+        # no rank may unmap its mailbox while a peer's kernel could still store
+        # into it: close collectively
+        import torch.distributed as dist
+        dist.barrier(group)
+        sg.close()
     return gather_result(source, n, r.dist, r.pred, group)
