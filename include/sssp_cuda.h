@@ -71,6 +71,9 @@ typedef struct {
   int record_visit_order; /* 1: keep the elected vertex of every round */
   uint32_t replicas;      /* grid engine: copies of the L2 exchange array (0 = 1) */
   uint32_t warps_per_cta; /* cluster engine: 4, 8 or 16 (0 = 4) */
+  int64_t global_min_weight; /* shard mode: smallest finite off-diagonal weight of the WHOLE
+                                graph (sssp_block_weight_range + an allreduce), -1 = unknown;
+                                the bucket engine needs it >= 1 on every rank */
 } sssp_options;
 
 #define SSSP_FLAGS_DEFAULT 3u /* bit2 (4): speculative relax, off by default */
@@ -125,6 +128,11 @@ int sssp_shard_export(sssp_graph* g, void* handle_out);
 int sssp_shard_connect(sssp_graph* g, const void* handles);
 /* Columns [*col_begin, *col_begin + *col_count) are this process's slice. */
 int sssp_shard_range(const sssp_graph* g, uint64_t* col_begin, uint64_t* col_count);
+/* Finite weight range of a column block (rows 0..n-1, global column offset
+ * col_begin, leading dimension ld): *min_offdiag excludes the diagonal
+ * (UINT64_MAX if there is no edge), *max_finite includes it.  Host only. */
+int sssp_block_weight_range(const uint64_t* block, uint64_t ld, uint64_t n, uint64_t col_begin,
+                            uint64_t col_count, uint64_t* min_offdiag, uint64_t* max_finite);
 
 int sssp_graph_destroy(sssp_graph* g);
 int sssp_graph_info(const sssp_graph* g, sssp_solve_stats* st);

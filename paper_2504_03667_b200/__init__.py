@@ -209,8 +209,9 @@ ENGINES = {"auto": 0, "grid": 1, "cluster": 2, "bucket": 3}
 
 def _options(flags: Optional[int], ctas: int, max_batch: int, timeout_ms: int,
              visit_order: bool, replicas: int = 0, engine: str = "auto",
-             warps: int = 0) -> Options:
+             warps: int = 0, global_min_weight: int = -1) -> Options:
     o = Options()
+    o.global_min_weight = global_min_weight
     o.engine = ENGINES[engine]
     o.warps_per_cta = warps
     o.ctas_per_shard = ctas
@@ -324,9 +325,10 @@ class ShardGraph(DeviceGraph):
     def __init__(self, block: np.ndarray, n: int, world: int, rank: int, max_weight: int,
                  device: int = 0, *, flags: Optional[int] = None, ctas: int = 0,
                  timeout_ms: int = 0, replicas: int = 0, engine: str = "auto", warps: int = 0,
-                 max_batch: int = 1):
+                 max_batch: int = 1, global_min_weight: int = -1):
         self.n = n
-        self._opt = _options(flags, ctas, max_batch, timeout_ms, False, replicas, engine, warps)
+        self._opt = _options(flags, ctas, max_batch, timeout_ms, False, replicas, engine, warps,
+                             global_min_weight)
         blk = np.ascontiguousarray(block, dtype=np.uint64)
         ld = blk.shape[1] if blk.ndim == 2 else max(1, blk.size // max(1, n))
         h = ctypes.c_void_p()
@@ -347,6 +349,16 @@ class ShardGraph(DeviceGraph):
     def connect(self, handles: Sequence[bytes]) -> None:
         blob = b"".join(handles)
         check(lib.sssp_shard_connect(self._h, ctypes.c_char_p(blob)), "sssp_shard_connect")
+
+
+def block_weight_range(block: np.ndarray, n: int, col_begin: int) -> tuple:
+    """(min finite off-diagonal weight or None, max finite weight) of an n x c column block."""
+    blk = np.ascontiguousarray(block, dtype=np.uint64)
+    c = blk.shape[1] if blk.ndim == 2 else 0
+    mn, mx = ctypes.c_uint64(), ctypes.c_uint64()
+    check(lib.sssp_block_weight_range(_p64(blk), max(c, 1), n, col_begin, c, ctypes.byref(mn),
+                                      ctypes.byref(mx)), "sssp_block_weight_range")
+    return (None if mn.value == 0xFFFFFFFFFFFFFFFF else mn.value), mx.value
 
 
 def dijkstra(g: Graph, source: int, device: int = 0) -> ShortestPathResult:

@@ -38,21 +38,34 @@
 
 namespace sssp_b200 {
 
+// Global positions: shard j's local position p is global position
+// g = j*row_stride + p, i.e. vertex j*loc_n + vid(p).  Tiles are numbered
+// globally (shard j, CTA c) -> j*G + c.  With one shard this is the plain
+// position order.
 struct BucketParams {
-  const void* adj;      // [n rows][row_stride], positions (cyclic layout)
-  const void* adjT;     // [n rows (vertex v)][row_stride] = w(pos->u, v); nullptr: push only
+  const void* adj;      // [n rows][row_stride]: this shard's columns, positions
+  const void* adjT;     // PULL source (nullptr: push only); row r, global positions
+  uint64_t adjT_stride; // elements per adjT row (= nshards * row_stride)
+  uint32_t adjT_by_pos; // 1: adjT row of column p is the local position p (sharded
+                        //    transpose); 0: the vertex id vid(p) (one shard)
   uint64_t row_stride;  // positions per row (= Q*L)
-  uint32_t n;           // vertices
-  uint32_t Q, L;        // layout: position p = q*L + s  <->  vertex s*Q + q
+  uint32_t n;           // vertices (global)
+  uint32_t Q, L;        // layout: position p = q*L + s  <->  local vertex s*Q + q
   uint32_t qbits, lbits;
   uint32_t T;           // positions per CTA
-  uint32_t source;
-  uint32_t* bitmap;     // [2][row_stride / 32] (B_d by position)
-  uint32_t* ctrl;       // [2 parities][3][G]: per-tile lmin, candidate count, unsettled count
-  uint64_t* dist_out;   // [n]
-  uint64_t* pred_out;   // [n]
-  uint64_t* info;       // [4]: settled vertices, classes (steps), rows pushed, rows pulled
-  uint64_t* trace;      // optional [64]: %globaltimer after every grid barrier (CTA 0)
+  uint32_t source;      // global vertex id
+  uint32_t nshards, shard, loc_n;
+  uint32_t* peer_bitmap[kMaxShards];  // every shard's [2][nshards*row_stride/32] (self incl.)
+  uint32_t* peer_ctrl[kMaxShards];    // every shard's [2][3][nshards*G]: tile lmin, cand, uns
+  unsigned long long* peer_bar[kMaxShards];  // every shard's barrier counter (nshards > 1)
+  uint64_t* bar_epoch;  // this shard's count of cross-shard barriers completed by earlier
+                        // launches (read at start, advanced at exit; same on every shard)
+  uint64_t timeout_ns;
+  uint64_t* dist_out;   // [loc_n] (local vertex ids)
+  uint64_t* pred_out;   // [loc_n]
+  uint64_t* info;       // [4]: settled vertices, classes, rows pushed, rows pulled
+  uint64_t* info2;      // [2]: barriers used, error
+  uint64_t* trace;      // optional [64]: %globaltimer after every barrier (CTA 0 of shard 0)
 };
 
 __device__ __forceinline__ uint32_t pos_to_vid(uint32_t pos, uint32_t Q, uint32_t lbits,
@@ -106,8 +119,8 @@ __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t T, uint32_t G, u
                                                        uint32_t wbytes);
 constexpr int kBucketChunk = kBucketThreads * 32;  // ids of one pass over 256 bitmap words
 
-// Dynamic smem: dist[T] u32 | pred[T] u32 | settled[T/32] u32 | lmin[G] u32 |
-//               bitmap[row_stride/32] u32 | chunk[kBucketChunk] u32 |
+// Dynamic smem: dist[T] u32 | pred[T] u32 | settled[T/32] u32 | lmin[GT] u32 |
+//               bitmap[nshards*row_stride/32] u32 | chunk[kBucketChunk] u32 |
 //               combine[kBucketThreads * CPT] keys
 //
 // One grid barrier per class.  Before the barrier that ends step s every CTA
@@ -127,9 +140,10 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
   cg::grid_group grid = cg::this_grid();
 
   extern __shared__ __align__(16) uint32_t smem[];
-  const uint32_t T = p.T, G = gridDim.x;
+  const uint32_t T = p.T, G = gridDim.x * p.nshards;  // G = tiles of ALL shards
   const uint32_t TW = T / 32;  // bitmap words per tile
-  const uint32_t words = (uint32_t)(p.row_stride / 32);
+  const uint32_t lwords = (uint32_t)(p.row_stride / 32);
+  const uint32_t words = lwords * p.nshards;  // global bitmap words
   uint32_t* sdist = smem;
   uint32_t* spred = sdist + T;
   uint32_t* ssettled = spred + T;
@@ -141,19 +155,57 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
   __shared__ uint32_t s_cnt[2];
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t me = blockIdx.x;
-  const uint32_t p0 = me * T;
+  const uint32_t me = p.shard * gridDim.x + blockIdx.x;  // global tile id
+  const uint32_t p0 = blockIdx.x * T;                    // first LOCAL position of the tile
   const uint32_t tbits = 31u - __clz(T);  // T is a power of two
   const W* adj = static_cast<const W*>(p.adj);
   const W* adjT = static_cast<const W*>(p.adjT);
   const uint32_t TPR = T * sizeof(W) / 16;  // threads per row slice
   const uint32_t RG = kBucketThreads / TPR; // row groups
   // global per-step arrays: ctrl = [2][3][G] (lmin, candidates, unsettled)
-  uint32_t* const glob = p.ctrl;
+  uint32_t* const glob = p.peer_ctrl[p.shard];
+  const uint32_t* const gbm = p.peer_bitmap[p.shard];
+  // global position -> global vertex id
+  auto gvid = [&](uint32_t g) -> uint32_t {
+    const uint32_t j = g >> (p.qbits + p.lbits);  // row_stride = Q*L = 2^(qbits+lbits)
+    return j * p.loc_n + pos_to_vid(g & ((1u << (p.qbits + p.lbits)) - 1u), p.Q, p.lbits, p.qbits);
+  };
 
   uint32_t ntr = 0;
   auto stamp = [&]() {
     if (p.trace && me == 0 && tid == 0 && ntr < 64) p.trace[ntr++] = globaltimer();
+  };
+  // One barrier over every CTA of every shard: the cooperative grid barrier
+  // with one shard; with several, each CTA bumps every shard's counter by a
+  // system-scope atomic (an NVLink write for a remote shard) and waits until
+  // its own shard's counter shows all G tiles of this barrier.
+  uint64_t nbar = 0;
+  bool failed = false;
+  const uint64_t t_start = globaltimer();
+  const uint64_t bar_base = p.nshards > 1 ? *(volatile uint64_t*)p.bar_epoch : 0;
+  auto barrier = [&]() {
+    if (p.nshards == 1) {
+      grid.sync();
+    } else {
+      __syncthreads();
+      if (tid == 0) {
+        __threadfence_system();
+        for (uint32_t j = 0; j < p.nshards; ++j) atomicAdd_system(p.peer_bar[j], 1ull);
+        const unsigned long long target = (bar_base + nbar + 1) * (unsigned long long)G;
+        unsigned long long v;
+        uint32_t polls = 0;
+        while (true) {
+          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.peer_bar[p.shard]) : "memory");
+          if (v >= target) break;
+          if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) {
+            failed = true;
+            break;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    ++nbar;
   };
 
   // Publishes this tile's minimum, candidate bitmap and counts for step `s`.
@@ -171,45 +223,52 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
     __syncthreads();
     if (lane == 0) atomicAdd(&s_cnt[1], uns);
     for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) m = min(m, s_red[w2]);
-    uint32_t* bm = p.bitmap + par * words + me * TW;
     for (uint32_t i = tid; i < TW; i += kBucketThreads) {
       uint32_t cm = 0;
       const uint32_t sm = ssettled[i];
       if (m != DINF)
         for (uint32_t b = 0; b < 32; ++b)
           if (!((sm >> b) & 1u) && sdist[i * 32 + b] == m) cm |= 1u << b;
-      bm[i] = cm;
+      for (uint32_t j = 0; j < p.nshards; ++j)  // remote shards: P2P stores
+        p.peer_bitmap[j][par * words + me * TW + i] = cm;
       if (cm) atomicAdd(&s_cnt[0], __popc(cm));
     }
     __syncthreads();
-    if (tid == 0) {
-      glob[(par * 3 + 0) * G + me] = m;
-      glob[(par * 3 + 1) * G + me] = s_cnt[0];
-      glob[(par * 3 + 2) * G + me] = s_cnt[1];
+    if (tid < p.nshards) {
+      uint32_t* c = p.peer_ctrl[tid];
+      c[(par * 3 + 0) * G + me] = m;
+      c[(par * 3 + 1) * G + me] = s_cnt[0];
+      c[(par * 3 + 2) * G + me] = s_cnt[1];
     }
   };
 
   // ---- init: dist = INF, pred = NONE, padding settled (serial.hpp:32-36)
+  const uint32_t vbase = p.shard * p.loc_n;
   for (uint32_t i = tid; i < T; i += kBucketThreads) {
-    const uint32_t v = pos_to_vid(p0 + i, p.Q, p.lbits, p.qbits);
-    sdist[i] = v == p.source ? 0u : DINF;
+    const uint32_t vl = pos_to_vid(p0 + i, p.Q, p.lbits, p.qbits);
+    sdist[i] = (vl < p.loc_n && vbase + vl == p.source) ? 0u : DINF;
     spred[i] = 0xFFFFFFFFu;
   }
   for (uint32_t i = tid; i < TW; i += kBucketThreads) {
     uint32_t m = 0;
-    for (uint32_t b = 0; b < 32; ++b)
-      if (pos_to_vid(p0 + i * 32 + b, p.Q, p.lbits, p.qbits) >= p.n) m |= 1u << b;
+    for (uint32_t b = 0; b < 32; ++b) {
+      const uint32_t vl = pos_to_vid(p0 + i * 32 + b, p.Q, p.lbits, p.qbits);
+      if (vl >= p.loc_n || vbase + vl >= p.n) m |= 1u << b;
+    }
     ssettled[i] = m;
   }
   __syncthreads();
-  publish(0);
-  grid.sync();
+  // Buffer parity follows the GLOBAL barrier count (it continues across
+  // launches): a fast shard's next launch then publishes into the buffer the
+  // slow shard is NOT reading after its final barrier.
+  publish((uint32_t)(bar_base & 1ull));
+  barrier();
   stamp();
 
   uint64_t pushed = 0, pulled = 0, settled = 0;
   uint32_t step = 0;
-  while (true) {
-    const uint32_t par = step & 1u, nxt = par ^ 1u;
+  while (!failed) {
+    const uint32_t par = (uint32_t)((bar_base + nbar - 1) & 1ull), nxt = par ^ 1u;
     // ---- the class: d = min over tiles, B_d = candidates of the tiles at d
     uint32_t d = DINF, bcount = 0, uns = 0;
     for (uint32_t c = tid; c < G; c += kBucketThreads) {
@@ -244,7 +303,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
     // stage B_d (candidates of the tiles at d) in shared memory: every
     // later bitmap lookup of this class hits smem, not a few hot L2 lines
     {
-      const uint32_t* bm = p.bitmap + par * words;
+      const uint32_t* bm = gbm + par * words;
       for (uint32_t i = tid; i < words; i += kBucketThreads)
         sbm[i] = slmin[i / TW] == d ? __ldcg(&bm[i]) : 0u;
     }
@@ -285,7 +344,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
         }
         uint32_t o = wofs + incl - c;
         for (uint32_t m = bw; m; m &= m - 1)
-          schunk[o++] = pos_to_vid(wi * 32 + (__ffs(m) - 1), p.Q, p.lbits, p.qbits);
+          schunk[o++] = gvid(wi * 32 + (__ffs(m) - 1));
         __syncthreads();
         // batches of 8 rows: all 8 loads are issued before any is consumed
         for (uint32_t r0 = rg; r0 < tot; r0 += 8 * RG) {
@@ -352,8 +411,11 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
         }
       __syncthreads();
       const uint32_t nu = s_nu;
-      const uint32_t cbits = 31u - __clz((uint32_t)(p.row_stride * sizeof(W) / 16));  // chunks/row
-      const uint32_t total = nu << cbits;
+      // chunks per transposed row (nshards * row_stride: not a power of two for P = 3, 5, 6, 7)
+      const uint32_t cpr = (uint32_t)(p.adjT_stride * sizeof(W) / 16);
+      const bool cpow2 = (cpr & (cpr - 1u)) == 0;  // uniform: shifts instead of divisions
+      const uint32_t cbits = 31u - __clz(cpr);
+      const uint32_t total = nu * cpr;
       uint32_t cur = 0xFFFFFFFFu;
       K run = KT::kNone;
       for (uint32_t it0 = tid; it0 < total; it0 += kBucketThreads * 8) {
@@ -365,13 +427,14 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
           ci[m] = 0xFFFFFFFFu;
           bits[m] = 0;
           if (item < total) {
-            ci[m] = item >> cbits;
-            const uint32_t chunk = item & ((1u << cbits) - 1u);
+            ci[m] = cpow2 ? item >> cbits : item / cpr;
+            const uint32_t chunk = item - ci[m] * cpr;
             const uint32_t pos0 = chunk * CPT;
-            const uint32_t v = pos_to_vid(p0 + slist[ci[m]], p.Q, p.lbits, p.qbits);
+            const uint32_t v = p.adjT_by_pos ? p0 + slist[ci[m]]
+                                             : pos_to_vid(p0 + slist[ci[m]], p.Q, p.lbits, p.qbits);
             bits[m] = (sbm[pos0 >> 5] >> (pos0 & 31)) & ((1u << CPT) - 1u);
             v4[m] = __ldg(reinterpret_cast<const uint4*>(
-                reinterpret_cast<const uint8_t*>(adjT + (size_t)v * p.row_stride) + chunk * 16));
+                reinterpret_cast<const uint8_t*>(adjT + (size_t)v * p.adjT_stride) + chunk * 16));
           }
         }
 #pragma unroll
@@ -382,9 +445,9 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
             cur = ci[m];
             run = KT::kNone;
           }
-          const uint32_t pos0 = ((it0 + m * kBucketThreads) & ((1u << cbits) - 1u)) * CPT;
+          const uint32_t pos0 = ((it0 + m * kBucketThreads) - ci[m] * cpr) * CPT;
           // consecutive positions of one participant: vertex ids step by Q
-          const uint32_t vid0 = pos_to_vid(pos0, p.Q, p.lbits, p.qbits);
+          const uint32_t vid0 = gvid(pos0);
           const uint32_t wd[4] = {v4[m].x, v4[m].y, v4[m].z, v4[m].w};
 #pragma unroll
           for (int c = 0; c < CPT; ++c) {
@@ -412,24 +475,27 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
     }
     // ---- publish the next class's candidates, one barrier per class
     publish(nxt);
-    grid.sync();
+    barrier();
     stamp();
   }
 
-  // ---- write back (positions -> vertex ids)
+  // ---- write back (positions -> local vertex ids)
   for (uint32_t i = tid; i < T; i += kBucketThreads) {
     const uint32_t v = pos_to_vid(p0 + i, p.Q, p.lbits, p.qbits);
-    if (v < p.n) {
+    if (v < p.loc_n && vbase + v < p.n) {
       p.dist_out[v] = sdist[i] == DINF ? ~0ull : (uint64_t)sdist[i];
       p.pred_out[v] = spred[i] == 0xFFFFFFFFu ? ~0ull : (uint64_t)spred[i];
     }
   }
-  if (me == 0 && tid == 0) {
+  if (blockIdx.x == 0 && tid == 0) {
     p.info[0] = settled;
     p.info[1] = step;
     p.info[2] = pushed;
     p.info[3] = pulled;
+    p.info2[0] = nbar;
+    if (p.nshards > 1) *p.bar_epoch = bar_base + nbar;  // every CTA read it before barrier 1
   }
+  if (failed && tid == 0) p.info2[1] = 1;
 }
 
 __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t T, uint32_t G, uint32_t words,
@@ -466,6 +532,30 @@ __global__ void __launch_bounds__(256) transpose_positions_kernel(const W* __res
     const uint32_t v = pos_to_vid(pb + r, Q, lbits, qbits);
     if (v < n) at[(size_t)v * row_stride + ppb + tx] = tile[tx][r];
   }
+}
+
+// Sharded transpose: AT_k[p][g] = A_k[vertex(g)][p] for this shard's local
+// positions p and all global positions g (shard j, local position q ->
+// g = j*rs + q, vertex j*loc_n + vid(q)); padding / absent rows give INF.
+template <typename W>
+__global__ void __launch_bounds__(256) transpose_global_kernel(const W* __restrict__ a,
+                                                               W* __restrict__ at, uint64_t rs,
+                                                               uint32_t n, uint32_t Q,
+                                                               uint32_t qbits, uint32_t lbits,
+                                                               uint32_t P, uint32_t loc_n) {
+  __shared__ W tile[64][65];
+  const uint32_t pb = blockIdx.x * 64;  // local positions (rows of AT)
+  const uint32_t gb = blockIdx.y * 64;  // global positions (columns of AT)
+  const uint32_t tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
+  for (uint32_t r = ty; r < 64; r += 4) {
+    const uint32_t g = gb + r;
+    const uint32_t j = (uint32_t)(g / rs), vl = pos_to_vid((uint32_t)(g - j * rs), Q, lbits, qbits);
+    const uint32_t u = j * loc_n + vl;
+    tile[r][tx] = (vl < loc_n && u < n) ? a[(size_t)u * rs + pb + tx] : (W)WInf<W>::v;
+  }
+  __syncthreads();
+  const uint64_t ats = rs * P;
+  for (uint32_t r = ty; r < 64; r += 4) at[(size_t)(pb + r) * ats + gb + tx] = tile[tx][r];
 }
 
 // flag = 1 if the stored matrix is not symmetric: compares every element

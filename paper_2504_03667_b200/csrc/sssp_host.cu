@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <mutex>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -127,9 +128,7 @@ struct Shard {
   // bucket engine (bucket_kernel.cuh)
   void* d_adjT = nullptr;        // transpose in position order (nullptr: symmetric or absent)
   const void* pull_src = nullptr;// d_adjT, or d_adj when the matrix is symmetric
-  uint32_t* d_bitmap = nullptr;  // [2][row_stride/32]
-  uint32_t* d_ctrl = nullptr;    // [8]
-  uint32_t bT = 0, bG = 0;       // positions per CTA, CTAs
+  uint64_t* d_info2 = nullptr;   // bucket: [B][2] barriers used, watchdog
   uint64_t* d_trace = nullptr;   // debug (SSSP_BUCKET_TRACE)
   bool peer_ipc[kMaxShards] = {};
   KernelFn fn = nullptr;
@@ -151,6 +150,10 @@ struct sssp_graph {
   uint32_t nrep = 1;
   bool cluster = true;  // scan engine: cluster (DSMEM exchange) or grid (L2 exchange)
   bool bucket = false;  // distance-class engine available and selected (min weight >= 1)
+  // bucket engine layout (identical on every shard)
+  uint32_t bT = 0, bG = 0;               // positions per CTA, CTAs per shard
+  uint64_t slots_bytes = 0;              // scan-engine exchange region (start of d_slots)
+  uint64_t bar_off = 0, epoch_off = 0, ctrl_off = 0, bm_off = 0, region_bytes = 0;
   uint64_t exch_base = 0;
   double transfer_in_s = 0;
   uint32_t pending = 0;  // solves of the last enqueued launch (0: nothing pending)
@@ -165,6 +168,7 @@ sssp_options default_options(const sssp_options* o) {
   if (o) d = *o;
   else d.flags = SSSP_FLAGS_DEFAULT;
   if (d.timeout_ms == 0) d.timeout_ms = 60000;
+  if (!o) d.global_min_weight = -1;
   return d;
 }
 
@@ -209,6 +213,26 @@ int plan_cluster_layout(Shard& s, uint64_t loc_n, uint32_t cmax, uint32_t nw) {
   return fail(SSSP_ERR_UNSUPPORTED, "graph too large for one cluster; use more shards or the grid engine");
 }
 
+// Process-wide pinned staging buffers for uploads (two, double-buffered).
+struct PinnedStaging {
+  std::mutex m;
+  void* buf[2] = {nullptr, nullptr};
+  size_t cap[2] = {0, 0};
+  void* get(int b, size_t bytes) {
+    if (cap[b] < bytes) {
+      if (buf[b]) cudaFreeHost(buf[b]);
+      buf[b] = nullptr;
+      cap[b] = 0;
+      if (cudaHostAlloc(&buf[b], bytes, cudaHostAllocDefault) != cudaSuccess) return nullptr;
+      cap[b] = bytes;
+    }
+    return buf[b];
+  }
+};
+PinnedStaging g_staging;
+
+int pool_alloc(struct Shard& s, void** p, size_t bytes);
+
 struct ScanResult {
   std::atomic<bool> overflow{false};
   uint64_t max_w = 0, min_w = ~0ull;
@@ -228,6 +252,10 @@ int upload_block(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, ScanRes
   const uint64_t row_in_bytes = std::max<uint64_t>(1, cols) * 8;
   const uint64_t R = std::max<uint64_t>(1, std::min<uint64_t>(n, (32ull << 20) / row_in_bytes));
   const uint64_t stage_elems = R * std::max<uint64_t>(1, cols);
+  // pinned staging is process-wide and grow-only (pinning / unpinning on every
+  // graph creation measured 0.2-0.8 s of jitter); device staging comes from the
+  // stream-ordered pool (no cudaFree device synchronisation)
+  std::lock_guard<std::mutex> staging_lock(g_staging.m);
   W* pin[2] = {nullptr, nullptr};
   W* dst[2] = {nullptr, nullptr};
   cudaEvent_t done[2] = {nullptr, nullptr};
@@ -237,18 +265,20 @@ int upload_block(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, ScanRes
   auto cleanup = [&]() {
     cudaStreamSynchronize(s.stream);
     for (int b = 0; b < 2; ++b) {
-      if (pin[b]) cudaFreeHost(pin[b]);
-      if (dst[b]) cudaFree(dst[b]);
+      if (dst[b]) cudaFreeAsync(dst[b], s.stream);
       if (done[b]) cudaEventDestroy(done[b]);
     }
   };
   for (int b = 0; b < 2; ++b) {
-    if (cudaHostAlloc(&pin[b], stage_elems * sizeof(W), cudaHostAllocDefault) != cudaSuccess ||
-        cudaMalloc(&dst[b], stage_elems * sizeof(W)) != cudaSuccess ||
+    void* d = nullptr;
+    if (!(pin[b] = static_cast<W*>(g_staging.get(b, stage_elems * sizeof(W)))) ||
+        pool_alloc(s, &d, stage_elems * sizeof(W)) != SSSP_OK ||
         cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming) != cudaSuccess) {
+      dst[b] = static_cast<W*>(d);
       cleanup();
       return fail(SSSP_ERR_OOM, "upload staging allocation failed");
     }
+    dst[b] = static_cast<W*>(d);
   }
   uint64_t chunk = 0;
   for (uint64_t r0 = 0; r0 < n && rc == SSSP_OK; r0 += R, ++chunk) {
@@ -355,8 +385,11 @@ int upload_shard(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, uint64_
 int alloc_state(sssp_graph* g, Shard& s) {
   CK(cudaSetDevice(s.device));
   const uint64_t B = g->max_batch;
-  CK(cudaMalloc(&s.d_slots, B * g->slot_stride * sizeof(uint64_t)));
-  CK(cudaMemset(s.d_slots, 0, B * g->slot_stride * sizeof(uint64_t)));
+  g->slots_bytes = (B * g->slot_stride * sizeof(uint64_t) + 255) & ~255ull;
+  const uint64_t bytes = g->slots_bytes + (g->bucket ? g->region_bytes : 0);
+  CK(cudaMalloc(&s.d_slots, bytes));
+  CK(cudaMemset(s.d_slots, 0, bytes));
+  CK(cudaMalloc(&s.d_info2, B * 2 * sizeof(uint64_t)));
   CK(cudaMalloc(&s.d_dist, B * std::max<uint64_t>(1, s.loc_n) * sizeof(uint64_t)));
   CK(cudaMalloc(&s.d_pred, B * std::max<uint64_t>(1, s.loc_n) * sizeof(uint64_t)));
   CK(cudaMalloc(&s.d_info, B * 4 * sizeof(uint64_t)));
@@ -460,11 +493,75 @@ int compute_max_batch(sssp_graph* g) {
   return SSSP_OK;
 }
 
+void* bucket_fn(uint32_t wbytes) {
+  return wbytes == 1 ? (void*)bucket_kernel<uint8_t>
+         : wbytes == 2 ? (void*)bucket_kernel<uint16_t> : (void*)bucket_kernel<uint32_t>;
+}
+
+size_t bucket_smem(const sssp_graph* g) {
+  const uint64_t rs = g->sh[0].row_stride;
+  return bucket_smem_bytes(g->bT, g->bG * g->P, (uint32_t)(rs / 32 * g->P), g->wbytes);
+}
+
 // The distance-class engine is exact iff every finite off-diagonal weight is
-// >= 1 (bucket_kernel.cuh); it runs on single-shard graphs with the cluster
-// layout (power-of-two participant count).  It needs the matrix transpose for
-// PULL steps: none when the matrix is symmetric, else a second device copy
-// when it fits (otherwise PUSH only).
+// >= 1 (bucket_kernel.cuh); it needs the cluster layout (power-of-two
+// participant count) and no visit-order recording.  Chooses the tile T (128 B
+// of each row per CTA, widened until every shard's grid is co-resident) and
+// the exchange-region layout; allocation happens in alloc_state.
+int plan_bucket(sssp_graph* g) {
+  g->bucket = false;
+  const int want = g->opt.engine;
+  if (want == SSSP_ENGINE_GRID || want == SSSP_ENGINE_CLUSTER) return SSSP_OK;
+  const bool exact = g->min_w >= 1;
+  const Shard& s0 = g->sh[0];
+  const bool shape = g->cluster && g->n > 1 && !g->opt.record_visit_order &&
+                     !(s0.G & (s0.G - 1)) && !(s0.L & (s0.L - 1));
+  if (want == SSSP_ENGINE_BUCKET && !(exact && shape))
+    return fail(SSSP_ERR_UNSUPPORTED, exact ? "bucket engine needs the cluster layout"
+                                            : "bucket engine needs min weight >= 1");
+  if (!(exact && shape)) return SSSP_OK;
+  void* fn = bucket_fn(g->wbytes);
+  uint32_t T = 128 / g->wbytes;
+  while (true) {
+    if (T > s0.row_stride) T = (uint32_t)s0.row_stride;
+    g->bT = T;
+    g->bG = (uint32_t)(s0.row_stride / T);
+    const size_t smem = bucket_smem(g);
+    bool fits = T * g->wbytes / 16 <= kBucketThreads && smem <= 200 * 1024;
+    for (const auto& s : g->sh) {
+      if (!fits) break;
+      CK(cudaSetDevice(s.device));
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      int per_sm = 0, sms = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBucketThreads, smem));
+      CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
+      uint32_t same = 0;
+      for (const auto& t : g->sh) same += t.device == s.device ? 1 : 0;
+      fits = per_sm > 0 && (uint64_t)g->bG * same <= (uint64_t)per_sm * sms;
+    }
+    if (fits) break;
+    if (T * g->wbytes >= 4096 || T >= s0.row_stride) {
+      if (want == SSSP_ENGINE_BUCKET) return fail(SSSP_ERR_UNSUPPORTED, "bucket grid does not fit");
+      return SSSP_OK;  // AUTO: stay on the scan engine
+    }
+    T *= 2;
+  }
+  // exchange region: [barrier counter | epoch | ctrl [2][3][P*G] | bitmap [2][P*row_stride/32]]
+  const uint64_t GT = (uint64_t)g->bG * g->P;
+  const uint64_t words = s0.row_stride / 32 * g->P;
+  g->bar_off = 0;
+  g->epoch_off = 128;
+  g->ctrl_off = 256;
+  g->bm_off = (g->ctrl_off + 2 * 3 * GT * 4 + 255) & ~255ull;
+  g->region_bytes = (g->bm_off + 2 * words * 4 + 255) & ~255ull;
+  g->bucket = true;
+  return SSSP_OK;
+}
+
+// Builds the PULL source of every local shard.  One shard: the matrix itself
+// when symmetric (row v = column v), else its transpose in position order.
+// Several shards: AT_k[p][g] = A_k[vertex(g)][p] over global positions g
+// (a shard holds every row of its columns, so a column is local but strided).
 int prepare_bucket_impl(sssp_graph* g);
 int prepare_bucket(sssp_graph* g) {
   const double t0 = now_s();
@@ -473,90 +570,52 @@ int prepare_bucket(sssp_graph* g) {
   return rc;
 }
 int prepare_bucket_impl(sssp_graph* g) {
-  const int want = g->opt.engine;
-  if (want == SSSP_ENGINE_GRID || want == SSSP_ENGINE_CLUSTER) return SSSP_OK;
-  const bool exact = g->min_w >= 1;
-  // the visit-order debug output is produced by the round-by-round engines
-  const bool shape = g->P == 1 && g->cluster && g->n > 1 && !g->opt.record_visit_order;
-  if (want == SSSP_ENGINE_BUCKET && !(exact && shape))
-    return fail(SSSP_ERR_UNSUPPORTED,
-                exact ? "bucket engine needs one shard" : "bucket engine needs min weight >= 1");
-  if (!(exact && shape)) return SSSP_OK;
-  Shard& s = g->sh[0];
-  CK(cudaSetDevice(s.device));
-  const uint32_t Q = s.G, L = s.L;
-  if ((Q & (Q - 1)) || (L & (L - 1))) return SSSP_OK;
-  // tile T: 128 B of each row per CTA, widened until the grid is co-resident
-  void* fn = g->wbytes == 1 ? (void*)bucket_kernel<uint8_t>
-             : g->wbytes == 2 ? (void*)bucket_kernel<uint16_t> : (void*)bucket_kernel<uint32_t>;
-  int sms = 0;
-  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
-  uint32_t T = 128 / g->wbytes;
-  while (true) {
-    if (T > s.row_stride) T = (uint32_t)s.row_stride;
-    const size_t cpt = 16 / g->wbytes, ksz = g->wbytes == 1 ? 4 : 8;
-    const uint64_t G0 = s.row_stride / T;
-    const size_t smem = bucket_smem_bytes(T, (uint32_t)G0, (uint32_t)(s.row_stride / 32), g->wbytes);
-    (void)cpt;
-    (void)ksz;
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBucketThreads, smem));
-    const uint64_t G = s.row_stride / T;
-    if (per_sm > 0 && G <= (uint64_t)per_sm * sms && T * g->wbytes / 16 <= kBucketThreads) {
-      s.bT = T;
-      s.bG = (uint32_t)G;
-      break;
-    }
-    if (T * g->wbytes >= 4096 || T >= s.row_stride)
-      return fail(SSSP_ERR_UNSUPPORTED, "bucket grid does not fit co-resident");
-    T *= 2;
-  }
-  CK(cudaMalloc(&s.d_bitmap, 2 * (s.row_stride / 32) * sizeof(uint32_t)));
-  CK(cudaMalloc(&s.d_ctrl, 2 * 3 * (size_t)s.bG * sizeof(uint32_t)));
-  // symmetry check; PULL reads row v of the matrix itself when symmetric, else
-  // row v of a transpose kept in position order (when it fits)
-  s.pull_src = nullptr;
-  if (s.row_stride % 64 == 0) {
-    const dim3 grid((unsigned)(s.row_stride / 64), (unsigned)(s.row_stride / 64));
-    const uint32_t qb = bitlen(Q) - 1, lb = bitlen(L) - 1;
-    uint32_t* d_flag = nullptr;
-    CK(cudaMallocAsync((void**)&d_flag, 4, s.stream));
-    CK(cudaMemsetAsync(d_flag, 0, 4, s.stream));
-    if (g->wbytes == 1)
-      symmetric_check_kernel<uint8_t><<<grid, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, s.row_stride, (uint32_t)g->n, Q, qb, lb, d_flag);
-    else if (g->wbytes == 2)
-      symmetric_check_kernel<uint16_t><<<grid, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, s.row_stride, (uint32_t)g->n, Q, qb, lb, d_flag);
-    else
-      symmetric_check_kernel<uint32_t><<<grid, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, s.row_stride, (uint32_t)g->n, Q, qb, lb, d_flag);
-    CK(cudaGetLastError());
-    uint32_t asym = 1;
-    CK(cudaMemcpyAsync(&asym, d_flag, 4, cudaMemcpyDeviceToHost, s.stream));
-    CK(cudaFreeAsync(d_flag, s.stream));
-    CK(cudaStreamSynchronize(s.stream));
-    if (!asym) {
-      s.pull_src = s.d_adj;
-    } else {
-      size_t free_b = 0, total_b = 0;
-      CK(cudaMemGetInfo(&free_b, &total_b));
-      const uint64_t mbytes = g->n * s.row_stride * g->wbytes;
-      if (mbytes + (256ull << 20) < free_b && pool_alloc(s, &s.d_adjT, mbytes) == SSSP_OK) {
-        if (g->wbytes == 1)
-          transpose_positions_kernel<uint8_t><<<grid, 256, 0, s.stream>>>(
-              (const uint8_t*)s.d_adj, (uint8_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
-        else if (g->wbytes == 2)
-          transpose_positions_kernel<uint16_t><<<grid, 256, 0, s.stream>>>(
-              (const uint16_t*)s.d_adj, (uint16_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
-        else
-          transpose_positions_kernel<uint32_t><<<grid, 256, 0, s.stream>>>(
-              (const uint32_t*)s.d_adj, (uint32_t*)s.d_adjT, s.row_stride, (uint32_t)g->n, Q, qb, lb);
-        CK(cudaGetLastError());
-        s.pull_src = s.d_adjT;
-        g->matrix_bytes += mbytes;
+  if (!g->bucket) return SSSP_OK;
+  for (auto& s : g->sh) {
+    CK(cudaSetDevice(s.device));
+    const uint32_t Q = s.G, L = s.L, qb = bitlen(Q) - 1, lb = bitlen(L) - 1;
+    const uint64_t rs = s.row_stride;
+    s.pull_src = nullptr;
+    if (rs % 64) continue;
+    const uint64_t mbytes = g->n * rs * g->wbytes;
+    if (g->P == 1) {
+      const dim3 grid((unsigned)(rs / 64), (unsigned)(rs / 64));
+      uint32_t* d_flag = nullptr;
+      CK(cudaMallocAsync((void**)&d_flag, 4, s.stream));
+      CK(cudaMemsetAsync(d_flag, 0, 4, s.stream));
+      if (g->wbytes == 1)
+        symmetric_check_kernel<uint8_t><<<grid, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, d_flag);
+      else if (g->wbytes == 2)
+        symmetric_check_kernel<uint16_t><<<grid, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, d_flag);
+      else
+        symmetric_check_kernel<uint32_t><<<grid, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, d_flag);
+      CK(cudaGetLastError());
+      uint32_t asym = 1;
+      CK(cudaMemcpyAsync(&asym, d_flag, 4, cudaMemcpyDeviceToHost, s.stream));
+      CK(cudaFreeAsync(d_flag, s.stream));
+      CK(cudaStreamSynchronize(s.stream));
+      if (!asym) {
+        s.pull_src = s.d_adj;
+        continue;
       }
     }
+    size_t free_b = 0, total_b = 0;
+    CK(cudaMemGetInfo(&free_b, &total_b));
+    const uint64_t tbytes = (uint64_t)rs * rs * g->P * g->wbytes;  // loc positions x global positions
+    if (tbytes + (256ull << 20) >= free_b || pool_alloc(s, &s.d_adjT, tbytes) != SSSP_OK) continue;
+    const dim3 grid((unsigned)(rs / 64), (unsigned)(rs * g->P / 64));
+    const uint32_t P = g->P, loc = (uint32_t)s.loc_n;
+    if (g->wbytes == 1)
+      transpose_global_kernel<uint8_t><<<grid, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, (uint8_t*)s.d_adjT, rs, (uint32_t)g->n, Q, qb, lb, P, loc);
+    else if (g->wbytes == 2)
+      transpose_global_kernel<uint16_t><<<grid, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, (uint16_t*)s.d_adjT, rs, (uint32_t)g->n, Q, qb, lb, P, loc);
+    else
+      transpose_global_kernel<uint32_t><<<grid, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, (uint32_t*)s.d_adjT, rs, (uint32_t)g->n, Q, qb, lb, P, loc);
+    CK(cudaGetLastError());
+    s.pull_src = s.d_adjT;
+    g->matrix_bytes += tbytes;
+    (void)mbytes;
   }
-  g->bucket = true;
   return SSSP_OK;
 }
 
@@ -564,6 +623,8 @@ int setup_common(sssp_graph* g) {
   int rc = finalize_encoding(g);
   if (rc) return rc;
   rc = compute_max_batch(g);
+  if (rc) return rc;
+  rc = plan_bucket(g);
   if (rc) return rc;
   g->matrix_bytes = 0;
   for (auto& s : g->sh) {
@@ -624,8 +685,7 @@ void destroy_graph(sssp_graph* g) {
     cudaFree(s.d_visit);
     pool_free(s, s.d_adjT);
     if (s.stream) cudaStreamSynchronize(s.stream);
-    cudaFree(s.d_bitmap);
-    cudaFree(s.d_ctrl);
+    cudaFree(s.d_info2);
     cudaFree(s.d_trace);
     if (s.h_sources) cudaFreeHost(s.h_sources);
     if (s.h_info) cudaFreeHost(s.h_info);
@@ -674,41 +734,67 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
   for (uint32_t i = 0; i < k; ++i)
     if (sources[i] >= g->n) return fail(SSSP_ERR_BAD_SOURCE, "dijkstra: source out of range");
   if (g->bucket) {
-    Shard& s = g->sh[0];
-    CK(cudaSetDevice(s.device));
-    if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
-    void* fn = g->wbytes == 1 ? (void*)bucket_kernel<uint8_t>
-               : g->wbytes == 2 ? (void*)bucket_kernel<uint16_t> : (void*)bucket_kernel<uint32_t>;
-    const size_t cpt = 16 / g->wbytes, ksz = g->wbytes == 1 ? 4 : 8;
-    const size_t smem = bucket_smem_bytes(s.bT, s.bG, (uint32_t)(s.row_stride / 32), g->wbytes);
-    (void)cpt;
-    (void)ksz;
-    for (uint32_t i = 0; i < k; ++i) {
-      BucketParams bp{};
-      bp.adj = s.d_adj;
-      bp.adjT = s.pull_src;
-      bp.row_stride = s.row_stride;
-      bp.n = (uint32_t)g->n;
-      bp.Q = s.G;
-      bp.L = s.L;
-      bp.qbits = bitlen(s.G) - 1;
-      bp.lbits = bitlen(s.L) - 1;
-      bp.T = s.bT;
-      bp.source = (uint32_t)sources[i];
-      bp.bitmap = s.d_bitmap;
-      bp.ctrl = s.d_ctrl;
-      bp.dist_out = s.d_dist + (uint64_t)i * s.loc_n;
-      bp.pred_out = s.d_pred + (uint64_t)i * s.loc_n;
-      bp.info = s.d_info + (uint64_t)i * 4;
-      if (getenv("SSSP_BUCKET_TRACE")) {  // debug: per-barrier timestamps to stderr
-        if (!s.d_trace) CK(cudaMalloc(&s.d_trace, 64 * 8));
-        CK(cudaMemsetAsync(s.d_trace, 0, 64 * 8, s.stream));
-        bp.trace = s.d_trace;
-      }
-      void* args[] = {&bp};
-      CK(cudaLaunchCooperativeKernel(fn, dim3(s.bG), dim3(kBucketThreads), args, smem, s.stream));
+    void* fn = bucket_fn(g->wbytes);
+    const size_t smem = bucket_smem(g);
+    for (auto& s : g->sh) {
+      CK(cudaSetDevice(s.device));
+      if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
+      CK(cudaMemsetAsync(s.d_info2, 0, (uint64_t)k * 2 * sizeof(uint64_t), s.stream));
     }
-    CK(cudaEventRecord(s.ev1, s.stream));
+    for (uint32_t i = 0; i < k; ++i) {
+      for (auto& s : g->sh) {
+        CK(cudaSetDevice(s.device));
+        BucketParams bp{};
+        bp.adj = s.d_adj;
+        bp.adjT = s.pull_src;
+        bp.adjT_by_pos = s.pull_src == s.d_adj ? 0u : 1u;  // transpose rows: local positions
+        bp.adjT_stride = s.pull_src == s.d_adj ? s.row_stride : s.row_stride * g->P;
+        bp.row_stride = s.row_stride;
+        bp.n = (uint32_t)g->n;
+        bp.Q = s.G;
+        bp.L = s.L;
+        bp.qbits = bitlen(s.G) - 1;
+        bp.lbits = bitlen(s.L) - 1;
+        bp.T = g->bT;
+        bp.source = (uint32_t)sources[i];
+        bp.nshards = g->P;
+        bp.shard = s.k;
+        bp.loc_n = (uint32_t)s.loc_n;
+        for (uint32_t j = 0; j < g->P; ++j) {
+          char* base = reinterpret_cast<char*>(g->multiproc ? (void*)s.peer[j] : (void*)g->sh[j].d_slots) +
+                       g->slots_bytes;
+          bp.peer_ctrl[j] = reinterpret_cast<uint32_t*>(base + g->ctrl_off);
+          bp.peer_bitmap[j] = reinterpret_cast<uint32_t*>(base + g->bm_off);
+          bp.peer_bar[j] = reinterpret_cast<unsigned long long*>(base + g->bar_off);
+        }
+        bp.bar_epoch = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(s.d_slots) + g->slots_bytes + g->epoch_off);
+        bp.timeout_ns = g->opt.timeout_ms * 1000000ull;
+        bp.dist_out = s.d_dist + (uint64_t)i * s.loc_n;
+        bp.pred_out = s.d_pred + (uint64_t)i * s.loc_n;
+        bp.info = s.d_info + (uint64_t)i * 4;
+        bp.info2 = s.d_info2 + (uint64_t)i * 2;
+        if (getenv("SSSP_BUCKET_TRACE") && s.k == 0) {  // debug: per-barrier timestamps
+          if (!s.d_trace) CK(cudaMalloc(&s.d_trace, 64 * 8));
+          CK(cudaMemsetAsync(s.d_trace, 0, 64 * 8, s.stream));
+          bp.trace = s.d_trace;
+        }
+        void* args[] = {&bp};
+        if (g->P == 1) {
+          CK(cudaLaunchCooperativeKernel(fn, dim3(g->bG), dim3(kBucketThreads), args, smem, s.stream));
+        } else {  // co-residency was checked in plan_bucket; cross-shard barrier in-kernel
+          cudaLaunchConfig_t cfg{};
+          cfg.gridDim = dim3(g->bG);
+          cfg.blockDim = dim3(kBucketThreads);
+          cfg.dynamicSmemBytes = smem;
+          cfg.stream = s.stream;
+          CK(cudaLaunchKernelExC(&cfg, fn, args));
+        }
+      }
+    }
+    for (auto& s : g->sh) {
+      CK(cudaSetDevice(s.device));
+      CK(cudaEventRecord(s.ev1, s.stream));
+    }
     g->pending = k;
     g->queued += 1;
     return SSSP_OK;
@@ -785,15 +871,24 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     CK(cudaSetDevice(s.device));
     CK(cudaMemcpyAsync(s.h_info, s.d_info, (uint64_t)k * 4 * sizeof(uint64_t),
                        cudaMemcpyDeviceToHost, s.stream));
+    if (g->bucket) {
+      uint64_t i2[2 * 64] = {};
+      CK(cudaMemcpyAsync(i2, s.d_info2, std::min<uint64_t>(k, 64) * 2 * sizeof(uint64_t),
+                         cudaMemcpyDeviceToHost, s.stream));
+      CK(cudaStreamSynchronize(s.stream));
+      for (uint32_t i = 0; i < std::min<uint32_t>(k, 64); ++i) timeout |= i2[2 * i + 1] != 0;
+    }
     CK(cudaStreamSynchronize(s.stream));
     float ms = 0;
     CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
     rounds = std::max(rounds, ms * 1e-3 / std::max(1u, g->queued));
     for (uint32_t i = 0; i < k; ++i) {
       if (g->bucket) {
-        iters += s.h_info[4 * i];
-        classes += s.h_info[4 * i + 1];
-        rows += s.h_info[4 * i + 2] + s.h_info[4 * i + 3];
+        if (s.k == g->sh[0].k) {
+          iters += s.h_info[4 * i];
+          classes += s.h_info[4 * i + 1];
+          rows += s.h_info[4 * i + 2] + s.h_info[4 * i + 3];
+        }
         continue;
       }
       iters += s.k == g->sh[0].k ? s.h_info[4 * i] : 0;
@@ -978,7 +1073,10 @@ int sssp_shard_create(const uint64_t* block, uint64_t ld, uint64_t n, uint32_t w
     rc = upload_shard(g->sh[0], block, ld, n, max_weight, &wb, &mx, &mn);
     g->wbytes = wb;
     g->max_w = std::max(mx, max_weight);
-    g->min_w = mn;
+    // the bucket engine must be chosen identically on every rank: with several
+    // ranks only the caller-supplied global minimum counts
+    g->min_w = world == 1 ? mn
+               : g->opt.global_min_weight >= 0 ? (uint64_t)g->opt.global_min_weight : 0;
     // all ranks must agree on the encoding: derive it from the global bound
     if (rc == SSSP_OK && max_weight) {
       const uint32_t want = max_weight <= 0xFE ? 1 : max_weight <= 0xFFFE ? 2 : 4;
@@ -993,6 +1091,31 @@ int sssp_shard_create(const uint64_t* block, uint64_t ld, uint64_t n, uint32_t w
   }
   g->transfer_in_s = now_s() - t0;
   *out = g;
+  return SSSP_OK;
+}
+
+int sssp_block_weight_range(const uint64_t* block, uint64_t ld, uint64_t n, uint64_t col_begin,
+                            uint64_t col_count, uint64_t* min_offdiag, uint64_t* max_finite) {
+  if (!block || !min_offdiag || !max_finite || ld < col_count)
+    return fail(SSSP_ERR_BAD_ARG, "bad block");
+  const unsigned nt = narrow_threads();
+  std::vector<uint64_t> mn(nt, ~0ull), mx(nt, 0);
+  parallel_run([&](unsigned t) {
+    uint64_t lo = ~0ull, hi = 0;
+    for (uint64_t r = n * t / nt; r < n * (t + 1) / nt; ++r) {
+      const uint64_t* row = block + r * ld;
+      for (uint64_t j = 0; j < col_count; ++j) {
+        const uint64_t x = row[j];
+        if (x == ~0ull) continue;
+        hi = std::max(hi, x);
+        if (col_begin + j != r) lo = std::min(lo, x);
+      }
+    }
+    mn[t] = lo;
+    mx[t] = hi;
+  });
+  *min_offdiag = *std::min_element(mn.begin(), mn.end());
+  *max_finite = *std::max_element(mx.begin(), mx.end());
   return SSSP_OK;
 }
 

@@ -54,9 +54,21 @@ def open_shard(block: np.ndarray, n: int, max_weight: int, device: int, group=No
                **kw) -> ShardGraph:
     """Creates this rank's shard from its column block and connects it to the
     other ranks' shards."""
+    import torch
     import torch.distributed as dist
+    from . import block_weight_range
     world, rank = dist.get_world_size(group), dist.get_rank(group)
-    sg = ShardGraph(block, n, world, rank, max_weight, device, **kw)
+    # every rank must pick the same engine: agree on the graph's weight range
+    b, c = shard_range(n, world, rank)
+    mn, mx = block_weight_range(block, n, b) if c else (None, 0)
+    t = torch.tensor([-(2**62) if mn is None else -int(mn), int(mx)], dtype=torch.int64)
+    if dist.get_backend(group) == "nccl":
+        t = t.cuda()
+    dist.all_reduce(t, op=dist.ReduceOp.MAX, group=group)
+    gmin = int(-t[0])
+    gmin = -1 if gmin >= 2**62 else gmin
+    kw.setdefault("global_min_weight", gmin if gmin >= 0 else -1)
+    sg = ShardGraph(block, n, world, rank, max(max_weight, int(t[1])), device, **kw)
     sg.connect(exchange_handles(sg.export(), group))
     return sg
 

@@ -42,7 +42,7 @@ def test_abi_constants_and_strings():
     assert _native.lib.sssp_abi_version() == 1
     for code in range(9):
         assert _native.lib.sssp_status_string(code)
-    assert ctypes.sizeof(_native.Options) == 40
+    assert ctypes.sizeof(_native.Options) == 48
     assert ctypes.sizeof(_native.Stats) == 88
 
 

@@ -21,9 +21,9 @@ def rand_graph(rng, n, wlo, whi, density, directed):
     return adj
 
 
-def check(gpu, oracle_c, g, s, **kw):
+def check(gpu, oracle_c, g, s, devices=(0,), **kw):
     d, p = oracle_c.serial(g.adj, g.n, s)
-    with gpu.DeviceGraph(g, **kw) as dg:
+    with gpu.DeviceGraph(g, devices, **kw) as dg:
         info = dg.info()
         r = dg.solve(s)
     ok = np.array_equal(r.dist, d) and np.array_equal(r.pred, p)
@@ -108,3 +108,24 @@ def test_bucket_config3(gpu, oracle_c):
     g = gpu.generate_dense(32768, 32768)
     info, r = check(gpu, oracle_c, g, 0, engine="bucket")
     assert r.stats["classes"] == 4
+
+
+@pytest.mark.parametrize("P", [2, 3, 4, 8])
+def test_bucket_logical_shards(gpu, oracle_c, P):
+    """Bucket engine over P column shards on one GPU: global class bitmap
+    all-gathered by every tile into every shard, cross-shard barrier by
+    system-scope atomics, pull from the sharded transpose."""
+    rng = np.random.default_rng(P)
+    cases = [gpu.generate_dense(1000, 3), gpu.generate_sparse(2049, 4),
+             gpu.generate_sparse(1500, 5, directed=True),
+             gpu.Graph(700, True, rand_graph(rng, 700, 1, 3, 0.02, True))]
+    for g in cases:
+        for s in (0, g.n - 1):
+            info, r = check(gpu, oracle_c, g, s, devices=[0] * P)
+            assert info["engine"] == 3 and info["shards"] == P
+
+
+def test_bucket_logical_shards_config3(gpu, oracle_c):
+    g = gpu.generate_dense(32768, 32768)
+    info, r = check(gpu, oracle_c, g, 0, devices=[0, 0])
+    assert info["engine"] == 3 and r.stats["classes"] == 4
