@@ -117,7 +117,7 @@ __host__ __device__ constexpr uint32_t bucket_round4(uint32_t x) { return (x + 3
 // dynamic shared memory of bucket_kernel (keeps every region 16 B aligned)
 __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t T, uint32_t G, uint32_t words,
                                                        uint32_t wbytes);
-constexpr int kBucketChunk = kBucketThreads * 32;  // ids of one pass over 256 bitmap words
+constexpr int kBucketChunk = kBucketThreads * 32 * 2;  // ids of one pass over 512 bitmap words
 
 // Dynamic smem: dist[T] u32 | pred[T] u32 | settled[T/32] u32 | lmin[GT] u32 |
 //               bitmap[nshards*row_stride/32] u32 | chunk[kBucketChunk] u32 |
@@ -152,6 +152,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
   uint32_t* schunk = sbm + bucket_round4(words);
   K* scomb = reinterpret_cast<K*>(schunk + kBucketChunk);
   __shared__ uint32_t s_red[kBucketThreads / 32];
+  __shared__ uint32_t s_red2[kBucketThreads / 32], s_red3[kBucketThreads / 32];
   __shared__ uint32_t s_cnt[2];
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -269,45 +270,56 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
   uint32_t step = 0;
   while (!failed) {
     const uint32_t par = (uint32_t)((bar_base + nbar - 1) & 1ull), nxt = par ^ 1u;
-    // ---- the class: d = min over tiles, B_d = candidates of the tiles at d
-    uint32_t d = DINF, bcount = 0, uns = 0;
-    for (uint32_t c = tid; c < G; c += kBucketThreads) {
-      const uint32_t lm = __ldcg(&glob[(par * 3 + 0) * G + c]);
-      slmin[c] = lm;
-      d = min(d, lm);
+    // ---- the class: d = min over tiles, B_d = candidates of the tiles at d.
+    // One memory round trip: every tile's (lmin, candidates, unsettled) and
+    // the whole candidate bitmap are loaded together, then reduced in smem.
+    {
+      const uint32_t* bm = gbm + par * words;
+      for (uint32_t i = tid; i < words; i += kBucketThreads) sbm[i] = __ldcg(&bm[i]);
+    }
+    uint32_t lm_r[4], cc_r[4], uu_r[4];  // G <= 4 * kBucketThreads tiles (host-checked)
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      const uint32_t c = tid + k2 * kBucketThreads;
+      lm_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 0) * G + c]) : DINF;
+      cc_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 1) * G + c]) : 0u;
+      uu_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 2) * G + c]) : 0u;
+    }
+    uint32_t d = DINF;
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      const uint32_t c = tid + k2 * kBucketThreads;
+      if (c < G) slmin[c] = lm_r[k2];
+      d = min(d, lm_r[k2]);
     }
     d = __reduce_min_sync(0xFFFFFFFFu, d);
     if (lane == 0) s_red[warp] = d;
     __syncthreads();
     for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) d = min(d, s_red[w2]);
     if (d == DINF) break;  // uniform: every CTA reads the same values
-    for (uint32_t c = tid; c < G; c += kBucketThreads) {
-      if (slmin[c] == d) bcount += __ldcg(&glob[(par * 3 + 1) * G + c]);
-      uns += __ldcg(&glob[(par * 3 + 2) * G + c]);
+    uint32_t bcount = 0, uns = 0;
+#pragma unroll
+    for (int k2 = 0; k2 < 4; ++k2) {
+      bcount += lm_r[k2] == d ? cc_r[k2] : 0u;
+      uns += uu_r[k2];
     }
     bcount = __reduce_add_sync(0xFFFFFFFFu, bcount);
     uns = __reduce_add_sync(0xFFFFFFFFu, uns);
-    __syncthreads();  // s_red reuse
     if (lane == 0) {
-      s_red[warp] = bcount;
+      s_red2[warp] = bcount;
+      s_red3[warp] = uns;
     }
+    // mask the staged bitmap to the tiles at d
+    for (uint32_t i = tid; i < words; i += kBucketThreads)
+      if (slmin[i / TW] != d) sbm[i] = 0u;
     __syncthreads();
     bcount = 0;
-    for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) bcount += s_red[w2];
-    __syncthreads();
-    if (lane == 0) s_red[warp] = uns;
-    __syncthreads();
     uns = 0;
-    for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) uns += s_red[w2];
-    const uint32_t ucount = uns - bcount;  // unsettled after settling B_d
-    // stage B_d (candidates of the tiles at d) in shared memory: every
-    // later bitmap lookup of this class hits smem, not a few hot L2 lines
-    {
-      const uint32_t* bm = gbm + par * words;
-      for (uint32_t i = tid; i < words; i += kBucketThreads)
-        sbm[i] = slmin[i / TW] == d ? __ldcg(&bm[i]) : 0u;
+    for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) {
+      bcount += s_red2[w2];
+      uns += s_red3[w2];
     }
-    __syncthreads();
+    const uint32_t ucount = uns - bcount;  // unsettled after settling B_d
     // settle my candidates if my tile is in the class
     for (uint32_t i = tid; i < TW; i += kBucketThreads) ssettled[i] |= sbm[me * TW + i];
     __syncthreads();
@@ -324,11 +336,19 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
       K best[CPT];
 #pragma unroll
       for (int j = 0; j < CPT; ++j) best[j] = KT::kNone;
-      for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads) {
-        const uint32_t wi = wbase + tid;
-        const uint32_t bw = wi < words ? sbm[wi] : 0u;
-        if (!__syncthreads_or(bw != 0)) continue;
-        const uint32_t c = __popc(bw);
+      // enumerate B_d in ascending order: each pass takes 2 bitmap words per
+      // thread (<= kBucketChunk ids) with one block scan
+      constexpr uint32_t WPT = 2;
+      for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads * WPT) {
+        const uint32_t w0 = wbase + tid * WPT;
+        uint32_t bw[WPT];
+        uint32_t c = 0;
+#pragma unroll
+        for (uint32_t k2 = 0; k2 < WPT; ++k2) {
+          bw[k2] = w0 + k2 < words ? sbm[w0 + k2] : 0u;
+          c += __popc(bw[k2]);
+        }
+        if (!__syncthreads_or(c != 0)) continue;
         uint32_t incl = c;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -343,8 +363,10 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
           tot += s_red[w2];
         }
         uint32_t o = wofs + incl - c;
-        for (uint32_t m = bw; m; m &= m - 1)
-          schunk[o++] = gvid(wi * 32 + (__ffs(m) - 1));
+#pragma unroll
+        for (uint32_t k2 = 0; k2 < WPT; ++k2)
+          for (uint32_t m = bw[k2]; m; m &= m - 1)
+            schunk[o++] = gvid((w0 + k2) * 32 + (__ffs(m) - 1));
         __syncthreads();
         // batches of 8 rows: all 8 loads are issued before any is consumed
         for (uint32_t r0 = rg; r0 < tot; r0 += 8 * RG) {

@@ -527,7 +527,8 @@ int plan_bucket(sssp_graph* g) {
     g->bT = T;
     g->bG = (uint32_t)(s0.row_stride / T);
     const size_t smem = bucket_smem(g);
-    bool fits = T * g->wbytes / 16 <= kBucketThreads && smem <= 200 * 1024;
+    bool fits = T * g->wbytes / 16 <= kBucketThreads && smem <= 200 * 1024 &&
+                (uint64_t)g->bG * g->P <= 4ull * kBucketThreads;  // kernel: 4 tiles per thread
     for (const auto& s : g->sh) {
       if (!fits) break;
       CK(cudaSetDevice(s.device));
