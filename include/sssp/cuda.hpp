@@ -65,6 +65,24 @@ class DeviceGraph {
                             static_cast<int>(devices.size()), opt, &h_),
           "sssp_graph_create");
   }
+  // Built on the device from the reference's EdgeList (graph.hpp:20-26) with
+  // graph_from_edges semantics (graph.hpp:73-88); `directed` is the -w switch.
+  DeviceGraph(const EdgeList& el, bool directed, std::vector<int> devices = {0},
+              const sssp_options* opt = nullptr)
+      : n_(el.n) {
+    std::vector<std::uint64_t> e;
+    e.reserve(el.edges.size() * 3);
+    for (const Edge& x : el.edges) {
+      e.push_back(x.u);
+      e.push_back(x.v);
+      e.push_back(x.w);
+    }
+    const int rc = sssp_graph_create_from_edges(el.n, e.data(), el.edges.size(), directed ? 1 : 0,
+                                                devices.data(), static_cast<int>(devices.size()),
+                                                opt, &h_);
+    if (rc == SSSP_ERR_BAD_ARG) throw std::invalid_argument("graph_from_edges: bad edge");
+    check(rc, "sssp_graph_create_from_edges");
+  }
   DeviceGraph(const DeviceGraph&) = delete;
   DeviceGraph& operator=(const DeviceGraph&) = delete;
   DeviceGraph(DeviceGraph&& o) noexcept : h_(std::exchange(o.h_, nullptr)), n_(o.n_) {}

@@ -243,6 +243,28 @@ class DeviceGraph:
         self._h = h
         self.row_len = g.n
 
+    @classmethod
+    def from_edges(cls, n: int, edges, directed: bool, devices: Sequence[int] = (0,), **kw):
+        """Builds the matrix ON THE DEVICE from (u, v, w) triples: the
+        reference's graph_from_edges (graph.hpp:73-88) without the n*n host
+        matrix.  Same keywords as the constructor."""
+        self = cls.__new__(cls)
+        e = np.ascontiguousarray(np.asarray(edges, dtype=np.uint64).reshape(-1, 3))
+        self.n = n
+        self._opt = _options(kw.get("flags"), kw.get("ctas", 0), kw.get("max_batch", 0),
+                             kw.get("timeout_ms", 0), kw.get("visit_order", False),
+                             kw.get("replicas", 0), kw.get("engine", "auto"), kw.get("warps", 0))
+        devs = (ctypes.c_int * len(devices))(*devices)
+        h = ctypes.c_void_p()
+        st = lib.sssp_graph_create_from_edges(n, _p64(e), len(e), int(directed), devs, len(devices),
+                                              ctypes.byref(self._opt), ctypes.byref(h))
+        if st == _native.SSSP_ERR_BAD_ARG:
+            raise ValueError("graph_from_edges: endpoint out of range, self-loop or weight > 2^32-1")
+        check(st, "sssp_graph_create_from_edges")
+        self._h = h
+        self.row_len = n
+        return self
+
     # -- lifecycle
     def close(self):
         if getattr(self, "_h", None):

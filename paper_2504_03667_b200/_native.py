@@ -27,7 +27,7 @@ SSSP_FLAGS_DEFAULT = 3
 # every symbol include/*.h declares (checked by tests/test_abi.py)
 EXPORTED = (
     "sssp_status_string", "sssp_last_error", "sssp_abi_version", "sssp_device_count",
-    "sssp_graph_create", "sssp_shard_create", "sssp_shard_export", "sssp_shard_connect",
+    "sssp_graph_create", "sssp_graph_create_from_edges", "sssp_shard_create", "sssp_shard_export", "sssp_shard_connect",
     "sssp_shard_range", "sssp_graph_destroy", "sssp_graph_info", "sssp_solve",
     "sssp_solve_batch", "sssp_enqueue", "sssp_finish", "sssp_stream",
     "sssp_probe_sync", "sssp_block_weight_range", "sssp_gen_dense", "sssp_gen_sparse", "sssp_gen_bernoulli", "sssp_graph_from_edges",
@@ -88,6 +88,10 @@ def _load() -> ctypes.CDLL:
         "sssp_graph_create": (ctypes.c_int, [_u64p, ctypes.c_uint64, ctypes.c_int,
                                              ctypes.POINTER(ctypes.c_int), ctypes.c_int,
                                              ctypes.POINTER(Options), ctypes.POINTER(_vp)]),
+        "sssp_graph_create_from_edges": (ctypes.c_int, [ctypes.c_uint64, _u64p, ctypes.c_uint64,
+                                                        ctypes.c_int, ctypes.POINTER(ctypes.c_int),
+                                                        ctypes.c_int, ctypes.POINTER(Options),
+                                                        ctypes.POINTER(_vp)]),
         "sssp_shard_create": (ctypes.c_int, [_u64p, ctypes.c_uint64, ctypes.c_uint64,
                                              ctypes.c_uint32, ctypes.c_uint32, ctypes.c_uint64,
                                              ctypes.c_int, ctypes.POINTER(Options),

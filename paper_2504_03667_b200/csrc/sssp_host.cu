@@ -81,6 +81,59 @@ __global__ void permute_rows_kernel(const W* __restrict__ stage, uint32_t cols,
   }
 }
 
+// ---- device-side graph_from_edges (graph.hpp:73-88) into the permuted layout
+
+// Rows u < n: INF everywhere, 0 on the diagonal (graph.hpp:37-44).
+template <typename W>
+__global__ void init_matrix_kernel(W* __restrict__ a, uint64_t n, uint64_t row_stride,
+                                   uint64_t col_base, uint64_t cols, uint32_t G, uint32_t L) {
+  const uint64_t total = n * row_stride;
+  for (uint64_t idx = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; idx < total;
+       idx += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = idx / row_stride;
+    const uint32_t q = (uint32_t)(idx - u * row_stride);
+    const uint32_t c = q / L, sl = q - c * L;
+    const uint64_t vl = (uint64_t)sl * G + c;
+    a[idx] = (vl < cols && col_base + vl == u) ? (W)0 : (W)WInf<W>::v;
+  }
+}
+
+// Keep-the-minimum store of w into cell (u, position of local column vl);
+// sub-word weights use a CAS on the containing 32-bit word.
+template <typename W>
+__device__ __forceinline__ void min_cell(W* a, uint64_t row_stride, uint64_t u, uint64_t vl,
+                                         uint32_t G, uint32_t L, uint32_t w) {
+  const uint64_t pos = (vl % G) * L + vl / G;
+  W* cell = a + u * row_stride + pos;
+  if constexpr (sizeof(W) == 4) {
+    atomicMin(reinterpret_cast<unsigned int*>(cell), w);
+  } else {
+    unsigned int* word = reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(cell) & ~(uintptr_t)3);
+    const uint32_t sh = (uint32_t)((reinterpret_cast<uintptr_t>(cell) & 3) * 8);
+    const uint32_t mask = (uint32_t)WInf<W>::v << sh;
+    unsigned int old = *word, assumed;
+    do {
+      assumed = old;
+      if (((assumed & mask) >> sh) <= w) break;
+      old = atomicCAS(word, assumed, (assumed & ~mask) | (w << sh));
+    } while (old != assumed);
+  }
+}
+
+template <typename W>
+__global__ void scatter_edges_kernel(const uint64_t* __restrict__ e, uint64_t m, W* __restrict__ a,
+                                     uint64_t row_stride, uint64_t col_base, uint64_t cols,
+                                     uint32_t G, uint32_t L, int directed) {
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m;
+       i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t u = e[3 * i], v = e[3 * i + 1];
+    const uint32_t w = (uint32_t)e[3 * i + 2];
+    if (v >= col_base && v < col_base + cols) min_cell<W>(a, row_stride, u, v - col_base, G, L, w);
+    if (!directed && u >= col_base && u < col_base + cols)
+      min_cell<W>(a, row_stride, v, u - col_base, G, L, w);
+  }
+}
+
 template <typename F>
 void parallel_for(uint64_t begin, uint64_t end, unsigned nthreads, F&& f) {
   if (end <= begin) return;
@@ -950,6 +1003,71 @@ int copy_out(sssp_graph* g, uint32_t k, uint64_t* dist_out, uint64_t* pred_out,
 
 }  // namespace
 
+namespace {
+
+// Uploads an edge list into every shard's matrix: H2D of the (u, v, w)
+// triples in pinned chunks, then init + keep-minimum scatter on the device.
+template <typename W>
+int build_from_edges(sssp_graph* g, Shard& s, const uint64_t* edges, uint64_t m) {
+  CK(cudaSetDevice(s.device));
+  int rc = alloc_matrix(s, g->n, sizeof(W));
+  if (rc) return rc;
+  const uint64_t total = g->n * s.row_stride;
+  init_matrix_kernel<W><<<(unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 32), 256, 0,
+                          s.stream>>>(static_cast<W*>(s.d_adj), g->n, s.row_stride, s.col_base,
+                                      s.cols, s.G, s.L);
+  CK(cudaGetLastError());
+  if (m == 0) return SSSP_OK;
+  std::lock_guard<std::mutex> staging_lock(g_staging.m);
+  const uint64_t chunk = std::min<uint64_t>(m, 1ull << 20);  // edges per chunk (24 MB)
+  void* dbuf[2] = {nullptr, nullptr};
+  cudaEvent_t done[2] = {nullptr, nullptr};
+  for (int b = 0; b < 2; ++b) {
+    if (!g_staging.get(b, chunk * 24) || pool_alloc(s, &dbuf[b], chunk * 24) != SSSP_OK)
+      return fail(SSSP_ERR_OOM, "edge staging");
+    CK(cudaEventCreateWithFlags(&done[b], cudaEventDisableTiming));
+  }
+  bool used[2] = {false, false};
+  for (uint64_t e0 = 0, k = 0; e0 < m; e0 += chunk, ++k) {
+    const int b = (int)(k & 1);
+    const uint64_t cnt = std::min(chunk, m - e0);
+    if (used[b]) CK(cudaEventSynchronize(done[b]));
+    std::memcpy(g_staging.buf[b], edges + 3 * e0, cnt * 24);
+    CK(cudaMemcpyAsync(dbuf[b], g_staging.buf[b], cnt * 24, cudaMemcpyHostToDevice, s.stream));
+    scatter_edges_kernel<W><<<(unsigned)std::min<uint64_t>((cnt + 255) / 256, 148ull * 16), 256, 0,
+                              s.stream>>>(static_cast<const uint64_t*>(dbuf[b]), cnt,
+                                          static_cast<W*>(s.d_adj), s.row_stride, s.col_base,
+                                          s.cols, s.G, s.L, g->directed);
+    CK(cudaGetLastError());
+    CK(cudaEventRecord(done[b], s.stream));
+    used[b] = true;
+  }
+  CK(cudaStreamSynchronize(s.stream));
+  for (int b = 0; b < 2; ++b) {
+    cudaFreeAsync(dbuf[b], s.stream);
+    cudaEventDestroy(done[b]);
+  }
+  return SSSP_OK;
+}
+
+int enable_peers(const int* devices, int ndev) {
+  for (int i = 0; i < ndev; ++i)
+    for (int j = 0; j < ndev; ++j) {
+      if (devices[i] == devices[j]) continue;
+      int can = 0;
+      cudaDeviceCanAccessPeer(&can, devices[i], devices[j]);
+      if (!can) return fail(SSSP_ERR_NO_PEER, "no peer access between devices");
+      cudaSetDevice(devices[i]);
+      cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled)
+        return fail(SSSP_ERR_NO_PEER, cudaGetErrorString(e));
+      cudaGetLastError();
+    }
+  return SSSP_OK;
+}
+
+}  // namespace
+
 extern "C" {
 
 const char* sssp_status_string(int status) {
@@ -977,6 +1095,68 @@ int sssp_device_count(int* count) {
   return SSSP_OK;
 }
 
+int sssp_graph_create_from_edges(uint64_t n, const uint64_t* edges, uint64_t m, int directed,
+                                 const int* devices, int ndev, const sssp_options* opt,
+                                 sssp_graph** out) {
+  *out = nullptr;
+  if (n == 0 || (m && !edges)) return fail(SSSP_ERR_BAD_ARG, "empty graph");
+  if (n > 0x1FFFFFFFull) return fail(SSSP_ERR_UNSUPPORTED, "n exceeds 2^29");
+  if (ndev < 0 || ndev > SSSP_MAX_SHARDS) return fail(SSSP_ERR_BAD_ARG, "1..8 shards");
+  const int dev0 = 0;
+  if (!devices || ndev == 0) {
+    devices = &dev0;
+    ndev = 1;
+  }
+  int count = 0;
+  CK(cudaGetDeviceCount(&count));
+  for (int i = 0; i < ndev; ++i)
+    if (devices[i] < 0 || devices[i] >= count) return fail(SSSP_ERR_BAD_ARG, "bad device id");
+  // graph.hpp:80-83: the inputs graph_from_edges rejects; and the weight range
+  const double t0 = now_s();
+  const unsigned nt = narrow_threads();
+  std::vector<uint64_t> tmx(nt, 0), tmn(nt, ~0ull);
+  std::vector<char> bad(nt, 0);
+  parallel_run([&](unsigned t) {
+    uint64_t mx = 0, mn = ~0ull;
+    for (uint64_t i = m * t / nt; i < m * (t + 1) / nt; ++i) {
+      const uint64_t u = edges[3 * i], v = edges[3 * i + 1], w = edges[3 * i + 2];
+      if (u >= n || v >= n || u == v || w > 0xFFFFFFFFull) bad[t] = 1;
+      mx = std::max(mx, w);
+      mn = std::min(mn, w);
+    }
+    tmx[t] = mx;
+    tmn[t] = mn;
+  });
+  for (unsigned t = 0; t < nt; ++t)
+    if (bad[t]) return fail(SSSP_ERR_BAD_ARG, "edge endpoint out of range, self-loop or weight > 2^32-1");
+  const uint64_t max_w = *std::max_element(tmx.begin(), tmx.end());
+  const uint64_t min_w = *std::min_element(tmn.begin(), tmn.end());
+  if (max_w > 0xFFFFFFFEull)
+    return fail(SSSP_ERR_WEIGHT_RANGE, "finite weight 0xFFFFFFFF needs the wide encoding");
+  sssp_graph* g = new sssp_graph();
+  g->n = n;
+  g->directed = directed;
+  g->P = (uint32_t)ndev;
+  g->opt = default_options(opt);
+  g->max_w = max_w;
+  g->min_w = min_w;
+  g->wbytes = max_w <= 0xFE ? 1 : max_w <= 0xFFFE ? 2 : 4;
+  int rc = create_shard_objects(g, g->P, devices, g->P, 0);
+  if (rc == SSSP_OK) rc = enable_peers(devices, ndev);
+  for (uint32_t i = 0; rc == SSSP_OK && i < g->P; ++i)
+    rc = g->wbytes == 1 ? build_from_edges<uint8_t>(g, g->sh[i], edges, m)
+         : g->wbytes == 2 ? build_from_edges<uint16_t>(g, g->sh[i], edges, m)
+                          : build_from_edges<uint32_t>(g, g->sh[i], edges, m);
+  if (rc == SSSP_OK) rc = setup_common(g);
+  if (rc) {
+    destroy_graph(g);
+    return rc;
+  }
+  g->transfer_in_s = now_s() - t0;
+  *out = g;
+  return SSSP_OK;
+}
+
 int sssp_graph_create(const uint64_t* adj, uint64_t n, int directed, const int* devices,
                       int ndev, const sssp_options* opt, sssp_graph** out) {
   *out = nullptr;
@@ -999,24 +1179,7 @@ int sssp_graph_create(const uint64_t* adj, uint64_t n, int directed, const int* 
   g->P = (uint32_t)ndev;
   g->opt = default_options(opt);
   int rc = create_shard_objects(g, g->P, devices, g->P, 0);
-  // peer access between distinct devices
-  for (int i = 0; rc == SSSP_OK && i < ndev; ++i)
-    for (int j = 0; j < ndev; ++j) {
-      if (devices[i] == devices[j]) continue;
-      int can = 0;
-      cudaDeviceCanAccessPeer(&can, devices[i], devices[j]);
-      if (!can) {
-        rc = fail(SSSP_ERR_NO_PEER, "no peer access between devices");
-        break;
-      }
-      cudaSetDevice(devices[i]);
-      cudaError_t e = cudaDeviceEnablePeerAccess(devices[j], 0);
-      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) {
-        rc = fail(SSSP_ERR_NO_PEER, cudaGetErrorString(e));
-        break;
-      }
-      cudaGetLastError();
-    }
+  if (rc == SSSP_OK) rc = enable_peers(devices, ndev);
   // Several shards must agree on one encoding: take it from a scan of the
   // whole matrix.  A single shard widens optimistically inside the upload.
   uint64_t hint = 0;

@@ -4,6 +4,7 @@
 // Exit code 0 = every ShortestPathResult compares equal (result.hpp:18).
 #include <cstdio>
 #include <random>
+#include <sstream>
 
 #include "sssp/cuda.hpp"
 #include "sssp/sssp.hpp"
@@ -55,6 +56,16 @@ int main() {
         EXPECT(dijkstra_partitioned(g, s, 3).result == want);
         ++graphs;
       }
+  // device-side build from the reference's own parsed EdgeList (-w off and on)
+  {
+    std::istringstream in("5 6\n0 1 4\n1 2 1\n0 2 9\n2 3 2\n3 4 1\n0 1 3\n");
+    const EdgeList pel = parse_edge_list_text(in);
+    for (bool directed : {false, true}) {
+      cuda::DeviceGraph eg(pel, directed);
+      const Graph hg = graph_from_edges(pel, directed);
+      for (VertexId s = 0; s < 5; ++s) EXPECT(eg.solve(s) == dijkstra_serial(hg, s));
+    }
+  }
   // repeated solves + batch on one resident graph
   const Graph big = graph_from_edges(generate_dense(3000, 99), false);
   cuda::DeviceGraph dg(big);

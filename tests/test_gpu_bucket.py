@@ -129,3 +129,39 @@ def test_bucket_logical_shards_config3(gpu, oracle_c):
     g = gpu.generate_dense(32768, 32768)
     info, r = check(gpu, oracle_c, g, 0, devices=[0, 0])
     assert info["engine"] == 3 and r.stats["classes"] == 4
+
+
+@pytest.mark.parametrize("directed", [False, True])
+@pytest.mark.parametrize("wmax", [3, 200, 5000, 100000])
+def test_device_build_from_edges(gpu, oracle_c, directed, wmax):
+    """sssp_graph_create_from_edges == graph_from_edges (graph.hpp:73-88) on the
+    host: duplicates keep the minimum, undirected edges are mirrored."""
+    rng = np.random.default_rng(wmax + directed)
+    n, m = 900, 6000
+    u = rng.integers(0, n, m)
+    v = (u + rng.integers(1, n, m)) % n           # no self-loops
+    w = rng.integers(0 if wmax == 3 else 1, wmax + 1, m)
+    e = np.stack([u, v, w], 1).astype(np.uint64)
+    e = np.concatenate([e, e[:500] * np.array([1, 1, 0], np.uint64) + np.array([0, 0, 1], np.uint64)])
+    g = gpu.graph_from_edges(n, e, directed)
+    for s in (0, 450):
+        d, p = oracle_c.serial(g.adj, n, s)
+        with gpu.DeviceGraph.from_edges(n, e, directed) as dg:
+            r = dg.solve(s)
+        assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p)
+
+
+def test_device_build_rejects_like_reference(gpu):
+    for bad in ([(0, 5, 1)], [(2, 2, 1)], [(0, 1, 1 << 32)]):
+        with pytest.raises(ValueError):
+            gpu.DeviceGraph.from_edges(5, bad, False)
+
+
+def test_device_build_config1_and_shards(gpu, oracle_c):
+    e = oracle_c.sparse_edges(1000, 42)
+    adj = oracle_c.from_edges(1000, e, False)
+    d, p = oracle_c.serial(adj, 1000, 0)
+    for devs in ([0], [0, 0, 0]):
+        with gpu.DeviceGraph.from_edges(1000, e, False, devs) as dg:
+            r = dg.solve(0)
+        assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p)
