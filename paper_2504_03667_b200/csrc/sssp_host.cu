@@ -953,6 +953,13 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
   }
   g->pending = 0;
   g->queued = 0;
+  // AUTO re-plan: a distance class costs ~10x a scan round (measured: ~5 us vs
+  // ~0.5 us), so a graph whose solves need more than n/8 classes (long sparse
+  // paths: config 1 sparse has 154 classes at n=1000) runs faster on the
+  // n-round cluster engine from the next solve on.  Deterministic, hence
+  // identical on every shard/rank.
+  if (g->bucket && g->opt.engine == SSSP_ENGINE_AUTO && k > 0 && classes / k > g->n / 8)
+    g->bucket = false;
   if (g->multiproc) g->exch_base = last + 1;
   if (g->bucket && g->sh[0].d_trace) {
     uint64_t tr[64];
