@@ -166,6 +166,13 @@ int sssp_enqueue(sssp_graph* g, const uint64_t* sources, uint32_t k);
 int sssp_finish(sssp_graph* g, sssp_solve_stats* st);
 void* sssp_stream(sssp_graph* g, int local);
 
+/* validate_result (oracle.hpp:51-120) on the device against the stored matrix:
+ * *violations = number of failed checks (0 = a valid shortest-path tree with
+ * fixpoint distances).  dist/pred: n entries, reference encoding.  The
+ * reference harness refuses to time invalid results (bench.hpp:167-173). */
+int sssp_validate(sssp_graph* g, uint64_t source, const uint64_t* dist, const uint64_t* pred,
+                  uint64_t* violations);
+
 /* t_sync_min microbenchmark (the roofline's sync term): runs
  * `rounds` exchange rounds with the solve's launch shape and exchange code
  * but no relaxation; *seconds_per_round = max over shards of elapsed/rounds

@@ -326,6 +326,15 @@ class DeviceGraph:
         check(lib.sssp_finish(self._h, ctypes.byref(st)), "sssp_finish")
         return st.as_dict()
 
+    def validate(self, r: "ShortestPathResult") -> int:
+        """validate_result (oracle.hpp:51-120) on the device; 0 = valid."""
+        out = ctypes.c_uint64()
+        d = np.ascontiguousarray(r.dist, np.uint64)
+        p = np.ascontiguousarray(r.pred, np.uint64)
+        check(lib.sssp_validate(self._h, r.source, _p64(d), _p64(p), ctypes.byref(out)),
+              "sssp_validate")
+        return out.value
+
     def probe_sync(self, rounds: int = 20000) -> float:
         """Seconds per exchange round of the solve's own launch shape (t_sync_min)."""
         out = ctypes.c_double()

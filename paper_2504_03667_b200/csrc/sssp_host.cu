@@ -20,6 +20,7 @@
 
 #include "../../include/sssp_cuda.h"
 #include "bucket_kernel.cuh"
+#include "validate_kernel.cuh"
 #include "dispatch.h"
 #include "host_narrow.h"
 
@@ -1479,6 +1480,61 @@ int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round) {
   for (cudaEvent_t e : reset_ev) cudaEventDestroy(e);
   if (g->multiproc) g->exch_base = last + 1;
   *seconds_per_round = worst;
+  return SSSP_OK;
+}
+
+int sssp_validate(sssp_graph* g, uint64_t source, const uint64_t* dist, const uint64_t* pred,
+                  uint64_t* violations) {
+  if (!g || !dist || !pred || !violations) return fail(SSSP_ERR_BAD_ARG, "null argument");
+  if (source >= g->n) return fail(SSSP_ERR_BAD_SOURCE, "validate: source out of range");
+  if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
+  uint64_t total = 0;
+  const uint64_t n = g->n;
+  for (auto& s : g->sh) {
+    CK(cudaSetDevice(s.device));
+    void *dd = nullptr, *dp = nullptr, *dj = nullptr, *dj2 = nullptr, *db = nullptr;
+    int rc = pool_alloc(s, &dd, n * 8);
+    if (!rc) rc = pool_alloc(s, &dp, n * 8);
+    if (!rc) rc = pool_alloc(s, &db, 8);
+    if (!rc && s.k == 0) rc = pool_alloc(s, &dj, n * 8);
+    if (!rc && s.k == 0) rc = pool_alloc(s, &dj2, n * 8);
+    if (rc) return rc;
+    CK(cudaMemcpyAsync(dd, dist, n * 8, cudaMemcpyHostToDevice, s.stream));
+    CK(cudaMemcpyAsync(dp, pred, n * 8, cudaMemcpyHostToDevice, s.stream));
+    CK(cudaMemsetAsync(db, 0, 8, s.stream));
+    const uint64_t* D = static_cast<const uint64_t*>(dd);
+    const uint64_t* Pp = static_cast<const uint64_t*>(dp);
+    auto* B = static_cast<unsigned long long*>(db);
+    const unsigned grid = 148 * 8;
+#define SSSP_VALIDATE(W)                                                                        \
+  validate_edges_kernel<W><<<grid, 256, 0, s.stream>>>(static_cast<const W*>(s.d_adj), n,        \
+                                                       s.row_stride, s.col_base, s.cols, s.G,    \
+                                                       s.L, D, B);                               \
+  validate_pred_kernel<W><<<grid, 256, 0, s.stream>>>(static_cast<const W*>(s.d_adj), n,         \
+                                                      s.row_stride, s.col_base, s.cols, s.G, s.L, \
+                                                      source, D, Pp, B)
+    if (g->wbytes == 1) { SSSP_VALIDATE(uint8_t); }
+    else if (g->wbytes == 2) { SSSP_VALIDATE(uint16_t); }
+    else { SSSP_VALIDATE(uint32_t); }
+#undef SSSP_VALIDATE
+    if (s.k == 0) {
+      uint64_t* j0 = static_cast<uint64_t*>(dj);
+      uint64_t* j1 = static_cast<uint64_t*>(dj2);
+      chain_init_kernel<<<grid, 256, 0, s.stream>>>(D, Pp, n, source, j0);
+      for (uint64_t r = 1; r < 2 * n; r <<= 1) {  // ceil(log2 n) + 1 doublings
+        chain_jump_kernel<<<grid, 256, 0, s.stream>>>(j0, j1, n);
+        std::swap(j0, j1);
+      }
+      chain_check_kernel<<<grid, 256, 0, s.stream>>>(D, j0, n, source, B);
+    }
+    CK(cudaGetLastError());
+    uint64_t bad = 0;
+    CK(cudaMemcpyAsync(&bad, db, 8, cudaMemcpyDeviceToHost, s.stream));
+    CK(cudaStreamSynchronize(s.stream));
+    total += bad;
+    for (void* x : {dd, dp, dj, dj2, db}) pool_free(s, x);
+  }
+  *violations = total;
   return SSSP_OK;
 }
 
