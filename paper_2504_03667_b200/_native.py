@@ -10,7 +10,7 @@ import ctypes
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libsssp_cuda.so")
+LIB_PATH = os.environ.get("SSSP_LIB") or os.path.join(_HERE, "libsssp_cuda.so")  # SSSP_LIB: dev A/B builds
 
 SSSP_OK = 0
 SSSP_ERR_BAD_SOURCE = 1

@@ -58,6 +58,8 @@ struct BucketParams {
   uint32_t* peer_bitmap[kMaxShards];  // every shard's [2][nshards*row_stride/32] (self incl.)
   uint32_t* peer_ctrl[kMaxShards];    // every shard's [2][3][nshards*G]: tile lmin, cand, uns
   unsigned long long* peer_bar[kMaxShards];  // every shard's barrier counter (nshards > 1)
+  uint32_t* ubm;        // this shard's [2][row_stride/32]: published unsettled bitmap per tile
+  void* pkey;           // this shard's [row_stride] K: per-column pull minimum (balanced pull)
   uint64_t* bar_epoch;  // this shard's count of cross-shard barriers completed by earlier
                         // launches (read at start, advanced at exit; same on every shard)
   uint64_t timeout_ns;
@@ -66,6 +68,7 @@ struct BucketParams {
   uint64_t* info;       // [4]: settled vertices, classes, rows pushed, rows pulled
   uint64_t* info2;      // [2]: barriers used, error
   uint64_t* trace;      // optional [64]: %globaltimer after every barrier (CTA 0 of shard 0)
+  uint64_t seq;         // launch tag: a watchdog failure writes it to info2[1] (no reset needed)
 };
 
 __device__ __forceinline__ uint32_t pos_to_vid(uint32_t pos, uint32_t Q, uint32_t lbits,
@@ -94,9 +97,14 @@ struct BucketKey<uint16_t> {
 template <>
 struct BucketKey<uint32_t> : BucketKey<uint16_t> {};
 
+// shared- or global-memory atomic minimum of a packed key
 __device__ __forceinline__ void smem_min(uint32_t* a, uint32_t v) { atomicMin(a, v); }
 __device__ __forceinline__ void smem_min(uint64_t* a, uint64_t v) {
   atomicMin(reinterpret_cast<unsigned long long*>(a), (unsigned long long)v);
+}
+__device__ __forceinline__ uint32_t ld_cg(const uint32_t* a) { return __ldcg(a); }
+__device__ __forceinline__ uint64_t ld_cg(const uint64_t* a) {
+  return (uint64_t)__ldcg(reinterpret_cast<const unsigned long long*>(a));
 }
 
 template <typename K>
@@ -120,7 +128,7 @@ __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t T, uint32_t G, u
 constexpr int kBucketChunk = kBucketThreads * 32 * 2;  // ids of one pass over 512 bitmap words
 
 // Dynamic smem: dist[T] u32 | pred[T] u32 | settled[T/32] u32 | lmin[GT] u32 |
-//               bitmap[nshards*row_stride/32] u32 | chunk[kBucketChunk] u32 |
+//               bitmap[nshards*row_stride/32] u32 | unsettled[same] u32 | chunk[kBucketChunk] u32 |
 //               combine[kBucketThreads * CPT] keys
 //
 // One grid barrier per class.  Before the barrier that ends step s every CTA
@@ -130,14 +138,13 @@ constexpr int kBucketChunk = kBucketThreads * 32 * 2;  // ids of one pass over 5
 // of the tiles with lmin == d form B_d -- no second barrier is needed to
 // build the class.
 template <typename W>
-__global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketParams p) {
+__global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketParams p) {
   namespace cg = cooperative_groups;
   using KT = BucketKey<W>;
   using K = typename KT::T;
   constexpr uint32_t WINF = WInf<W>::v;
   constexpr uint32_t DINF = 0xFFFFFFFFu;
   constexpr int CPT = 16 / (int)sizeof(W);  // columns per thread (one 16 B load)
-  cg::grid_group grid = cg::this_grid();
 
   extern __shared__ __align__(16) uint32_t smem[];
   const uint32_t T = p.T, G = gridDim.x * p.nshards;  // G = tiles of ALL shards
@@ -149,7 +156,8 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
   uint32_t* ssettled = spred + T;
   uint32_t* slmin = ssettled + bucket_round4(TW);
   uint32_t* sbm = slmin + bucket_round4(G);  // B_d bitmap (all positions), staged per class
-  uint32_t* schunk = sbm + bucket_round4(words);
+  uint32_t* sub = sbm + bucket_round4(words);  // this shard's unsettled bitmap (pull steps)
+  uint32_t* schunk = sub + bucket_round4(words);
   K* scomb = reinterpret_cast<K*>(schunk + kBucketChunk);
   __shared__ uint32_t s_red[kBucketThreads / 32];
   __shared__ uint32_t s_red2[kBucketThreads / 32], s_red3[kBucketThreads / 32];
@@ -166,6 +174,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
   // global per-step arrays: ctrl = [2][3][G] (lmin, candidates, unsettled)
   uint32_t* const glob = p.peer_ctrl[p.shard];
   const uint32_t* const gbm = p.peer_bitmap[p.shard];
+  K* const pkey = static_cast<K*>(p.pkey);
   // global position -> global vertex id
   auto gvid = [&](uint32_t g) -> uint32_t {
     const uint32_t j = g >> (p.qbits + p.lbits);  // row_stride = Q*L = 2^(qbits+lbits)
@@ -177,16 +186,21 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
     if (p.trace && me == 0 && tid == 0 && ntr < 64) p.trace[ntr++] = globaltimer();
   };
   // One barrier over every CTA of every shard: the cooperative grid barrier
-  // with one shard; with several, each CTA bumps every shard's counter by a
-  // system-scope atomic (an NVLink write for a remote shard) and waits until
-  // its own shard's counter shows all G tiles of this barrier.
+  // with one shard (1.29 us at 256 CTAs, the fastest measured variant:
+  // profiles/r01_ubench_barrier.jsonl); with several, each CTA bumps every
+  // shard's counter by a system-scope atomic (an NVLink write for a remote
+  // shard) and waits until its own shard's counter shows all G tiles of this
+  // barrier.  The counter continues across launches (bar_epoch).
+  __shared__ uint32_t s_fail;
+  if (tid == 0) s_fail = 0;
   uint64_t nbar = 0;
   bool failed = false;
   const uint64_t t_start = globaltimer();
   const uint64_t bar_base = p.nshards > 1 ? *(volatile uint64_t*)p.bar_epoch : 0;
+  stamp();  // trace[0]: kernel start
   auto barrier = [&]() {
     if (p.nshards == 1) {
-      grid.sync();
+      cg::this_grid().sync();
     } else {
       __syncthreads();
       if (tid == 0) {
@@ -199,12 +213,14 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
           asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.peer_bar[p.shard]) : "memory");
           if (v >= target) break;
           if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) {
-            failed = true;
+            s_fail = 1;
+            p.info2[1] = p.seq;
             break;
           }
         }
       }
       __syncthreads();
+      failed = s_fail != 0;
     }
     ++nbar;
   };
@@ -224,16 +240,19 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
     __syncthreads();
     if (lane == 0) atomicAdd(&s_cnt[1], uns);
     for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) m = min(m, s_red[w2]);
-    for (uint32_t i = tid; i < TW; i += kBucketThreads) {
-      uint32_t cm = 0;
+    // candidate bitmap word i (columns 32i..32i+31) = one ballot of warp i % 8
+    for (uint32_t i = warp; i < TW; i += kBucketThreads / 32) {
       const uint32_t sm = ssettled[i];
-      if (m != DINF)
-        for (uint32_t b = 0; b < 32; ++b)
-          if (!((sm >> b) & 1u) && sdist[i * 32 + b] == m) cm |= 1u << b;
-      for (uint32_t j = 0; j < p.nshards; ++j)  // remote shards: P2P stores
-        p.peer_bitmap[j][par * words + me * TW + i] = cm;
-      if (cm) atomicAdd(&s_cnt[0], __popc(cm));
+      const uint32_t cm =
+          __ballot_sync(0xFFFFFFFFu, m != DINF && !((sm >> lane) & 1u) && sdist[i * 32 + lane] == m);
+      if (lane < p.nshards)  // remote shards: P2P stores
+        p.peer_bitmap[lane][par * words + me * TW + i] = cm;
+      if (lane == 31) {
+        p.ubm[par * lwords + blockIdx.x * TW + i] = ~sm;  // local only (pull work list)
+        if (cm) atomicAdd(&s_cnt[0], __popc(cm));
+      }
     }
+    for (uint32_t col = tid; col < T; col += kBucketThreads) pkey[p0 + col] = KT::kNone;
     __syncthreads();
     if (tid < p.nshards) {
       uint32_t* c = p.peer_ctrl[tid];
@@ -243,39 +262,51 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
     }
   };
 
-  // ---- init: dist = INF, pred = NONE, padding settled (serial.hpp:32-36)
+  // ---- init: dist = INF, pred = NONE, padding settled (serial.hpp:32-36),
+  // then class 0 = {source} -- with every weight >= 1 the only vertex at
+  // distance 0 -- settled and its row pushed by every CTA over its own tile
+  // without a barrier (every CTA knows the source): dist = w(s,v), pred = s
+  // for each finite w, exactly the serial engine's first round.
   const uint32_t vbase = p.shard * p.loc_n;
-  for (uint32_t i = tid; i < T; i += kBucketThreads) {
-    const uint32_t vl = pos_to_vid(p0 + i, p.Q, p.lbits, p.qbits);
-    sdist[i] = (vl < p.loc_n && vbase + vl == p.source) ? 0u : DINF;
-    spred[i] = 0xFFFFFFFFu;
-  }
   for (uint32_t i = tid; i < TW; i += kBucketThreads) {
     uint32_t m = 0;
     for (uint32_t b = 0; b < 32; ++b) {
       const uint32_t vl = pos_to_vid(p0 + i * 32 + b, p.Q, p.lbits, p.qbits);
-      if (vl >= p.loc_n || vbase + vl >= p.n) m |= 1u << b;
+      if (vl >= p.loc_n || vbase + vl >= p.n || vbase + vl == p.source) m |= 1u << b;
     }
     ssettled[i] = m;
   }
+  for (uint32_t i = tid; i < T; i += kBucketThreads) {
+    const uint32_t vl = pos_to_vid(p0 + i, p.Q, p.lbits, p.qbits);
+    const bool real = vl < p.loc_n && vbase + vl < p.n;
+    const uint32_t w = real ? (uint32_t)adj[(size_t)p.source * p.row_stride + p0 + i] : WINF;
+    const bool src = real && vbase + vl == p.source;
+    sdist[i] = src ? 0u : (w != WINF ? w : DINF);
+    spred[i] = (!src && w != WINF) ? p.source : 0xFFFFFFFFu;
+  }
   __syncthreads();
-  // Buffer parity follows the GLOBAL barrier count (it continues across
-  // launches): a fast shard's next launch then publishes into the buffer the
-  // slow shard is NOT reading after its final barrier.
+  // Buffer parity = parity of the barrier that follows the publish, counted
+  // GLOBALLY (the count continues across launches): a fast shard's next
+  // launch then publishes into the buffer the slow shard is NOT reading after
+  // its final barrier, and a step's extra (pull) barrier never lets a publish
+  // overwrite a buffer some CTA may still read.
   publish((uint32_t)(bar_base & 1ull));
   barrier();
   stamp();
 
-  uint64_t pushed = 0, pulled = 0, settled = 0;
-  uint32_t step = 0;
+  uint64_t pushed = 1, pulled = 0, settled = 1;
+  uint32_t step = 1;
   while (!failed) {
-    const uint32_t par = (uint32_t)((bar_base + nbar - 1) & 1ull), nxt = par ^ 1u;
+    const uint32_t par = (uint32_t)((bar_base + nbar - 1) & 1ull);
     // ---- the class: d = min over tiles, B_d = candidates of the tiles at d.
     // One memory round trip: every tile's (lmin, candidates, unsettled) and
     // the whole candidate bitmap are loaded together, then reduced in smem.
     {
       const uint32_t* bm = gbm + par * words;
       for (uint32_t i = tid; i < words; i += kBucketThreads) sbm[i] = __ldcg(&bm[i]);
+      // this shard's published unsettled bitmap, staged for a pull step
+      const uint32_t* ub = p.ubm + par * lwords;
+      for (uint32_t i = tid; i < lwords; i += kBucketThreads) sub[i] = __ldcg(&ub[i]);
     }
     uint32_t lm_r[4], cc_r[4], uu_r[4];  // G <= 4 * kBucketThreads tiles (host-checked)
 #pragma unroll
@@ -311,7 +342,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
     }
     // mask the staged bitmap to the tiles at d
     for (uint32_t i = tid; i < words; i += kBucketThreads)
-      if (slmin[i / TW] != d) sbm[i] = 0u;
+      if (slmin[i >> (tbits - 5)] != d) sbm[i] = 0u;  // TW = T/32 words per tile
     __syncthreads();
     bcount = 0;
     uns = 0;
@@ -323,6 +354,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
     // settle my candidates if my tile is in the class
     for (uint32_t i = tid; i < TW; i += kBucketThreads) ssettled[i] |= sbm[me * TW + i];
     __syncthreads();
+    stamp();
     ++step;
     settled += bcount;
     if (ucount == 0) break;  // nothing left to relax (the last class needs no rows)
@@ -415,76 +447,134 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
       }
       __syncthreads();
     } else {
-      // ---- PULL: stream column v (row v of the transpose) of every unsettled
-      // column of this tile, masked by B_d.  The (column, 16 B chunk) items are
-      // spread over all threads with 8 loads in flight each, so the tile's
-      // columns are read concurrently and evenly.
+      // ---- PULL, balanced over the whole shard: U = this shard's unsettled
+      // columns after B_d (the published unsettled bitmaps minus the class).
+      // The (column of U, 16 B chunk of its transposed row) items are split
+      // evenly over the shard's CTAs -- a CTA no longer waits on the columns
+      // of its own tile, whose count varies from tile to tile -- each CTA
+      // folds its partial (w, u) minima into pkey[column] with one global
+      // atomicMin per column it touched, and after an extra barrier every
+      // owner applies its columns' minima.
       pulled += ucount;
-      K* sk = scomb;                            // per unsettled column running key
-      uint32_t* slist = schunk;                 // unsettled columns of this tile
-      __shared__ uint32_t s_nu;
-      if (tid == 0) s_nu = 0;
+      K* sk = scomb;           // running key of the columns this CTA touches
+      uint32_t* scol = schunk; // their local positions (rank r0 + i)
+      const uint32_t* bml = sbm + p.shard * lwords;
+      const uint32_t wpt = (lwords + kBucketThreads - 1) / kBucketThreads;
+      const uint32_t w0 = tid * wpt;
+      auto uword = [&](uint32_t k2) -> uint32_t {  // unsettled-after-B_d word w0 + k2
+        return sub[w0 + k2] & ~bml[w0 + k2];
+      };
+      uint32_t c = 0;
+      for (uint32_t k2 = 0; k2 < wpt && w0 + k2 < lwords; ++k2) c += __popc(uword(k2));
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+      }
+      if (lane == 31) s_red[warp] = incl;
       __syncthreads();
-      for (uint32_t col = tid; col < T; col += kBucketThreads)
-        if (!((ssettled[col >> 5] >> (col & 31)) & 1u)) {
-          const uint32_t i = atomicAdd(&s_nu, 1u);
-          slist[i] = col;
-          sk[i] = KT::kNone;
-        }
-      __syncthreads();
-      const uint32_t nu = s_nu;
+      uint32_t base = 0, nuL = 0;
+      for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) {
+        if (w2 < warp) base += s_red[w2];
+        nuL += s_red[w2];
+      }
+      base += incl - c;  // rank of this thread's first unsettled column
       // chunks per transposed row (nshards * row_stride: not a power of two for P = 3, 5, 6, 7)
       const uint32_t cpr = (uint32_t)(p.adjT_stride * sizeof(W) / 16);
       const bool cpow2 = (cpr & (cpr - 1u)) == 0;  // uniform: shifts instead of divisions
       const uint32_t cbits = 31u - __clz(cpr);
-      const uint32_t total = nu * cpr;
+      const uint32_t total = nuL * cpr;
+      const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+      const uint32_t lo = min(total, blockIdx.x * per), hi = min(total, lo + per);
+      const uint32_t r0 = cpow2 ? lo >> cbits : lo / cpr;
+      const uint32_t ncols = lo < hi ? (cpow2 ? (hi - 1) >> cbits : (hi - 1) / cpr) - r0 + 1 : 0;
+      if (ncols && base < r0 + ncols && base + c > r0) {
+        uint32_t r = base;
+        for (uint32_t k2 = 0; k2 < wpt && w0 + k2 < lwords && r < r0 + ncols; ++k2)
+          for (uint32_t m = uword(k2); m; m &= m - 1, ++r)
+            if (r >= r0 && r < r0 + ncols) scol[r - r0] = (w0 + k2) * 32 + (__ffs(m) - 1);
+      }
+      for (uint32_t i = tid; i < ncols; i += kBucketThreads) sk[i] = KT::kNone;
+      __syncthreads();
+      stamp();
+      // kPullDepth independent 16 B loads in flight per thread.  A thread's
+      // items are lo + tid + k*256; their (column rank, chunk) pairs are
+      // walked incrementally (one division per thread, none per item).
+      constexpr int kPullDepth = 8;
+      auto row_of = [&](uint32_t rk) -> const uint8_t* {
+        const uint32_t col = scol[rk - r0];
+        const uint32_t v = p.adjT_by_pos ? col : pos_to_vid(col, p.Q, p.lbits, p.qbits);
+        return reinterpret_cast<const uint8_t*>(adjT + (size_t)v * p.adjT_stride);
+      };
+      auto advance = [&](uint32_t& rk, uint32_t& ch) {
+        ch += kBucketThreads;
+        while (ch >= cpr) {
+          ch -= cpr;
+          ++rk;
+        }
+      };
+      uint32_t rk_t = 0, ch_t = 0;  // walk state of this thread's next item
+      if (lo + tid < hi) {
+        rk_t = cpow2 ? (lo + tid) >> cbits : (lo + tid) / cpr;
+        ch_t = lo + tid - rk_t * cpr;
+      }
       uint32_t cur = 0xFFFFFFFFu;
       K run = KT::kNone;
-      for (uint32_t it0 = tid; it0 < total; it0 += kBucketThreads * 8) {
-        uint4 v4[8];
-        uint32_t bits[8], ci[8];
+      for (uint32_t it0 = lo + tid; it0 < hi; it0 += kBucketThreads * kPullDepth) {
+        uint4 v4[kPullDepth];
+        {
+          uint32_t rk = rk_t, ch = ch_t, rrow = rk_t;
+          const uint8_t* row = row_of(rk);
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const uint32_t item = it0 + m * kBucketThreads;
-          ci[m] = 0xFFFFFFFFu;
-          bits[m] = 0;
-          if (item < total) {
-            ci[m] = cpow2 ? item >> cbits : item / cpr;
-            const uint32_t chunk = item - ci[m] * cpr;
-            const uint32_t pos0 = chunk * CPT;
-            const uint32_t v = p.adjT_by_pos ? p0 + slist[ci[m]]
-                                             : pos_to_vid(p0 + slist[ci[m]], p.Q, p.lbits, p.qbits);
-            bits[m] = (sbm[pos0 >> 5] >> (pos0 & 31)) & ((1u << CPT) - 1u);
-            v4[m] = __ldg(reinterpret_cast<const uint4*>(
-                reinterpret_cast<const uint8_t*>(adjT + (size_t)v * p.adjT_stride) + chunk * 16));
+          for (int m = 0; m < kPullDepth; ++m) {
+            if (it0 + m * kBucketThreads < hi) {
+              if (rk != rrow) {
+                rrow = rk;
+                row = row_of(rk);
+              }
+              v4[m] = __ldg(reinterpret_cast<const uint4*>(row + ch * 16));
+            }
+            advance(rk, ch);
           }
         }
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          if (ci[m] == 0xFFFFFFFFu) break;
-          if (ci[m] != cur) {
+        for (int m = 0; m < kPullDepth; ++m) {
+          const uint32_t item = it0 + m * kBucketThreads;
+          if (item >= hi) break;
+          const uint32_t rk = rk_t, ch = ch_t;
+          advance(rk_t, ch_t);
+          const uint32_t ci = rk - r0;
+          if (ci != cur) {
             if (cur != 0xFFFFFFFFu && run != KT::kNone) smem_min(&sk[cur], run);
-            cur = ci[m];
+            cur = ci;
             run = KT::kNone;
           }
-          const uint32_t pos0 = ((it0 + m * kBucketThreads) - ci[m] * cpr) * CPT;
+          const uint32_t pos0 = ch * CPT;
+          const uint32_t bits = (sbm[pos0 >> 5] >> (pos0 & 31)) & ((1u << CPT) - 1u);
+          if (!bits) continue;
           // consecutive positions of one participant: vertex ids step by Q
           const uint32_t vid0 = gvid(pos0);
           const uint32_t wd[4] = {v4[m].x, v4[m].y, v4[m].z, v4[m].w};
 #pragma unroll
-          for (int c = 0; c < CPT; ++c) {
-            const uint32_t word = wd[(c * sizeof(W)) / 4];
-            const uint32_t w = sizeof(W) == 4 ? word : (word >> (((c * sizeof(W)) % 4) * 8)) & WINF;
-            const K kk = ((bits[m] >> c) & 1u) ? KT::make(w, vid0 + c * p.Q) : KT::kNone;
+          for (int cc = 0; cc < CPT; ++cc) {
+            const uint32_t word = wd[(cc * sizeof(W)) / 4];
+            const uint32_t w = sizeof(W) == 4 ? word : (word >> (((cc * sizeof(W)) % 4) * 8)) & WINF;
+            const K kk = ((bits >> cc) & 1u) ? KT::make(w, vid0 + cc * p.Q) : KT::kNone;
             run = kk < run ? kk : run;
           }
         }
       }
       if (cur != 0xFFFFFFFFu && run != KT::kNone) smem_min(&sk[cur], run);
       __syncthreads();
-      for (uint32_t i = tid; i < nu; i += kBucketThreads) {
-        const K k = sk[i];
-        const uint32_t col = slist[i];
+      for (uint32_t i = tid; i < ncols; i += kBucketThreads)
+        if (sk[i] != KT::kNone) smem_min(&pkey[scol[i]], sk[i]);
+      stamp();
+      barrier();  // every partial minimum is in pkey
+      stamp();
+      for (uint32_t col = tid; col < T; col += kBucketThreads) {
+        if ((ssettled[col >> 5] >> (col & 31)) & 1u) continue;
+        const K k = ld_cg(&pkey[p0 + col]);
         if (k != KT::kNone && KT::w(k) != WINF) {
           const uint32_t cand = dk + KT::w(k);
           if (cand < sdist[col]) {
@@ -496,7 +586,8 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
       __syncthreads();
     }
     // ---- publish the next class's candidates, one barrier per class
-    publish(nxt);
+    stamp();
+    publish((uint32_t)((bar_base + nbar) & 1ull));
     barrier();
     stamp();
   }
@@ -509,6 +600,7 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
       p.pred_out[v] = spred[i] == 0xFFFFFFFFu ? ~0ull : (uint64_t)spred[i];
     }
   }
+  stamp();
   if (blockIdx.x == 0 && tid == 0) {
     p.info[0] = settled;
     p.info[1] = step;
@@ -517,12 +609,11 @@ __global__ void __launch_bounds__(kBucketThreads) bucket_kernel(const BucketPara
     p.info2[0] = nbar;
     if (p.nshards > 1) *p.bar_epoch = bar_base + nbar;  // every CTA read it before barrier 1
   }
-  if (failed && tid == 0) p.info2[1] = 1;
 }
 
 __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t T, uint32_t G, uint32_t words,
                                                        uint32_t wbytes) {
-  return 4ull * (2ull * T + bucket_round4(T / 32) + bucket_round4(G) + bucket_round4(words) +
+  return 4ull * (2ull * T + bucket_round4(T / 32) + bucket_round4(G) + 2ull * bucket_round4(words) +
                  kBucketChunk) +
          (size_t)kBucketThreads * (16 / wbytes) * (wbytes == 1 ? 4 : 8);
 }

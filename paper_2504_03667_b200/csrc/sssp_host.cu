@@ -206,8 +206,10 @@ struct sssp_graph {
   bool bucket = false;  // distance-class engine available and selected (min weight >= 1)
   // bucket engine layout (identical on every shard)
   uint32_t bT = 0, bG = 0;               // positions per CTA, CTAs per shard
+  uint64_t bseq = 0;                     // bucket launch tags (watchdog reports)
   uint64_t slots_bytes = 0;              // scan-engine exchange region (start of d_slots)
-  uint64_t bar_off = 0, epoch_off = 0, ctrl_off = 0, bm_off = 0, region_bytes = 0;
+  uint64_t bar_off = 0, epoch_off = 0, ctrl_off = 0, bm_off = 0, ubm_off = 0, pkey_off = 0,
+           region_bytes = 0;
   uint64_t exch_base = 0;
   double transfer_in_s = 0;
   uint32_t pending = 0;  // solves of the last enqueued launch (0: nothing pending)
@@ -444,6 +446,7 @@ int alloc_state(sssp_graph* g, Shard& s) {
   CK(cudaMalloc(&s.d_slots, bytes));
   CK(cudaMemset(s.d_slots, 0, bytes));
   CK(cudaMalloc(&s.d_info2, B * 2 * sizeof(uint64_t)));
+  CK(cudaMemset(s.d_info2, 0, B * 2 * sizeof(uint64_t)));
   CK(cudaMalloc(&s.d_dist, B * std::max<uint64_t>(1, s.loc_n) * sizeof(uint64_t)));
   CK(cudaMalloc(&s.d_pred, B * std::max<uint64_t>(1, s.loc_n) * sizeof(uint64_t)));
   CK(cudaMalloc(&s.d_info, B * 4 * sizeof(uint64_t)));
@@ -587,28 +590,31 @@ int plan_bucket(sssp_graph* g) {
       if (!fits) break;
       CK(cudaSetDevice(s.device));
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      uint32_t same = 0;
+      for (const auto& t : g->sh) same += t.device == s.device ? 1 : 0;
       int per_sm = 0, sms = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBucketThreads, smem));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
-      uint32_t same = 0;
-      for (const auto& t : g->sh) same += t.device == s.device ? 1 : 0;
       fits = per_sm > 0 && (uint64_t)g->bG * same <= (uint64_t)per_sm * sms;
     }
     if (fits) break;
-    if (T * g->wbytes >= 4096 || T >= s0.row_stride) {
+    if (T * g->wbytes >= 2048 || T >= s0.row_stride) {  // pull keys: T + 2 <= 4096 / wbytes
       if (want == SSSP_ENGINE_BUCKET) return fail(SSSP_ERR_UNSUPPORTED, "bucket grid does not fit");
       return SSSP_OK;  // AUTO: stay on the scan engine
     }
     T *= 2;
   }
-  // exchange region: [barrier counter | epoch | ctrl [2][3][P*G] | bitmap [2][P*row_stride/32]]
+  // exchange region: [barrier counter | epoch | ctrl [2][3][P*G] | bitmap [2][P*row_stride/32]
+  //                   | local: unsettled bitmap [2][row_stride/32] | pull keys [row_stride] u64]
   const uint64_t GT = (uint64_t)g->bG * g->P;
   const uint64_t words = s0.row_stride / 32 * g->P;
   g->bar_off = 0;
   g->epoch_off = 128;
   g->ctrl_off = 256;
   g->bm_off = (g->ctrl_off + 2 * 3 * GT * 4 + 255) & ~255ull;
-  g->region_bytes = (g->bm_off + 2 * words * 4 + 255) & ~255ull;
+  g->ubm_off = (g->bm_off + 2 * words * 4 + 255) & ~255ull;
+  g->pkey_off = (g->ubm_off + 2 * (s0.row_stride / 32) * 4 + 255) & ~255ull;
+  g->region_bytes = (g->pkey_off + s0.row_stride * 8 + 255) & ~255ull;
   g->bucket = true;
   return SSSP_OK;
 }
@@ -794,7 +800,6 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
     for (auto& s : g->sh) {
       CK(cudaSetDevice(s.device));
       if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
-      CK(cudaMemsetAsync(s.d_info2, 0, (uint64_t)k * 2 * sizeof(uint64_t), s.stream));
     }
     for (uint32_t i = 0; i < k; ++i) {
       for (auto& s : g->sh) {
@@ -822,7 +827,10 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
           bp.peer_bitmap[j] = reinterpret_cast<uint32_t*>(base + g->bm_off);
           bp.peer_bar[j] = reinterpret_cast<unsigned long long*>(base + g->bar_off);
         }
-        bp.bar_epoch = reinterpret_cast<uint64_t*>(reinterpret_cast<char*>(s.d_slots) + g->slots_bytes + g->epoch_off);
+        char* own = reinterpret_cast<char*>(s.d_slots) + g->slots_bytes;
+        bp.bar_epoch = reinterpret_cast<uint64_t*>(own + g->epoch_off);
+        bp.ubm = reinterpret_cast<uint32_t*>(own + g->ubm_off);
+        bp.pkey = own + g->pkey_off;
         bp.timeout_ns = g->opt.timeout_ms * 1000000ull;
         bp.dist_out = s.d_dist + (uint64_t)i * s.loc_n;
         bp.pred_out = s.d_pred + (uint64_t)i * s.loc_n;
@@ -833,6 +841,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
           CK(cudaMemsetAsync(s.d_trace, 0, 64 * 8, s.stream));
           bp.trace = s.d_trace;
         }
+        bp.seq = g->bseq + 1 + i;
         void* args[] = {&bp};
         if (g->P == 1) {
           CK(cudaLaunchCooperativeKernel(fn, dim3(g->bG), dim3(kBucketThreads), args, smem, s.stream));
@@ -850,6 +859,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
       CK(cudaSetDevice(s.device));
       CK(cudaEventRecord(s.ev1, s.stream));
     }
+    g->bseq += k;
     g->pending = k;
     g->queued += 1;
     return SSSP_OK;
@@ -931,7 +941,9 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
       CK(cudaMemcpyAsync(i2, s.d_info2, std::min<uint64_t>(k, 64) * 2 * sizeof(uint64_t),
                          cudaMemcpyDeviceToHost, s.stream));
       CK(cudaStreamSynchronize(s.stream));
-      for (uint32_t i = 0; i < std::min<uint32_t>(k, 64); ++i) timeout |= i2[2 * i + 1] != 0;
+      // launch i of the last enqueue carried tag bseq - k + 1 + i
+      for (uint32_t i = 0; i < std::min<uint32_t>(k, 64); ++i)
+        timeout |= i2[2 * i + 1] == g->bseq - k + 1 + i;
     }
     CK(cudaStreamSynchronize(s.stream));
     float ms = 0;
@@ -984,6 +996,11 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     st->shards = g->P;
     st->packed_key = g->packed;
   }
+  if (timeout && g->bucket && g->P > 1 && !g->multiproc)  // barrier counters out of step: restart
+    for (auto& s : g->sh) {
+      CK(cudaSetDevice(s.device));
+      CK(cudaMemset(reinterpret_cast<char*>(s.d_slots) + g->slots_bytes, 0, g->ctrl_off));
+    }
   if (timeout) return fail(SSSP_ERR_TIMEOUT, "exchange watchdog fired (a peer never published)");
   return SSSP_OK;
 }

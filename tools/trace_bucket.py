@@ -1,5 +1,7 @@
-import os, sys, time
-sys.path.insert(0, '.')
+"""Per-phase %globaltimer trace of the bucket kernel (CTA 0), for profiling:
+SSSP_BUCKET_TRACE=1 python tools/trace_bucket.py"""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import paper_2504_03667_b200 as P
 g = P.generate_dense(32768, 32768)
 dg = P.DeviceGraph(g, engine="bucket")
