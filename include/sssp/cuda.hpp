@@ -9,10 +9,12 @@
 //   dijkstra_serial(g, s)            serial.hpp:65   sssp::cuda::dijkstra(g, s)
 //   dijkstra_serial(g, s, c, &vo)    serial.hpp:26   sssp::cuda::dijkstra(g, s, &vo)
 //   dijkstra_partitioned(g, s, p)    partitioned:184 sssp::cuda::dijkstra_partitioned(g, s, devices)
+//   dijkstra_dataparallel(g, s)      dataparallel:302 sssp::cuda::dijkstra_dataparallel(g, s)
 //   (repeated solves on one graph)                   sssp::cuda::DeviceGraph
 //
 // Results are bit-identical to dijkstra_serial (dist AND pred), so
-// `sssp::cuda::dijkstra(g, s) == sssp::dijkstra_serial(g, s)` holds.
+// `sssp::cuda::dijkstra(g, s) == sssp::dijkstra_serial(g, s)` holds; the
+// data-parallel drop-in equals dijkstra_dataparallel (result and rounds).
 // source >= n throws std::invalid_argument (serial.hpp:30); every other
 // failure throws std::runtime_error -- there is no CPU fallback.
 #pragma once
@@ -127,6 +129,25 @@ class DeviceGraph {
     return out;
   }
 
+  // The paper's data-parallel engine (dataparallel.hpp:302-327): result and
+  // round count equal dijkstra_dataparallel's.
+  CudaRun run_dataparallel(VertexId source, std::size_t* rounds = nullptr) {
+    if (source >= n_) throw std::invalid_argument("dijkstra_dataparallel: source out of range");
+    CudaRun r;
+    r.result.source = source;
+    r.result.dist.resize(n_);
+    r.result.pred.resize(n_);
+    std::uint64_t nr = 0;
+    check(sssp_solve_dataparallel(h_, source, r.result.dist.data(),
+                                  reinterpret_cast<std::uint64_t*>(r.result.pred.data()), &nr,
+                                  &r.stats),
+          "sssp_solve_dataparallel");
+    r.phases = {r.stats.transfer_in_s, r.stats.rounds_s, r.stats.transfer_out_s};
+    r.iterations = nr;
+    if (rounds) *rounds = nr;
+    return r;
+  }
+
   sssp_graph* handle() const { return h_; }
 
  private:
@@ -160,6 +181,28 @@ inline ShortestPathResult dijkstra_partitioned(const Graph& g, VertexId source,
   if (source >= g.n) throw std::invalid_argument("dijkstra_partitioned: source out of range");
   DeviceGraph dg(g, std::move(devices));
   return dg.solve(source);
+}
+
+// Mirrors DataParallelRun (dataparallel.hpp:284-296): result, rounds, phases.
+struct DataParallelRun {
+  ShortestPathResult result;
+  std::size_t rounds = 0;
+  Phases phases;
+  std::size_t cells_in = 0;   // n*n, as transfer_in reports (:269-276)
+  std::size_t cells_out = 0;  // 2n (:279-282)
+};
+
+// Drop-in for dijkstra_dataparallel(g, source) (dataparallel.hpp:302-327).
+inline DataParallelRun dijkstra_dataparallel(const Graph& g, VertexId source) {
+  if (source >= g.n) throw std::invalid_argument("dijkstra_dataparallel: source out of range");
+  DeviceGraph dg(g);
+  DataParallelRun out;
+  CudaRun r = dg.run_dataparallel(source, &out.rounds);
+  out.result = std::move(r.result);
+  out.phases = r.phases;
+  out.cells_in = g.n * g.n;
+  out.cells_out = 2 * g.n;
+  return out;
 }
 
 }  // namespace sssp::cuda

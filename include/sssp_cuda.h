@@ -57,7 +57,8 @@ typedef enum {
   SSSP_ENGINE_AUTO = 0,
   SSSP_ENGINE_GRID = 1,    /* single-warp CTAs across the GPU, exchange through L2 */
   SSSP_ENGINE_CLUSTER = 2, /* one thread-block cluster per solve, exchange through DSMEM */
-  SSSP_ENGINE_BUCKET = 3   /* distance-class steps, push/pull over B200 HBM */
+  SSSP_ENGINE_BUCKET = 3,  /* distance-class steps, push/pull over B200 HBM */
+  SSSP_ENGINE_DATAPARALLEL = 4 /* reported by sssp_solve_dataparallel only */
 } sssp_engine;
 
 typedef struct {
@@ -172,6 +173,18 @@ void* sssp_stream(sssp_graph* g, int local);
  * reference harness refuses to time invalid results (bench.hpp:167-173). */
 int sssp_validate(sssp_graph* g, uint64_t source, const uint64_t* dist, const uint64_t* pred,
                   uint64_t* violations);
+
+/* The paper's data-parallel engine: dijkstra_dataparallel(g, s)
+ * (dataparallel.hpp:302-327; Alg. 3-4) -- synchronous relaxation
+ * rounds to the fixpoint, then reconstruct_predecessors (:221-264).  dist
+ * equals dijkstra_serial's; pred follows the reference's reconstruction (it
+ * differs from serial's on tie-heavy graphs, exactly as the reference's
+ * does); *rounds_out = DataParallelRun::rounds (relax rounds executed,
+ * including the final one that changes nothing).  Bad source:
+ * SSSP_ERR_BAD_SOURCE (std::invalid_argument at :305).  One shard only.
+ * stats.classes = pass-number sweeps needed by zero-weight ties (0: none). */
+int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out,
+                            uint64_t* pred_out, uint64_t* rounds_out, sssp_solve_stats* st);
 
 /* t_sync_min microbenchmark (the roofline's sync term): runs
  * `rounds` exchange rounds with the solve's launch shape and exchange code

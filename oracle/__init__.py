@@ -58,6 +58,7 @@ class _Oracle:
             "o_pad_vertex_count": (U64, [U64, U64]),
             "o_all_pairs": (ctypes.c_int, [_u64p, U64, _u64p]),
             "o_validate": (U64, [_u64p, U64, U64, _u64p, _u64p]),
+            "o_dijkstra_dataparallel": (ctypes.c_int, [_u64p, U64, U64, _u64p, _u64p, _u64p]),
         })
 
     # --- rng (for reproducing the reference tests' graph sweeps)
@@ -123,6 +124,17 @@ class _Oracle:
     def pad_vertex_count(self, n, p):
         return int(self.lib.o_pad_vertex_count(n, p))
 
+    def dataparallel(self, adj, n, source):
+        """dijkstra_dataparallel (dataparallel.hpp:302-327) -> (dist, pred, rounds)."""
+        adj = np.ascontiguousarray(adj, np.uint64)
+        dist = np.empty(n, np.uint64)
+        pred = np.empty(n, np.uint64)
+        r = np.zeros(1, np.uint64)
+        rc = self.lib.o_dijkstra_dataparallel(_p(adj), n, source, _p(dist), _p(pred), _p(r))
+        if rc == 1:
+            raise ValueError("dijkstra_dataparallel: source out of range")
+        return dist, pred, int(r[0])
+
     def all_pairs(self, adj, n):
         d = np.empty(n * n, np.uint64)
         self.lib.o_all_pairs(_p(np.ascontiguousarray(adj, np.uint64)), n, _p(d))
@@ -158,6 +170,8 @@ class _Ref:
             "ref_graph_serial": (ctypes.c_int, [ctypes.c_void_p, U64, _u64p, _u64p]),
             "ref_graph_partitioned": (ctypes.c_int, [ctypes.c_void_p, U64, U64, _u64p, _u64p,
                                                      ctypes.POINTER(ctypes.c_double)]),
+            "ref_dijkstra_dataparallel": (ctypes.c_int, [_u64p, U64, U64, ctypes.c_int, _u64p,
+                                                         _u64p, _u64p]),
         })
 
     def dense(self, n, seed, directed=False):
@@ -232,6 +246,21 @@ class _Ref:
         if rc:
             raise ValueError(self.lib.ref_last_error().decode())
         return dist, pred, dt
+
+    def dataparallel(self, adj, n, source, schedule=0):
+        """The reference's dijkstra_dataparallel -> (dist, pred, rounds);
+        schedule 0 threaded, 1 sequential, 2 shuffled."""
+        adj = np.ascontiguousarray(adj, np.uint64)
+        dist = np.empty(n, np.uint64)
+        pred = np.empty(n, np.uint64)
+        r = np.zeros(1, np.uint64)
+        rc = self.lib.ref_dijkstra_dataparallel(_p(adj), n, source, schedule, _p(dist), _p(pred),
+                                                _p(r))
+        if rc == 1:
+            raise ValueError("dijkstra_dataparallel: source out of range")
+        if rc:
+            raise RuntimeError(self.lib.ref_last_error().decode())
+        return dist, pred, int(r[0])
 
     def partitioned(self, adj, n, source, p, threaded=True):
         adj = np.ascontiguousarray(adj, np.uint64)

@@ -163,6 +163,31 @@ int ref_dijkstra_partitioned(const std::uint64_t* adj, std::uint64_t n, std::uin
   }
 }
 
+// dataparallel.hpp:302-327 with the given lane schedule (0 threaded,
+// 1 sequential, 2 shuffled with seed 7); *rounds = DataParallelRun::rounds.
+int ref_dijkstra_dataparallel(const std::uint64_t* adj, std::uint64_t n, std::uint64_t source,
+                              int schedule, std::uint64_t* dist, std::uint64_t* pred,
+                              std::uint64_t* rounds) {
+  try {
+    const sssp::Graph g = make_graph(adj, n, 1);
+    sssp::LaneConfig cfg;
+    cfg.schedule = schedule == 1   ? sssp::LaneSchedule::sequential
+                   : schedule == 2 ? sssp::LaneSchedule::shuffled
+                                   : sssp::LaneSchedule::threaded;
+    cfg.shuffle_seed = 7;
+    const sssp::DataParallelRun run = sssp::dijkstra_dataparallel(g, source, cfg);
+    copy_out(run.result, dist, pred);
+    if (rounds) *rounds = run.rounds;
+    return RS_OK;
+  } catch (const std::invalid_argument& e) {
+    g_last_error = e.what();
+    return RS_BAD_SOURCE;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return RS_ERR;
+  }
+}
+
 // bench.hpp:114-180 (detail::timed_run): min-of-reps, validated.  engine:
 // 0 serial, 1 partitioned.  Returns the scoped total seconds in *total_s
 // and the result of the best repetition.  The Graph is built once from adj

@@ -8,7 +8,7 @@
  *
  * Parity is pinned two ways (see tests/test_oracle.py):
  *   - against the known-answer tests of the reference's own unit suite
- *     (proj/tests/test_serial.cpp:11-38, test_dataparallel.cpp:144-154,
+ *     (proj/tests/test_serial.cpp:11-38, test_dataparallel.cpp:60-80, 144-154,
  *     test_partitioned.cpp:194-246), and
  *   - against oracle/_ref/libref_sssp.so, the reference headers compiled
  *     unmodified from /root/reference/proj/include (oracle/Makefile), on
@@ -382,4 +382,88 @@ uint64_t o_validate(const uint64_t* adj, uint64_t n, uint64_t source, const uint
     if (cur != source) ++bad;
   }
   return bad;
+}
+
+/* dataparallel.hpp:302-327 (dijkstra_dataparallel) with the sequential lane
+ * schedule (:207-210), which the reference proves produces the same result as
+ * the threaded one: relax_round (:184-217) until a round lowers nothing,
+ * then reconstruct_predecessors (:221-264).  *rounds = rounds_executed. */
+static const uint64_t* o_dp_dist;
+static int o_dp_cmp(const void* a, const void* b) { /* (dist, id) ascending, :233-237 */
+  const uint64_t x = *(const uint64_t*)a, y = *(const uint64_t*)b;
+  const uint64_t dx = o_dp_dist[x], dy = o_dp_dist[y];
+  if (dx != dy) return dx < dy ? -1 : 1;
+  return x < y ? -1 : (x > y ? 1 : 0);
+}
+int o_dijkstra_dataparallel(const uint64_t* adj, uint64_t n, uint64_t source, uint64_t* dist,
+                            uint64_t* pred, uint64_t* rounds) {
+  if (source >= n) return O_BAD_SOURCE; /* :305-306 */
+  uint64_t* snap = (uint64_t*)malloc((n ? n : 1) * 8);
+  uint64_t* order = (uint64_t*)malloc((n ? n : 1) * 8);
+  char* attached = (char*)calloc(n ? n : 1, 1);
+  if (!snap || !order || !attached) {
+    free(snap);
+    free(order);
+    free(attached);
+    return O_OOM;
+  }
+  for (uint64_t v = 0; v < n; ++v) { /* RelaxState, :44-52 */
+    dist[v] = v == source ? 0 : O_INF;
+    pred[v] = O_NOV;
+  }
+  uint64_t r = 0;
+  int any;
+  do { /* relax_round, :184-217; relax_cell, :67-79 */
+    any = 0;
+    memcpy(snap, dist, n * 8);
+    for (uint64_t u = 0; u < n; ++u) {
+      const uint64_t su = snap[u];
+      if (su == O_INF) continue;
+      for (uint64_t v = 0; v < n; ++v) {
+        const uint64_t w = adj[u * n + v];
+        if (w == O_INF) continue;
+        if (su + w < dist[v]) {
+          dist[v] = su + w;
+          pred[v] = u;
+          any = 1;
+        }
+      }
+    }
+    ++r;
+  } while (any);
+  /* reconstruct_predecessors, :221-264 */
+  uint64_t m = 0;
+  for (uint64_t v = 0; v < n; ++v) {
+    pred[v] = O_NOV;
+    if (v != source && dist[v] != O_INF) order[m++] = v;
+  }
+  o_dp_dist = dist;
+  qsort(order, m, 8, o_dp_cmp);
+  attached[source] = 1;
+  int progress = 1;
+  while (progress) {
+    progress = 0;
+    for (uint64_t i = 0; i < m; ++i) {
+      const uint64_t v = order[i];
+      if (attached[v]) continue;
+      const uint64_t dv = dist[v];
+      for (uint64_t u = 0; u < n; ++u) {
+        if (u == v || !attached[u]) continue;
+        const uint64_t w = adj[u * n + v];
+        if (w == O_INF) continue;
+        const uint64_t du = dist[u];
+        if (du != O_INF && du + w == dv) {
+          pred[v] = u;
+          attached[v] = 1;
+          progress = 1;
+          break;
+        }
+      }
+    }
+  }
+  if (rounds) *rounds = r;
+  free(snap);
+  free(order);
+  free(attached);
+  return O_OK;
 }

@@ -44,6 +44,7 @@ __all__ = [
     "INF", "NO_VERTEX", "MAX_WEIGHT", "Graph", "ShortestPathResult", "ParseError", "SsspError",
     "graph_from_edges", "parse_edge_list", "generate_dense", "generate_sparse",
     "generate_bernoulli", "DeviceGraph", "ShardGraph", "dijkstra", "dijkstra_partitioned",
+    "dijkstra_dataparallel",
     "pad_vertex_count", "Options", "Stats",
 ]
 
@@ -326,6 +327,22 @@ class DeviceGraph:
         check(lib.sssp_finish(self._h, ctypes.byref(st)), "sssp_finish")
         return st.as_dict()
 
+    def solve_dataparallel(self, source: int) -> "ShortestPathResult":
+        """The paper's data-parallel engine, dijkstra_dataparallel(g, s)
+        (dataparallel.hpp:302-327): stats["rounds"] = DataParallelRun::rounds."""
+        if source < 0:
+            raise ValueError("dijkstra_dataparallel: source out of range")
+        dist = np.empty(self.n, dtype=np.uint64)
+        pred = np.empty(self.n, dtype=np.uint64)
+        rounds = ctypes.c_uint64()
+        st = Stats()
+        check(lib.sssp_solve_dataparallel(self._h, source, _p64(dist), _p64(pred),
+                                          ctypes.byref(rounds), ctypes.byref(st)),
+              "sssp_solve_dataparallel")
+        r = ShortestPathResult(source, dist, pred, st.as_dict())
+        r.stats["rounds"] = rounds.value
+        return r
+
     def validate(self, r: "ShortestPathResult") -> int:
         """validate_result (oracle.hpp:51-120) on the device; 0 = valid."""
         out = ctypes.c_uint64()
@@ -398,6 +415,15 @@ def dijkstra(g: Graph, source: int, device: int = 0) -> ShortestPathResult:
         raise ValueError("dijkstra: source out of range")
     with DeviceGraph(g, (device,)) as dg:
         return dg.solve(source)
+
+
+def dijkstra_dataparallel(g: Graph, source: int, device: int = 0) -> ShortestPathResult:
+    """Drop-in for ``dijkstra_dataparallel(g, source)`` (dataparallel.hpp:302-327):
+    same dist, the reference's reconstructed pred, stats["rounds"] = run.rounds."""
+    if not 0 <= source < g.n:
+        raise ValueError("dijkstra_dataparallel: source out of range")
+    with DeviceGraph(g, (device,)) as dg:
+        return dg.solve_dataparallel(source)
 
 
 def dijkstra_partitioned(g: Graph, source: int, p: int,

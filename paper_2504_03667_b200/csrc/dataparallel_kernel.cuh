@@ -1,0 +1,357 @@
+// dataparallel_kernel.cuh -- the paper's data-parallel engine (PAPER.md
+// Alg. 3-4), restated for B200: synchronous relaxation rounds to a fixpoint,
+// then the deterministic predecessor rebuild.  Bit-identical to the
+// reference's dijkstra_dataparallel (dataparallel.hpp:302-327): same dist,
+// same pred (reconstruct_predecessors, :221-264), same round count.
+//
+// Rounds (relax_round, dataparallel.hpp:184-217).  Every round relaxes every
+// edge against the round-start snapshot; the reference's atomic minimum makes
+// the round's outcome schedule-independent:
+//   dist_{r+1}[v] = min(dist_r[v], min_u snapshot_r[u] + w(u,v)).
+// A row u whose snapshot did not change since the previous round cannot lower
+// anything (its candidates were applied then), so only the FRONTIER -- the
+// vertices lowered in the previous round, {source} in round 1 -- is pushed.
+// That gives the same dist after every round and the same round count
+// (rounds_executed counts the final round that changes nothing).  One
+// cooperative launch runs all rounds: a CTA owns T matrix positions (dist in
+// shared memory), pushes its slice of every frontier row, and publishes its
+// lowered columns (bitmap + snapshot values) before one grid barrier per
+// round.
+//
+// Predecessors (reconstruct_predecessors).  Vertices are attached in
+// ascending (dist, id) order, each to its smallest already-attached tight
+// parent, in passes until nothing changes.  Writing pass(v) for the pass in
+// which v attaches, with the source attached before pass 1, v attaches in the
+// first pass p in which some tight parent u (u != v, du + w(u,v) == dv) is
+// attached when v is visited:  u == source, or pass(u) < p, or pass(u) == p
+// and u precedes v in the order.  Hence
+//   pass(v) = min over tight u of f(u),  f(source) = 1,
+//             f(u) = pass(u) + [(du, u) > (dv, v)]  otherwise,
+//   pred(v) = the smallest tight u with f(u) <= pass(v).
+// A tight edge with w >= 1 always runs forward in the order, so without a
+// zero-weight tight edge every pass is 1 and pred(v) is simply the smallest
+// tight parent: one pass over the matrix (dp_pred_kernel).  Only when that
+// pass finds a zero-weight tight edge between distinct vertices are the pass
+// numbers solved -- a min-plus fixpoint over the tight edges, iterated to
+// convergence by dp_pass_kernel -- and the predecessors recomputed with them.
+#pragma once
+
+#include <cooperative_groups.h>
+
+#include <cstdint>
+
+#include "bucket_kernel.cuh"
+
+namespace sssp_b200 {
+
+struct DpParams {
+  const void* adj;      // [n rows][row_stride] positions (the permuted matrix)
+  uint64_t row_stride;  // positions per row (= Q*L)
+  uint32_t n, Q, qbits, lbits, T, source;
+  uint32_t* gfront;     // [2][row_stride/32] frontier bitmap by position, per round parity
+  uint32_t* gcnt;       // [2][G] frontier vertices per tile
+  uint32_t* gsnap;      // [2][row_stride] snapshot dist of frontier positions
+  uint32_t* dist_v;     // [n] final dist by vertex id (u32, all-ones = INF)
+  uint32_t* pass_v;     // [n] pass numbers (dp_pass_kernel); nullptr: every pass is 1
+  uint32_t* sweep_chg;  // [max_sweeps] CTAs that changed a pass number in sweep i (zeroed)
+  uint32_t max_sweeps;
+  uint32_t* flag;       // [1] dp_pred_kernel: 1 if a zero-weight tight edge u != v exists
+  uint64_t* dist_out;   // [n] reference encoding
+  uint64_t* pred_out;   // [n]
+  uint64_t* info;       // [4]: rounds, frontier rows pushed, sweeps, -
+};
+
+constexpr uint32_t kDpInf = 0xFFFFFFFFu;
+
+// Dynamic smem of dp_relax_kernel: dist[T] | lowered[T/32] | frontier bitmap
+// [row_stride/32] | ids [kBucketChunk] | combine [kBucketThreads*CPT] u32.
+__host__ __device__ constexpr size_t dp_relax_smem_bytes(uint32_t T, uint32_t words, uint32_t wbytes) {
+  return 4ull * (T + bucket_round4(T / 32) + bucket_round4(words) + kBucketChunk) +
+         4ull * kBucketThreads * (16 / wbytes);
+}
+
+template <typename W>
+__global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpParams p) {
+  namespace cg = cooperative_groups;
+  constexpr uint32_t WINF = WInf<W>::v;
+  constexpr int CPT = 16 / (int)sizeof(W);
+  extern __shared__ __align__(16) uint32_t smem[];
+  const uint32_t T = p.T, G = gridDim.x, TW = T / 32;
+  const uint32_t words = (uint32_t)(p.row_stride / 32);
+  uint32_t* sdist = smem;
+  uint32_t* slow = sdist + T;  // columns lowered this round
+  uint32_t* sbm = slow + bucket_round4(TW);
+  uint32_t* schunk = sbm + bucket_round4(words);
+  uint32_t* scomb = schunk + kBucketChunk;
+  __shared__ uint32_t s_red[kBucketThreads / 32];
+  const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const uint32_t p0 = blockIdx.x * T;
+  const W* adj = static_cast<const W*>(p.adj);
+  const uint32_t TPR = T * sizeof(W) / 16, RG = kBucketThreads / TPR;
+  auto vid = [&](uint32_t pos) { return pos_to_vid(pos, p.Q, p.lbits, p.qbits); };
+
+  // ---- init (RelaxState, dataparallel.hpp:44-52): dist = INF, dist[s] = 0;
+  // round 1's frontier is {source} with snapshot 0.
+  for (uint32_t i = tid; i < T; i += kBucketThreads) sdist[i] = vid(p0 + i) == p.source ? 0u : kDpInf;
+  __shared__ uint32_t s_src;
+  if (tid == 0) s_src = 0;
+  __syncthreads();
+  for (uint32_t i = warp; i < TW; i += kBucketThreads / 32) {
+    const uint32_t pos = p0 + i * 32 + lane;
+    const uint32_t b = __ballot_sync(0xFFFFFFFFu, vid(pos) == p.source);
+    if (lane == 0) p.gfront[i + blockIdx.x * TW] = b;
+    if (b && lane == __ffs(b) - 1) {
+      p.gsnap[pos] = 0;
+      s_src = 1;
+    }
+  }
+  __syncthreads();
+  if (tid == 0) p.gcnt[blockIdx.x] = s_src;
+  cg::this_grid().sync();
+
+  uint64_t rounds = 0, pushed = 0;
+  uint32_t par = 0;
+  while (true) {
+    // frontier of this round (published before the last barrier)
+    const uint32_t* fb = p.gfront + par * words;
+    for (uint32_t i = tid; i < words; i += kBucketThreads) sbm[i] = __ldcg(&fb[i]);
+    uint32_t f = 0;
+    for (uint32_t c = tid; c < G; c += kBucketThreads) f += __ldcg(&p.gcnt[par * G + c]);
+    f = __reduce_add_sync(0xFFFFFFFFu, f);
+    if (lane == 0) s_red[warp] = f;
+    for (uint32_t i = tid; i < TW; i += kBucketThreads) slow[i] = 0u;
+    __syncthreads();
+    f = 0;
+    for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) f += s_red[w2];
+    if (f == 0) break;  // the previous round lowered nothing: fixpoint (uniform)
+    ++rounds;
+    pushed += f;
+    // ---- push the frontier rows: per column min of snapshot[u] + w(u, v)
+    const uint32_t rg = tid / TPR, ct = tid - rg * TPR;
+    uint32_t best[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) best[j] = kDpInf;
+    constexpr uint32_t WPT = 2;
+    for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads * WPT) {
+      const uint32_t w0 = wbase + tid * WPT;
+      uint32_t bw[WPT];
+      uint32_t c = 0;
+#pragma unroll
+      for (uint32_t k2 = 0; k2 < WPT; ++k2) {
+        bw[k2] = w0 + k2 < words ? sbm[w0 + k2] : 0u;
+        c += __popc(bw[k2]);
+      }
+      if (!__syncthreads_or(c != 0)) continue;
+      uint32_t incl = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+        if (lane >= (uint32_t)o) incl += t;
+      }
+      if (lane == 31) s_red[warp] = incl;
+      __syncthreads();
+      uint32_t wofs = 0, tot = 0;
+      for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) {
+        if (w2 < warp) wofs += s_red[w2];
+        tot += s_red[w2];
+      }
+      uint32_t o = wofs + incl - c;
+#pragma unroll
+      for (uint32_t k2 = 0; k2 < WPT; ++k2)
+        for (uint32_t m = bw[k2]; m; m &= m - 1) schunk[o++] = (w0 + k2) * 32 + (__ffs(m) - 1);
+      __syncthreads();
+      const uint32_t* snap = p.gsnap + par * p.row_stride;
+      for (uint32_t r0 = rg; r0 < tot; r0 += 8 * RG) {
+        uint32_t du[8];
+        uint4 vb[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          const uint32_t r = r0 + m * RG;
+          du[m] = kDpInf;
+          if (r < tot) {
+            const uint32_t pos = schunk[r];
+            du[m] = __ldcg(&snap[pos]);
+            vb[m] = __ldg(reinterpret_cast<const uint4*>(
+                reinterpret_cast<const uint8_t*>(adj + (size_t)vid(pos) * p.row_stride + p0) + ct * 16));
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          if (r0 + m * RG >= tot) break;
+          const uint32_t wd[4] = {vb[m].x, vb[m].y, vb[m].z, vb[m].w};
+#pragma unroll
+          for (int j = 0; j < CPT; ++j) {
+            const uint32_t word = wd[(j * sizeof(W)) / 4];
+            const uint32_t w = sizeof(W) == 4 ? word : (word >> (((j * sizeof(W)) % 4) * 8)) & WINF;
+            // du + w < 2^32 - 1 for finite operands (host-checked n * max_w)
+            const uint32_t cand = w == WINF ? kDpInf : du[m] + w;
+            best[j] = min(best[j], cand);
+          }
+        }
+      }
+      __syncthreads();
+    }
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) scomb[tid * CPT + j] = best[j];
+    __syncthreads();
+    // ---- apply (strict '<', relax_cell :74) and publish the lowered columns
+    const uint32_t nxt = par ^ 1u;
+    for (uint32_t col = tid; col < T; col += kBucketThreads) {
+      const uint32_t cth = col / CPT, j = col % CPT;
+      uint32_t k = kDpInf;
+      for (uint32_t g2 = 0; g2 < RG; ++g2) k = min(k, scomb[(g2 * TPR + cth) * CPT + j]);
+      if (k < sdist[col]) {
+        sdist[col] = k;
+        atomicOr(&slow[col >> 5], 1u << (col & 31));
+        p.gsnap[nxt * p.row_stride + p0 + col] = k;
+      }
+    }
+    __syncthreads();
+    uint32_t cnt = 0;
+    for (uint32_t i = tid; i < TW; i += kBucketThreads) {
+      p.gfront[nxt * words + blockIdx.x * TW + i] = slow[i];
+      cnt += __popc(slow[i]);
+    }
+    cnt = __reduce_add_sync(0xFFFFFFFFu, cnt);
+    if (lane == 0) s_red[warp] = cnt;
+    __syncthreads();
+    if (tid == 0) {
+      uint32_t c = 0;
+      for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) c += s_red[w2];
+      p.gcnt[nxt * G + blockIdx.x] = c;
+    }
+    cg::this_grid().sync();
+    par = nxt;
+  }
+  for (uint32_t i = tid; i < T; i += kBucketThreads) {
+    const uint32_t v = vid(p0 + i);
+    if (v < p.n) {
+      p.dist_v[v] = sdist[i];
+      p.dist_out[v] = sdist[i] == kDpInf ? ~0ull : (uint64_t)sdist[i];
+    }
+  }
+  if (blockIdx.x == 0 && tid == 0) {
+    p.info[0] = rounds;
+    p.info[1] = pushed;
+  }
+}
+
+// Dynamic smem of dp_pred_kernel / dp_pass_kernel: dv[T] | passv[T] | combine.
+__host__ __device__ constexpr size_t dp_pred_smem_bytes(uint32_t T, uint32_t wbytes) {
+  return 4ull * 2 * T + 4ull * kBucketThreads * (16 / wbytes);
+}
+
+// One pass over every row: pred(v) = the smallest tight u != v with
+// f(u) <= pass(v) (pass_v == nullptr: every pass is 1, so every tight parent
+// qualifies); flags a zero-weight tight edge between distinct vertices.
+// SWEEP = true instead iterates pass(v) = min over tight u of f(u) to its
+// fixpoint (cooperative launch; one grid barrier per sweep).
+template <typename W, bool SWEEP>
+__global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpParams p) {
+  namespace cg = cooperative_groups;
+  constexpr uint32_t WINF = WInf<W>::v;
+  constexpr int CPT = 16 / (int)sizeof(W);
+  extern __shared__ __align__(16) uint32_t smem[];
+  const uint32_t T = p.T;
+  uint32_t* sdv = smem;
+  uint32_t* spv = sdv + T;
+  uint32_t* scomb = spv + T;
+  const uint32_t tid = threadIdx.x;
+  const uint32_t p0 = blockIdx.x * T;
+  const W* adj = static_cast<const W*>(p.adj);
+  const uint32_t TPR = T * sizeof(W) / 16, RG = kBucketThreads / TPR;
+  const uint32_t rg = tid / TPR, ct = tid - rg * TPR;
+  auto vid = [&](uint32_t pos) { return pos_to_vid(pos, p.Q, p.lbits, p.qbits); };
+  for (uint32_t i = tid; i < T; i += kBucketThreads) {
+    const uint32_t v = vid(p0 + i);
+    sdv[i] = v < p.n ? p.dist_v[v] : kDpInf;
+    spv[i] = v < p.n && p.pass_v ? p.pass_v[v] : 1u;
+  }
+  __syncthreads();
+  // my CPT columns: vertex ids and (dist, pass)
+  uint32_t cv[CPT], cd[CPT], cp[CPT];
+#pragma unroll
+  for (int j = 0; j < CPT; ++j) {
+    const uint32_t col = ct * CPT + j;
+    cv[j] = vid(p0 + col);
+    cd[j] = sdv[col];
+    cp[j] = spv[col];
+  }
+  bool zero_tight = false;
+  for (uint32_t sweep = 0;; ++sweep) {
+    uint32_t best[CPT];
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) best[j] = kDpInf;
+    for (uint32_t u0 = rg; u0 < p.n; u0 += 8 * RG) {
+      uint32_t du[8], pu[8];
+      uint4 vb[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const uint32_t u = u0 + m * RG;
+        du[m] = u < p.n ? __ldcg(&p.dist_v[u]) : kDpInf;
+        pu[m] = (u < p.n && p.pass_v) ? __ldcg(&p.pass_v[u]) : 1u;
+        if (du[m] != kDpInf)
+          vb[m] = __ldg(reinterpret_cast<const uint4*>(
+              reinterpret_cast<const uint8_t*>(adj + (size_t)u * p.row_stride + p0) + ct * 16));
+      }
+#pragma unroll
+      for (int m = 0; m < 8; ++m) {
+        const uint32_t u = u0 + m * RG;
+        if (du[m] == kDpInf || pu[m] == kDpInf) continue;  // unreachable, or not attached yet
+        const uint32_t wd[4] = {vb[m].x, vb[m].y, vb[m].z, vb[m].w};
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) {
+          const uint32_t word = wd[(j * sizeof(W)) / 4];
+          const uint32_t w = sizeof(W) == 4 ? word : (word >> (((j * sizeof(W)) % 4) * 8)) & WINF;
+          if (w == WINF || u == cv[j] || cd[j] == kDpInf || du[m] + w != cd[j]) continue;
+          // f(u): the pass in which v may attach to u (source: pass 1)
+          const uint32_t after = (du[m] > cd[j] || (du[m] == cd[j] && u > cv[j])) ? 1u : 0u;
+          const uint32_t f = u == p.source ? 1u : pu[m] + after;
+          if (!SWEEP) {
+            zero_tight |= w == 0;
+            if (f <= cp[j]) best[j] = min(best[j], u);  // smallest qualifying parent
+          } else {
+            best[j] = min(best[j], f);
+          }
+        }
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) scomb[tid * CPT + j] = best[j];
+    __syncthreads();
+    if (!SWEEP) {
+      for (uint32_t col = tid; col < T; col += kBucketThreads) {
+        const uint32_t cth = col / CPT, j = col % CPT;
+        uint32_t k = kDpInf;
+        for (uint32_t g2 = 0; g2 < RG; ++g2) k = min(k, scomb[(g2 * TPR + cth) * CPT + j]);
+        const uint32_t v = vid(p0 + col);
+        if (v < p.n) p.pred_out[v] = (k == kDpInf || v == p.source) ? ~0ull : (uint64_t)k;
+      }
+      if (__syncthreads_or(zero_tight) && tid == 0) atomicOr(p.flag, 1u);
+      return;
+    }
+    // SWEEP: lower pass(v); count the CTAs that changed anything this sweep
+    bool changed = false;
+    for (uint32_t col = tid; col < T; col += kBucketThreads) {
+      const uint32_t cth = col / CPT, j = col % CPT;
+      uint32_t k = kDpInf;
+      for (uint32_t g2 = 0; g2 < RG; ++g2) k = min(k, scomb[(g2 * TPR + cth) * CPT + j]);
+      const uint32_t v = vid(p0 + col);
+      if (v < p.n && v != p.source && k < spv[col]) {
+        spv[col] = k;
+        p.pass_v[v] = k;  // read by other CTAs this or next sweep (monotone: any order converges)
+        changed = true;
+      }
+    }
+    if (__syncthreads_or(changed) && tid == 0) atomicAdd(&p.sweep_chg[sweep], 1u);
+#pragma unroll
+    for (int j = 0; j < CPT; ++j) cp[j] = spv[ct * CPT + j];
+    cg::this_grid().sync();
+    if (__ldcg(&p.sweep_chg[sweep]) == 0 || sweep + 1 >= p.max_sweeps) {
+      if (blockIdx.x == 0 && tid == 0) p.info[2] = sweep + 1;
+      return;
+    }
+  }
+}
+
+}  // namespace sssp_b200

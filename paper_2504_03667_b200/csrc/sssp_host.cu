@@ -20,6 +20,7 @@
 
 #include "../../include/sssp_cuda.h"
 #include "bucket_kernel.cuh"
+#include "dataparallel_kernel.cuh"
 #include "validate_kernel.cuh"
 #include "dispatch.h"
 #include "host_narrow.h"
@@ -1552,6 +1553,136 @@ int sssp_validate(sssp_graph* g, uint64_t source, const uint64_t* dist, const ui
     for (void* x : {dd, dp, dj, dj2, db}) pool_free(s, x);
   }
   *violations = total;
+  return SSSP_OK;
+}
+
+// The paper's data-parallel engine (dataparallel_kernel.cuh): relaxation
+// rounds to a fixpoint, then reconstruct_predecessors, bit-identical to
+// dijkstra_dataparallel (dataparallel.hpp:302-327).  One shard.
+int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, uint64_t* pred_out,
+                            uint64_t* rounds_out, sssp_solve_stats* st) {
+  if (!g) return fail(SSSP_ERR_BAD_ARG, "null handle");
+  if (source >= g->n) return fail(SSSP_ERR_BAD_SOURCE, "dijkstra_dataparallel: source out of range");
+  if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
+  if (g->P != 1 || g->multiproc) return fail(SSSP_ERR_UNSUPPORTED, "dataparallel engine: one shard");
+  Shard& s = g->sh[0];
+  if (!g->cluster || (s.G & (s.G - 1)) || (s.L & (s.L - 1)))
+    return fail(SSSP_ERR_UNSUPPORTED, "dataparallel engine needs the cluster layout");
+  CK(cudaSetDevice(s.device));
+  const uint32_t wb = g->wbytes, n = (uint32_t)g->n;
+  const uint64_t rs = s.row_stride, words = rs / 32;
+  void* frelax = wb == 1 ? (void*)dp_relax_kernel<uint8_t>
+                 : wb == 2 ? (void*)dp_relax_kernel<uint16_t> : (void*)dp_relax_kernel<uint32_t>;
+  void* ftree = wb == 1 ? (void*)dp_tree_kernel<uint8_t, false>
+                : wb == 2 ? (void*)dp_tree_kernel<uint16_t, false> : (void*)dp_tree_kernel<uint32_t, false>;
+  void* fsweep = wb == 1 ? (void*)dp_tree_kernel<uint8_t, true>
+                 : wb == 2 ? (void*)dp_tree_kernel<uint16_t, true> : (void*)dp_tree_kernel<uint32_t, true>;
+  // tile: 128 B of every row per CTA, widened until the grid is co-resident
+  uint32_t T = 128 / wb;
+  size_t sm_relax = 0, sm_tree = 0;
+  int sms = 0;
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
+  while (true) {
+    if (T > rs) T = (uint32_t)rs;
+    const uint64_t G = rs / T;
+    sm_relax = dp_relax_smem_bytes(T, (uint32_t)words, wb);
+    sm_tree = dp_pred_smem_bytes(T, wb);
+    bool fits = T * wb / 16 <= (uint32_t)kBucketThreads && sm_relax <= 200 * 1024;
+    for (void* f : {frelax, fsweep}) {
+      if (!fits) break;
+      const size_t sm = f == frelax ? sm_relax : sm_tree;
+      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      int per_sm = 0;
+      CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kBucketThreads, sm));
+      fits = per_sm > 0 && G <= (uint64_t)per_sm * sms;
+    }
+    if (fits) break;
+    if (T * wb >= 4096 || T >= rs) return fail(SSSP_ERR_UNSUPPORTED, "dataparallel grid does not fit");
+    T *= 2;
+  }
+  CK(cudaFuncSetAttribute(ftree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tree));
+  const uint32_t G = (uint32_t)(rs / T);
+  const uint32_t max_sweeps = n + 2;
+  // scratch: front [2][words] | cnt [2][G] | snap [2][rs] | dist_v [n] | pass_v [n] |
+  //          sweep_chg [max_sweeps] | flag | info [4] u64
+  const uint64_t o_front = 0, o_cnt = o_front + 2 * words * 4, o_snap = (o_cnt + 2ull * G * 4 + 15) & ~15ull;
+  const uint64_t o_dv = o_snap + 2 * rs * 4, o_pv = o_dv + (uint64_t)n * 4, o_chg = o_pv + (uint64_t)n * 4;
+  const uint64_t o_flag = o_chg + (uint64_t)max_sweeps * 4, o_info = (o_flag + 4 + 15) & ~15ull;
+  const uint64_t bytes = o_info + 4 * 8;
+  void* scratch = nullptr;
+  int rc = pool_alloc(s, &scratch, bytes);
+  if (rc) return rc;
+  char* b = static_cast<char*>(scratch);
+  DpParams p{};
+  p.adj = s.d_adj;
+  p.row_stride = rs;
+  p.n = n;
+  p.Q = s.G;
+  p.qbits = bitlen(s.G) - 1;
+  p.lbits = bitlen(s.L) - 1;
+  p.T = T;
+  p.source = (uint32_t)source;
+  p.gfront = reinterpret_cast<uint32_t*>(b + o_front);
+  p.gcnt = reinterpret_cast<uint32_t*>(b + o_cnt);
+  p.gsnap = reinterpret_cast<uint32_t*>(b + o_snap);
+  p.dist_v = reinterpret_cast<uint32_t*>(b + o_dv);
+  p.pass_v = nullptr;
+  p.sweep_chg = reinterpret_cast<uint32_t*>(b + o_chg);
+  p.max_sweeps = max_sweeps;
+  p.flag = reinterpret_cast<uint32_t*>(b + o_flag);
+  p.dist_out = s.d_dist;
+  p.pred_out = s.d_pred;
+  p.info = reinterpret_cast<uint64_t*>(b + o_info);
+  CK(cudaMemsetAsync(b + o_flag, 0, o_info + 32 - o_flag, s.stream));
+  CK(cudaEventRecord(s.ev0, s.stream));
+  void* args[] = {&p};
+  CK(cudaLaunchCooperativeKernel(frelax, dim3(G), dim3(kBucketThreads), args, sm_relax, s.stream));
+  CK(cudaLaunchKernel(ftree, dim3(G), dim3(kBucketThreads), args, sm_tree, s.stream));
+  uint32_t flag = 0;
+  CK(cudaMemcpyAsync(&flag, p.flag, 4, cudaMemcpyDeviceToHost, s.stream));
+  CK(cudaStreamSynchronize(s.stream));
+  uint64_t tree_passes = 1;
+  if (flag) {  // zero-weight tight edges: solve the pass numbers, then rebuild pred with them
+    p.pass_v = reinterpret_cast<uint32_t*>(b + o_pv);
+    CK(cudaMemsetAsync(p.pass_v, 0xFF, (uint64_t)n * 4, s.stream));
+    const uint32_t one = 1;
+    CK(cudaMemcpyAsync(p.pass_v + source, &one, 4, cudaMemcpyHostToDevice, s.stream));
+    CK(cudaMemsetAsync(p.sweep_chg, 0, (uint64_t)max_sweeps * 4, s.stream));
+    CK(cudaLaunchCooperativeKernel(fsweep, dim3(G), dim3(kBucketThreads), args, sm_tree, s.stream));
+    CK(cudaLaunchKernel(ftree, dim3(G), dim3(kBucketThreads), args, sm_tree, s.stream));
+    tree_passes = 2;
+  }
+  CK(cudaEventRecord(s.ev1, s.stream));
+  uint64_t info[4] = {};
+  CK(cudaMemcpyAsync(info, p.info, sizeof(info), cudaMemcpyDeviceToHost, s.stream));
+  CK(cudaStreamSynchronize(s.stream));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
+  if (flag && info[2] >= max_sweeps) {
+    pool_free(s, scratch);
+    return fail(SSSP_ERR_CUDA, "dataparallel: pass numbers did not converge");
+  }
+  const double t0 = now_s();
+  if (dist_out) CK(cudaMemcpyAsync(dist_out, s.d_dist, g->n * 8, cudaMemcpyDeviceToHost, s.stream));
+  if (pred_out) CK(cudaMemcpyAsync(pred_out, s.d_pred, g->n * 8, cudaMemcpyDeviceToHost, s.stream));
+  CK(cudaStreamSynchronize(s.stream));
+  pool_free(s, scratch);
+  if (rounds_out) *rounds_out = info[0];
+  if (st) {
+    *st = sssp_solve_stats{};
+    st->transfer_in_s = g->transfer_in_s;
+    st->rounds_s = ms * 1e-3;
+    st->transfer_out_s = now_s() - t0;
+    st->iterations = info[0];
+    st->rows_read = info[1] + g->n * (tree_passes + (flag ? info[2] : 0));
+    st->relax_checks = st->rows_read * rs;
+    st->matrix_bytes = g->matrix_bytes;
+    st->weight_bytes = wb;
+    st->ctas = G;
+    st->shards = 1;
+    st->engine = SSSP_ENGINE_DATAPARALLEL;
+    st->classes = (uint32_t)(flag ? info[2] : 0);  // pass-number sweeps (0: none needed)
+  }
   return SSSP_OK;
 }
 

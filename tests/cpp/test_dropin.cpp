@@ -1,5 +1,6 @@
 // test_dropin.cpp -- the C++ drop-in (include/sssp/cuda.hpp) against the
-// reference's own dijkstra_serial / dijkstra_partitioned, compiled from the
+// reference's own dijkstra_serial / dijkstra_partitioned /
+// dijkstra_dataparallel, compiled from the
 // unmodified reference headers (oracle/Makefile -> oracle/_ref/test_dropin).
 // Exit code 0 = every ShortestPathResult compares equal (result.hpp:18).
 #include <cstdio>
@@ -54,8 +55,32 @@ int main() {
         EXPECT(cuda::dijkstra(g, s) == want);
         EXPECT(cuda::dijkstra_partitioned(g, s, {0, 0, 0}) == want);
         EXPECT(dijkstra_partitioned(g, s, 3).result == want);
+        // the paper's data-parallel engine: result AND round count
+        const DataParallelRun dp = dijkstra_dataparallel(g, s);
+        const cuda::DataParallelRun cdp = cuda::dijkstra_dataparallel(g, s);
+        EXPECT(cdp.result == dp.result);
+        EXPECT(cdp.rounds == dp.rounds);
+        EXPECT(cdp.cells_in == dp.cells_in && cdp.cells_out == dp.cells_out);
         ++graphs;
       }
+  // test_dataparallel.cpp:144-154: zero-weight ties, reconstructed pred
+  {
+    EdgeList z;
+    z.n = 4;
+    z.edges = {{2, 0, 5}, {2, 1, 5}, {0, 1, 0}, {1, 3, 2}};
+    const Graph zg = graph_from_edges(z, false);
+    const cuda::DataParallelRun c = cuda::dijkstra_dataparallel(zg, 2);
+    EXPECT(c.result == dijkstra_dataparallel(zg, 2).result);
+    EXPECT((c.result.dist == std::vector<Weight>{5, 5, 0, 7}));
+    EXPECT(validate_result(zg, c.result).empty());
+    bool t2 = false;
+    try {
+      cuda::dijkstra_dataparallel(zg, 4);
+    } catch (const std::invalid_argument&) {
+      t2 = true;
+    }
+    EXPECT(t2);
+  }
   // device-side build from the reference's own parsed EdgeList (-w off and on)
   {
     std::istringstream in("5 6\n0 1 4\n1 2 1\n0 2 9\n2 3 2\n3 4 1\n0 1 3\n");

@@ -82,6 +82,25 @@ def main():
             r = R.parse(t, directed)
             parse[f"{k}:{directed}"] = [r[0], r[1], r[2]] if r[0] != "ok" else ["ok", r[1], h(r[2])]
     out["parse"] = {"texts": texts, "results": parse}
+    # dijkstra_dataparallel (dataparallel.hpp:302-327): dist, reconstructed pred, rounds
+    dp = []
+
+    def dpcase(name, adj, n, source, keep_arrays=True, **extra):
+        d, p, r = R.dataparallel(adj, n, source, 1)
+        c = {"name": name, "n": n, "source": source, "rounds": r, **extra}
+        if keep_arrays:
+            c.update(adj=[int(x) for x in adj], dist=[int(x) for x in d], pred=[int(x) for x in p])
+        else:
+            c.update(dist_sha=h(d), pred_sha=h(p))
+        dp.append(c)
+
+    dpcase("four_vertex_undirected_s0", R.from_edges(4, four, False), 4, 0)       # test_dataparallel.cpp:60-66
+    dpcase("single_vertex", np.zeros(1, np.uint64), 1, 0)                         # :68-73
+    dpcase("zero_weight_tie_s2", R.from_edges(4, zw, False), 4, 2)                # :144-154
+    zw2 = [(0, 1, 0), (1, 2, 0), (2, 0, 0), (3, 1, 0), (3, 4, 1), (4, 2, 0), (5, 3, 2), (0, 5, 2)]
+    dpcase("zero_weight_cycle_s5", R.from_edges(6, zw2, True), 6, 5)              # multi-pass attach
+    dpcase("config1_dense_n1000_seed42", R.dense(1000, 42), 1000, 0, keep_arrays=False, seed=42)
+    out["dataparallel"] = dp
     with open(os.path.join(HERE, "golden.json"), "w") as f:
         json.dump(out, f, indent=0)
     print("wrote", os.path.join(HERE, "golden.json"))

@@ -146,6 +146,31 @@ __global__ void __launch_bounds__(256, 2) bulk_kernel(const uint8_t* __restrict_
   if (acc == 0x12345678u) out[0] = acc;
 }
 
+// Matrix-slice streaming: a [rows x rowbytes] matrix read by 256 CTAs, CTA c
+// taking column block c % nb (width rowbytes/nb) over row block c / nb;
+// 16 B per thread, 8 rows in flight.  nb = 256 is the bucket/dataparallel
+// tile layout (128 B of every row per CTA).
+__global__ void __launch_bounds__(256, 2) slice_kernel(const uint8_t* __restrict__ m, uint32_t rows,
+                                                       uint32_t rowbytes, uint32_t nb, uint32_t* out) {
+  const uint32_t cb = blockIdx.x % nb, rb = blockIdx.x / nb, nrb = gridDim.x / nb;
+  const uint32_t width = rowbytes / nb, tpr = width / 16, rg = 256 / tpr;
+  const uint32_t r_lo = rb * (rows / nrb), r_hi = r_lo + rows / nrb;
+  const uint32_t t = threadIdx.x % tpr, g = threadIdx.x / tpr;
+  uint32_t acc = 0;
+  for (uint32_t r0 = r_lo + g; r0 < r_hi; r0 += 8 * rg) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t r = r0 + k * rg;
+      v[k] = r < r_hi ? __ldg(reinterpret_cast<const uint4*>(m + (size_t)r * rowbytes + cb * width) + t)
+                      : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc = min(acc ^ v[k].x, v[k].y ^ v[k].z ^ v[k].w);
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
 int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -193,7 +218,7 @@ int main() {
   // streaming: in-kernel span (min start .. max end, %globaltimer) of a read of
   // `bytes` over `grid` CTAs, L2 holding clean unrelated lines (no dirty flush)
   uint8_t* buf;
-  CK(cudaMalloc(&buf, 1024ull << 20));
+  CK(cudaMalloc(&buf, 1024ull << 20));  // >= the 1 GiB slice matrix
   CK(cudaMemset(buf, 1, 1024ull << 20));
   CK(cudaDeviceSynchronize());
   const uint64_t sizes[] = {1073ull * 32768, 128ull << 20, 512ull << 20};
@@ -218,6 +243,29 @@ int main() {
                variant ? 16 : 8, grid, (unsigned long long)bytes, best * 1e-3, bytes / (best * 1e-9) / 1e9);
       }
     }
+  {
+    const uint32_t rows = 32768, rowbytes = 32768;
+    const uint32_t nbs[] = {256, 64, 16, 8};
+    for (uint32_t nb : nbs) {
+      float best = 1e9;
+      for (int it = 0; it < 5; ++it) {
+        stream_kernel<8, false><<<296, 256, 0>>>((const uint4*)(buf + (512ull << 20)), (256ull << 20) / 16, (uint32_t*)out);
+        cudaEvent_t a, b2;
+        CK(cudaEventCreate(&a));
+        CK(cudaEventCreate(&b2));
+        CK(cudaEventRecord(a));
+        slice_kernel<<<256, 256>>>(buf, rows, rowbytes, nb, (uint32_t*)out);
+        CK(cudaEventRecord(b2));
+        CK(cudaEventSynchronize(b2));
+        float ms;
+        CK(cudaEventElapsedTime(&ms, a, b2));
+        if (ms < best) best = ms;
+      }
+      const double bytes = (double)rows * rowbytes;
+      printf("{\"bench\": \"slice\", \"col_blocks\": %u, \"slice_bytes\": %u, \"us\": %.1f, \"GBps\": %.0f}\n",
+             nb, rowbytes / nb, best * 1e3, bytes / (best * 1e-3) / 1e9);
+    }
+  }
   printf("{\"bench\": \"info\", \"sms\": %d}\n", sms);
   return 0;
 }
