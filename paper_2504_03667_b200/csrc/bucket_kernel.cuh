@@ -97,6 +97,18 @@ struct BucketKey<uint16_t> {
 template <>
 struct BucketKey<uint32_t> : BucketKey<uint16_t> {};
 
+// Packed key of weight j of a 16 B chunk word and vertex u.  u8: one PRMT
+// builds (w << 24) | u (u < 2^24).
+template <typename W>
+__device__ __forceinline__ typename BucketKey<W>::T chunk_key(uint32_t word, int j, uint32_t u) {
+  if constexpr (sizeof(W) == 1) {
+    return __byte_perm(word, u, 0x0654u | ((uint32_t)(j % 4) << 12));
+  } else {
+    const uint32_t w = sizeof(W) == 4 ? word : (word >> ((j % 2) * 16)) & 0xFFFFu;
+    return BucketKey<W>::make(w, u);
+  }
+}
+
 // shared- or global-memory atomic minimum of a packed key
 __device__ __forceinline__ void smem_min(uint32_t* a, uint32_t v) { atomicMin(a, v); }
 __device__ __forceinline__ void smem_min(uint64_t* a, uint64_t v) {
@@ -418,9 +430,8 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
             const uint32_t wd[4] = {vb[m].x, vb[m].y, vb[m].z, vb[m].w};
 #pragma unroll
             for (int j = 0; j < CPT; ++j) {
-              const uint32_t word = wd[(j * sizeof(W)) / 4];
-              const uint32_t w = sizeof(W) == 4 ? word : (word >> (((j * sizeof(W)) % 4) * 8)) & WINF;
-              const K k = KT::make(w, ub[m]);  // INF weights make keys above every finite one
+              // INF weights make keys above every finite one
+              const K k = chunk_key<W>(wd[(j * sizeof(W)) / 4], j, ub[m]);
               best[j] = k < best[j] ? k : best[j];
             }
           }
@@ -556,11 +567,12 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
           // consecutive positions of one participant: vertex ids step by Q
           const uint32_t vid0 = gvid(pos0);
           const uint32_t wd[4] = {v4[m].x, v4[m].y, v4[m].z, v4[m].w};
+          // scalar and branch-free: measured faster than 16x2/byte-SIMD
+          // variants with a data-dependent skip (profiles/r01_bucket_phase_trace_v2.txt)
 #pragma unroll
           for (int cc = 0; cc < CPT; ++cc) {
-            const uint32_t word = wd[(cc * sizeof(W)) / 4];
-            const uint32_t w = sizeof(W) == 4 ? word : (word >> (((cc * sizeof(W)) % 4) * 8)) & WINF;
-            const K kk = ((bits >> cc) & 1u) ? KT::make(w, vid0 + cc * p.Q) : KT::kNone;
+            const K kk = ((bits >> cc) & 1u) ? chunk_key<W>(wd[(cc * sizeof(W)) / 4], cc, vid0 + cc * p.Q)
+                                              : KT::kNone;
             run = kk < run ? kk : run;
           }
         }

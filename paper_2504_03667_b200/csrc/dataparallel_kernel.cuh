@@ -30,10 +30,10 @@
 //   pred(v) = the smallest tight u with f(u) <= pass(v).
 // A tight edge with w >= 1 always runs forward in the order, so without a
 // zero-weight tight edge every pass is 1 and pred(v) is simply the smallest
-// tight parent: one pass over the matrix (dp_pred_kernel).  Only when that
+// tight parent: one pass over the matrix (dp_tree_kernel).  Only when that
 // pass finds a zero-weight tight edge between distinct vertices are the pass
 // numbers solved -- a min-plus fixpoint over the tight edges, iterated to
-// convergence by dp_pass_kernel -- and the predecessors recomputed with them.
+// convergence by dp_tree_kernel<SWEEP> -- and the predecessors recomputed.
 #pragma once
 
 #include <cooperative_groups.h>
@@ -58,10 +58,18 @@ struct DpParams {
   uint32_t* flag;       // [1] dp_pred_kernel: 1 if a zero-weight tight edge u != v exists
   uint64_t* dist_out;   // [n] reference encoding
   uint64_t* pred_out;   // [n]
-  uint64_t* info;       // [4]: rounds, frontier rows pushed, sweeps, -
+  uint64_t* info;       // [4]: rounds, frontier rows pushed, sweeps, max finite dist (zeroed)
 };
 
 constexpr uint32_t kDpInf = 0xFFFFFFFFu;
+
+// weight j of a 16 B chunk word (u8: one PRMT, zero-extended)
+template <typename W>
+__device__ __forceinline__ uint32_t dp_weight(uint32_t word, int j) {
+  if constexpr (sizeof(W) == 1) return __byte_perm(word, 0u, 0x4440u + (uint32_t)(j % 4));
+  else if constexpr (sizeof(W) == 2) return __byte_perm(word, 0u, (j % 2) ? 0x4432u : 0x4410u);
+  else return word;
+}
 
 // Dynamic smem of dp_relax_kernel: dist[T] | lowered[T/32] | frontier bitmap
 // [row_stride/32] | ids [kBucketChunk] | combine [kBucketThreads*CPT] u32.
@@ -182,10 +190,12 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpPar
 #pragma unroll
           for (int j = 0; j < CPT; ++j) {
             const uint32_t word = wd[(j * sizeof(W)) / 4];
-            const uint32_t w = sizeof(W) == 4 ? word : (word >> (((j * sizeof(W)) % 4) * 8)) & WINF;
-            // du + w < 2^32 - 1 for finite operands (host-checked n * max_w)
-            const uint32_t cand = w == WINF ? kDpInf : du[m] + w;
-            best[j] = min(best[j], cand);
+            const uint32_t w = dp_weight<W>(word, j);
+            // min(du + w, best) in one VIADDMNMX; an INF weight gets the base
+            // INF - WINF so its candidate is exactly INF (du + w < 2^32 - 1
+            // for finite operands: host-checked n * max_w)
+            const uint32_t base = w == WINF ? kDpInf - WINF : du[m];
+            best[j] = __viaddmin_u32(base, w, best[j]);
           }
         }
       }
@@ -223,13 +233,17 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpPar
     cg::this_grid().sync();
     par = nxt;
   }
+  uint32_t dmax = 0;
   for (uint32_t i = tid; i < T; i += kBucketThreads) {
     const uint32_t v = vid(p0 + i);
     if (v < p.n) {
       p.dist_v[v] = sdist[i];
       p.dist_out[v] = sdist[i] == kDpInf ? ~0ull : (uint64_t)sdist[i];
+      if (sdist[i] != kDpInf) dmax = max(dmax, sdist[i]);
     }
   }
+  dmax = __reduce_max_sync(0xFFFFFFFFu, dmax);
+  if (lane == 0 && dmax) atomicMax(reinterpret_cast<unsigned long long*>(&p.info[3]), (unsigned long long)dmax);
   if (blockIdx.x == 0 && tid == 0) {
     p.info[0] = rounds;
     p.info[1] = pushed;
@@ -246,7 +260,13 @@ __host__ __device__ constexpr size_t dp_pred_smem_bytes(uint32_t T, uint32_t wby
 // qualifies); flags a zero-weight tight edge between distinct vertices.
 // SWEEP = true instead iterates pass(v) = min over tight u of f(u) to its
 // fixpoint (cooperative launch; one grid barrier per sweep).
-template <typename W, bool SWEEP>
+// FAST (non-SWEEP, u8/u16 weights, no zero weight anywhere and every finite
+// dist < WINF): tight <=> w == dv - du, and an INF weight or an unreachable
+// column (dv - du > WINF) can never satisfy it, so the per-weight work is one compare and a predicated
+// min; only the diagonal (w(v,v) = 0 == dv - dv) needs excluding, once per
+// row.  Branch-free straight-line code in the inner loops (a data-dependent
+// skip there measured slower).
+template <typename W, bool SWEEP, bool FAST>
 __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpParams p) {
   namespace cg = cooperative_groups;
   constexpr uint32_t WINF = WInf<W>::v;
@@ -268,15 +288,11 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpPara
     spv[i] = v < p.n && p.pass_v ? p.pass_v[v] : 1u;
   }
   __syncthreads();
-  // my CPT columns: vertex ids and (dist, pass)
-  uint32_t cv[CPT], cd[CPT], cp[CPT];
+  // my CPT columns: consecutive positions of one participant, ids step by Q
+  uint32_t cd[CPT];
 #pragma unroll
-  for (int j = 0; j < CPT; ++j) {
-    const uint32_t col = ct * CPT + j;
-    cv[j] = vid(p0 + col);
-    cd[j] = sdv[col];
-    cp[j] = spv[col];
-  }
+  for (int j = 0; j < CPT; ++j) cd[j] = sdv[ct * CPT + j];
+  const uint32_t cv0 = vid(p0 + ct * CPT);
   bool zero_tight = false;
   for (uint32_t sweep = 0;; ++sweep) {
     uint32_t best[CPT];
@@ -289,7 +305,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpPara
       for (int m = 0; m < 8; ++m) {
         const uint32_t u = u0 + m * RG;
         du[m] = u < p.n ? __ldcg(&p.dist_v[u]) : kDpInf;
-        pu[m] = (u < p.n && p.pass_v) ? __ldcg(&p.pass_v[u]) : 1u;
+        pu[m] = (!FAST && u < p.n && p.pass_v) ? __ldcg(&p.pass_v[u]) : 1u;
         if (du[m] != kDpInf)
           vb[m] = __ldg(reinterpret_cast<const uint4*>(
               reinterpret_cast<const uint8_t*>(adj + (size_t)u * p.row_stride + p0) + ct * 16));
@@ -299,19 +315,30 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpPara
         const uint32_t u = u0 + m * RG;
         if (du[m] == kDpInf || pu[m] == kDpInf) continue;  // unreachable, or not attached yet
         const uint32_t wd[4] = {vb[m].x, vb[m].y, vb[m].z, vb[m].w};
+        if constexpr (FAST) {
+          const uint32_t dj = u - cv0;  // row u is my column j's own vertex iff dj == j*Q
+          const uint32_t jd = ((dj & (p.Q - 1)) == 0 && (dj >> p.qbits) < (uint32_t)CPT)
+                                  ? (dj >> p.qbits) : (uint32_t)CPT;
 #pragma unroll
-        for (int j = 0; j < CPT; ++j) {
-          const uint32_t word = wd[(j * sizeof(W)) / 4];
-          const uint32_t w = sizeof(W) == 4 ? word : (word >> (((j * sizeof(W)) % 4) * 8)) & WINF;
-          if (w == WINF || u == cv[j] || cd[j] == kDpInf || du[m] + w != cd[j]) continue;
-          // f(u): the pass in which v may attach to u (source: pass 1)
-          const uint32_t after = (du[m] > cd[j] || (du[m] == cd[j] && u > cv[j])) ? 1u : 0u;
-          const uint32_t f = u == p.source ? 1u : pu[m] + after;
-          if (!SWEEP) {
-            zero_tight |= w == 0;
-            if (f <= cp[j]) best[j] = min(best[j], u);  // smallest qualifying parent
-          } else {
-            best[j] = min(best[j], f);
+          for (int j = 0; j < CPT; ++j) {
+            const uint32_t w = dp_weight<W>(wd[(j * (int)sizeof(W)) / 4], j);
+            if (w == cd[j] - du[m] && (uint32_t)j != jd) best[j] = min(best[j], u);
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < CPT; ++j) {
+            const uint32_t w = dp_weight<W>(wd[(j * (int)sizeof(W)) / 4], j);
+            const uint32_t v = cv0 + j * p.Q;
+            const bool tight = w != WINF && u != v && cd[j] != kDpInf && du[m] + w == cd[j];
+            // f(u): the pass in which v may attach to u (source: pass 1)
+            const uint32_t after = (du[m] > cd[j] || (du[m] == cd[j] && u > v)) ? 1u : 0u;
+            const uint32_t f = u == p.source ? 1u : pu[m] + after;
+            if (!SWEEP) {
+              zero_tight |= tight && w == 0;
+              if (tight && f <= spv[ct * CPT + j]) best[j] = min(best[j], u);  // smallest qualifying parent
+            } else {
+              if (tight) best[j] = min(best[j], f);
+            }
           }
         }
       }
@@ -344,8 +371,6 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpPara
       }
     }
     if (__syncthreads_or(changed) && tid == 0) atomicAdd(&p.sweep_chg[sweep], 1u);
-#pragma unroll
-    for (int j = 0; j < CPT; ++j) cp[j] = spv[ct * CPT + j];
     cg::this_grid().sync();
     if (__ldcg(&p.sweep_chg[sweep]) == 0 || sweep + 1 >= p.max_sweeps) {
       if (blockIdx.x == 0 && tid == 0) p.info[2] = sweep + 1;

@@ -1573,10 +1573,15 @@ int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, 
   const uint64_t rs = s.row_stride, words = rs / 32;
   void* frelax = wb == 1 ? (void*)dp_relax_kernel<uint8_t>
                  : wb == 2 ? (void*)dp_relax_kernel<uint16_t> : (void*)dp_relax_kernel<uint32_t>;
-  void* ftree = wb == 1 ? (void*)dp_tree_kernel<uint8_t, false>
-                : wb == 2 ? (void*)dp_tree_kernel<uint16_t, false> : (void*)dp_tree_kernel<uint32_t, false>;
-  void* fsweep = wb == 1 ? (void*)dp_tree_kernel<uint8_t, true>
-                 : wb == 2 ? (void*)dp_tree_kernel<uint16_t, true> : (void*)dp_tree_kernel<uint32_t, true>;
+  void* ftree = wb == 1 ? (void*)dp_tree_kernel<uint8_t, false, false>
+                : wb == 2 ? (void*)dp_tree_kernel<uint16_t, false, false>
+                          : (void*)dp_tree_kernel<uint32_t, false, false>;
+  void* ffast = wb == 1 ? (void*)dp_tree_kernel<uint8_t, false, true>
+                : wb == 2 ? (void*)dp_tree_kernel<uint16_t, false, true>
+                          : (void*)dp_tree_kernel<uint32_t, false, true>;
+  void* fsweep = wb == 1 ? (void*)dp_tree_kernel<uint8_t, true, false>
+                 : wb == 2 ? (void*)dp_tree_kernel<uint16_t, true, false>
+                           : (void*)dp_tree_kernel<uint32_t, true, false>;
   // tile: 128 B of every row per CTA, widened until the grid is co-resident
   uint32_t T = 128 / wb;
   size_t sm_relax = 0, sm_tree = 0;
@@ -1601,6 +1606,7 @@ int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, 
     T *= 2;
   }
   CK(cudaFuncSetAttribute(ftree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tree));
+  CK(cudaFuncSetAttribute(ffast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tree));
   const uint32_t G = (uint32_t)(rs / T);
   const uint32_t max_sweeps = n + 2;
   // scratch: front [2][words] | cnt [2][G] | snap [2][rs] | dist_v [n] | pass_v [n] |
@@ -1637,7 +1643,15 @@ int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, 
   CK(cudaEventRecord(s.ev0, s.stream));
   void* args[] = {&p};
   CK(cudaLaunchCooperativeKernel(frelax, dim3(G), dim3(kBucketThreads), args, sm_relax, s.stream));
-  CK(cudaLaunchKernel(ftree, dim3(G), dim3(kBucketThreads), args, sm_tree, s.stream));
+  // FAST tree pass when no weight is 0 (no zero-weight tie can exist) and no
+  // finite dist reaches WINF: with u8/u16 weights an INF weight or an
+  // unreachable column (dv = 2^32-1) can then never look tight (not u32)
+  uint64_t dmax = 0;
+  CK(cudaMemcpyAsync(&dmax, p.info + 3, 8, cudaMemcpyDeviceToHost, s.stream));
+  CK(cudaStreamSynchronize(s.stream));
+  const uint64_t winf = wb == 1 ? 0xFFull : wb == 2 ? 0xFFFFull : 0xFFFFFFFFull;
+  const bool fast = wb <= 2 && g->min_w >= 1 && dmax < winf;
+  CK(cudaLaunchKernel(fast ? ffast : ftree, dim3(G), dim3(kBucketThreads), args, sm_tree, s.stream));
   uint32_t flag = 0;
   CK(cudaMemcpyAsync(&flag, p.flag, 4, cudaMemcpyDeviceToHost, s.stream));
   CK(cudaStreamSynchronize(s.stream));
