@@ -109,6 +109,19 @@ __device__ __forceinline__ typename BucketKey<W>::T chunk_key(uint32_t word, int
   }
 }
 
+// Asynchronous 16 B global -> shared copies (LDGSTS, L2 only): a thread
+// streams row slices into its own shared-memory slots so the next batch's
+// loads are in flight while the current batch is processed.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
 // shared- or global-memory atomic minimum of a packed key
 __device__ __forceinline__ void smem_min(uint32_t* a, uint32_t v) { atomicMin(a, v); }
 __device__ __forceinline__ void smem_min(uint64_t* a, uint64_t v) {

@@ -71,11 +71,15 @@ __device__ __forceinline__ uint32_t dp_weight(uint32_t word, int j) {
   else return word;
 }
 
-// Dynamic smem of dp_relax_kernel: dist[T] | lowered[T/32] | frontier bitmap
-// [row_stride/32] | ids [kBucketChunk] | combine [kBucketThreads*CPT] u32.
+constexpr int kDpBatch = 8;  // rows per thread per cp.async pipeline stage
+constexpr int kDpChunk = kBucketThreads * 32;  // frontier ids enumerated per pass (1 word/thread)
+
+// Dynamic smem of dp_relax_kernel: stage[2][kDpBatch][threads] uint4 (aliased by
+// the per-thread column minima once the rows are consumed) | dist[T] |
+// lowered[T/32] | frontier bitmap [row_stride/32] | ids [kDpChunk].
 __host__ __device__ constexpr size_t dp_relax_smem_bytes(uint32_t T, uint32_t words, uint32_t wbytes) {
-  return 4ull * (T + bucket_round4(T / 32) + bucket_round4(words) + kBucketChunk) +
-         4ull * kBucketThreads * (16 / wbytes);
+  return 16ull * 2 * kDpBatch * kBucketThreads +
+         4ull * (T + bucket_round4(T / 32) + bucket_round4(words) + kDpChunk) + 0 * wbytes;
 }
 
 template <typename W>
@@ -86,11 +90,12 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpPar
   extern __shared__ __align__(16) uint32_t smem[];
   const uint32_t T = p.T, G = gridDim.x, TW = T / 32;
   const uint32_t words = (uint32_t)(p.row_stride / 32);
-  uint32_t* sdist = smem;
+  uint4* sstage = reinterpret_cast<uint4*>(smem);  // [2][kDpBatch][threads], thread-private
+  uint32_t* scomb = smem;                           // aliases the stage after the rows
+  uint32_t* sdist = smem + 4 * 2 * kDpBatch * kBucketThreads;
   uint32_t* slow = sdist + T;  // columns lowered this round
   uint32_t* sbm = slow + bucket_round4(TW);
   uint32_t* schunk = sbm + bucket_round4(words);
-  uint32_t* scomb = schunk + kBucketChunk;
   __shared__ uint32_t s_red[kBucketThreads / 32];
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t p0 = blockIdx.x * T;
@@ -139,7 +144,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpPar
     uint32_t best[CPT];
 #pragma unroll
     for (int j = 0; j < CPT; ++j) best[j] = kDpInf;
-    constexpr uint32_t WPT = 2;
+    constexpr uint32_t WPT = 1;
     for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads * WPT) {
       const uint32_t w0 = wbase + tid * WPT;
       uint32_t bw[WPT];
@@ -169,36 +174,52 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpPar
         for (uint32_t m = bw[k2]; m; m &= m - 1) schunk[o++] = (w0 + k2) * 32 + (__ffs(m) - 1);
       __syncthreads();
       const uint32_t* snap = p.gsnap + par * p.row_stride;
-      for (uint32_t r0 = rg; r0 < tot; r0 += 8 * RG) {
-        uint32_t du[8];
-        uint4 vb[8];
+      // two-stage cp.async pipeline over this pass's rows: batch b+1's slices
+      // stream into the thread's shared-memory slots while batch b is relaxed
+      const uint32_t per_batch = kDpBatch * RG;
+      const uint32_t nbatch = (tot + per_batch - 1) / per_batch;
+      uint32_t du_c[kDpBatch], du_n[kDpBatch];
+      auto issue = [&](uint32_t b, uint32_t* du) {
+        uint4* st = sstage + (size_t)(b & 1u) * kDpBatch * kBucketThreads;
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          const uint32_t r = r0 + m * RG;
+        for (int m = 0; m < kDpBatch; ++m) {
+          const uint32_t r = b * per_batch + rg + m * RG;
           du[m] = kDpInf;
           if (r < tot) {
             const uint32_t pos = schunk[r];
             du[m] = __ldcg(&snap[pos]);
-            vb[m] = __ldg(reinterpret_cast<const uint4*>(
-                reinterpret_cast<const uint8_t*>(adj + (size_t)vid(pos) * p.row_stride + p0) + ct * 16));
+            cp_async16(&st[m * kBucketThreads + tid],
+                       reinterpret_cast<const uint8_t*>(adj + (size_t)vid(pos) * p.row_stride + p0) +
+                           ct * 16);
           }
         }
+        cp_async_commit();
+      };
+      if (nbatch) issue(0, du_c);
+      for (uint32_t b = 0; b < nbatch; ++b) {
+        if (b + 1 < nbatch) issue(b + 1, du_n);
+        else cp_async_commit();
+        cp_async_wait<1>();
+        const uint4* st = sstage + (size_t)(b & 1u) * kDpBatch * kBucketThreads;
 #pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          if (r0 + m * RG >= tot) break;
-          const uint32_t wd[4] = {vb[m].x, vb[m].y, vb[m].z, vb[m].w};
+        for (int m = 0; m < kDpBatch; ++m) {
+          const uint32_t dum = du_c[m];
+          du_c[m] = du_n[m];
+          if (b * per_batch + rg + m * RG >= tot) break;
+          const uint4 v4 = st[m * kBucketThreads + tid];
+          const uint32_t wd[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
           for (int j = 0; j < CPT; ++j) {
-            const uint32_t word = wd[(j * sizeof(W)) / 4];
-            const uint32_t w = dp_weight<W>(word, j);
+            const uint32_t w = dp_weight<W>(wd[(j * sizeof(W)) / 4], j);
             // min(du + w, best) in one VIADDMNMX; an INF weight gets the base
             // INF - WINF so its candidate is exactly INF (du + w < 2^32 - 1
             // for finite operands: host-checked n * max_w)
-            const uint32_t base = w == WINF ? kDpInf - WINF : du[m];
+            const uint32_t base = w == WINF ? kDpInf - WINF : dum;
             best[j] = __viaddmin_u32(base, w, best[j]);
           }
         }
       }
+      cp_async_wait<0>();
       __syncthreads();
     }
 #pragma unroll
@@ -250,9 +271,11 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpPar
   }
 }
 
-// Dynamic smem of dp_pred_kernel / dp_pass_kernel: dv[T] | passv[T] | combine.
+
+// Dynamic smem of dp_tree_kernel: stage[2][kDpBatch][threads] uint4 | dv[T] |
+// passv[T] | combine.
 __host__ __device__ constexpr size_t dp_pred_smem_bytes(uint32_t T, uint32_t wbytes) {
-  return 4ull * 2 * T + 4ull * kBucketThreads * (16 / wbytes);
+  return 16ull * 2 * kDpBatch * kBucketThreads + 4ull * 2 * T + 4ull * kBucketThreads * (16 / wbytes);
 }
 
 // One pass over every row: pred(v) = the smallest tight u != v with
@@ -273,7 +296,8 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpPara
   constexpr int CPT = 16 / (int)sizeof(W);
   extern __shared__ __align__(16) uint32_t smem[];
   const uint32_t T = p.T;
-  uint32_t* sdv = smem;
+  uint4* sstage = reinterpret_cast<uint4*>(smem);  // [2][kDpBatch][threads], thread-private slots
+  uint32_t* sdv = smem + 4 * 2 * kDpBatch * kBucketThreads;
   uint32_t* spv = sdv + T;
   uint32_t* scomb = spv + T;
   const uint32_t tid = threadIdx.x;
@@ -298,23 +322,39 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpPara
     uint32_t best[CPT];
 #pragma unroll
     for (int j = 0; j < CPT; ++j) best[j] = kDpInf;
-    for (uint32_t u0 = rg; u0 < p.n; u0 += 8 * RG) {
-      uint32_t du[8], pu[8];
-      uint4 vb[8];
+    // two-stage pipeline: batch b+1's row slices stream into shared memory
+    // (cp.async) while batch b is processed
+    const uint32_t per_batch = kDpBatch * RG;
+    const uint32_t nbatch = (p.n + per_batch - 1) / per_batch;
+    uint32_t du_c[kDpBatch], pu_c[kDpBatch], du_n[kDpBatch], pu_n[kDpBatch];
+    auto issue = [&](uint32_t b, uint32_t* du, uint32_t* pu) {
+      uint4* st = sstage + (size_t)(b & 1u) * kDpBatch * kBucketThreads;
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const uint32_t u = u0 + m * RG;
+      for (int m = 0; m < kDpBatch; ++m) {
+        const uint32_t u = b * per_batch + rg + m * RG;
         du[m] = u < p.n ? __ldcg(&p.dist_v[u]) : kDpInf;
         pu[m] = (!FAST && u < p.n && p.pass_v) ? __ldcg(&p.pass_v[u]) : 1u;
-        if (du[m] != kDpInf)
-          vb[m] = __ldg(reinterpret_cast<const uint4*>(
-              reinterpret_cast<const uint8_t*>(adj + (size_t)u * p.row_stride + p0) + ct * 16));
+        if (u < p.n)
+          cp_async16(&st[m * kBucketThreads + tid],
+                     reinterpret_cast<const uint8_t*>(adj + (size_t)u * p.row_stride + p0) + ct * 16);
       }
+      cp_async_commit();
+    };
+    issue(0, du_c, pu_c);
+    for (uint32_t b = 0; b < nbatch; ++b) {
+      if (b + 1 < nbatch) issue(b + 1, du_n, pu_n);
+      else cp_async_commit();  // empty group: the wait below always leaves one group pending
+      cp_async_wait<1>();
+      const uint4* st = sstage + (size_t)(b & 1u) * kDpBatch * kBucketThreads;
 #pragma unroll
-      for (int m = 0; m < 8; ++m) {
-        const uint32_t u = u0 + m * RG;
-        if (du[m] == kDpInf || pu[m] == kDpInf) continue;  // unreachable, or not attached yet
-        const uint32_t wd[4] = {vb[m].x, vb[m].y, vb[m].z, vb[m].w};
+      for (int m = 0; m < kDpBatch; ++m) {
+        const uint32_t u = b * per_batch + rg + m * RG;
+        const uint32_t dum = du_c[m], pum = pu_c[m];
+        du_c[m] = du_n[m];
+        pu_c[m] = pu_n[m];
+        if (dum == kDpInf || pum == kDpInf) continue;  // unreachable, or not attached yet
+        const uint4 v4 = st[m * kBucketThreads + tid];
+        const uint32_t wd[4] = {v4.x, v4.y, v4.z, v4.w};
         if constexpr (FAST) {
           const uint32_t dj = u - cv0;  // row u is my column j's own vertex iff dj == j*Q
           const uint32_t jd = ((dj & (p.Q - 1)) == 0 && (dj >> p.qbits) < (uint32_t)CPT)
@@ -322,17 +362,17 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpPara
 #pragma unroll
           for (int j = 0; j < CPT; ++j) {
             const uint32_t w = dp_weight<W>(wd[(j * (int)sizeof(W)) / 4], j);
-            if (w == cd[j] - du[m] && (uint32_t)j != jd) best[j] = min(best[j], u);
+            if (w == cd[j] - dum && (uint32_t)j != jd) best[j] = min(best[j], u);
           }
         } else {
 #pragma unroll
           for (int j = 0; j < CPT; ++j) {
             const uint32_t w = dp_weight<W>(wd[(j * (int)sizeof(W)) / 4], j);
             const uint32_t v = cv0 + j * p.Q;
-            const bool tight = w != WINF && u != v && cd[j] != kDpInf && du[m] + w == cd[j];
+            const bool tight = w != WINF && u != v && cd[j] != kDpInf && dum + w == cd[j];
             // f(u): the pass in which v may attach to u (source: pass 1)
-            const uint32_t after = (du[m] > cd[j] || (du[m] == cd[j] && u > v)) ? 1u : 0u;
-            const uint32_t f = u == p.source ? 1u : pu[m] + after;
+            const uint32_t after = (dum > cd[j] || (dum == cd[j] && u > v)) ? 1u : 0u;
+            const uint32_t f = u == p.source ? 1u : pum + after;
             if (!SWEEP) {
               zero_tight |= tight && w == 0;
               if (tight && f <= spv[ct * CPT + j]) best[j] = min(best[j], u);  // smallest qualifying parent
@@ -343,6 +383,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpPara
         }
       }
     }
+    cp_async_wait<0>();
 #pragma unroll
     for (int j = 0; j < CPT; ++j) scomb[tid * CPT + j] = best[j];
     __syncthreads();
