@@ -480,8 +480,11 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       // atomicMin per column it touched, and after an extra barrier every
       // owner applies its columns' minima.
       pulled += ucount;
-      K* sk = scomb;           // running key of the columns this CTA touches
-      uint32_t* scol = schunk; // their local positions (rank r0 + i)
+      // the combine region holds the touched columns' running keys and local
+      // positions (ncols <= T + 2, host-checked); the id chunk region becomes
+      // the cp.async stage [2][kPullDepth][threads] of 16 B slots
+      K* sk = scomb;
+      uint32_t* scol = reinterpret_cast<uint32_t*>(scomb + (T + 2));
       const uint32_t* bml = sbm + p.shard * lwords;
       const uint32_t wpt = (lwords + kBucketThreads - 1) / kBucketThreads;
       const uint32_t w0 = tid * wpt;
@@ -522,10 +525,14 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       for (uint32_t i = tid; i < ncols; i += kBucketThreads) sk[i] = KT::kNone;
       __syncthreads();
       stamp();
-      // kPullDepth independent 16 B loads in flight per thread.  A thread's
-      // items are lo + tid + k*256; their (column rank, chunk) pairs are
-      // walked incrementally (one division per thread, none per item).
+      if (p.trace && tid == 0 && p.shard == 0 && blockIdx.x < 1024)  // per-CTA pull span (debug)
+        p.trace[64 + 2 * blockIdx.x] = globaltimer();
+      // Two-stage cp.async pipeline: a thread's items are lo + tid + k*256;
+      // batch b+1's 16 B chunks stream into the thread's stage slots while
+      // batch b is consumed.  (column rank, chunk) pairs are walked
+      // incrementally (one division per thread, none per item).
       constexpr int kPullDepth = 8;
+      uint4* sstage = reinterpret_cast<uint4*>(schunk);
       auto row_of = [&](uint32_t rk) -> const uint8_t* {
         const uint32_t col = scol[rk - r0];
         const uint32_t v = p.adjT_by_pos ? col : pos_to_vid(col, p.Q, p.lbits, p.qbits);
@@ -538,30 +545,41 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
           ++rk;
         }
       };
-      uint32_t rk_t = 0, ch_t = 0;  // walk state of this thread's next item
+      uint32_t rk_t = 0, ch_t = 0;  // consume walk: this thread's next item
       if (lo + tid < hi) {
         rk_t = cpow2 ? (lo + tid) >> cbits : (lo + tid) / cpr;
         ch_t = lo + tid - rk_t * cpr;
       }
+      uint32_t rk_i = rk_t, ch_i = ch_t;  // issue walk, one batch ahead
+      const uint32_t nbatch = lo + tid < hi ? (hi - (lo + tid) + kBucketThreads * kPullDepth - 1) /
+                                                  (kBucketThreads * kPullDepth) : 0u;
+      auto issue = [&](uint32_t b) {
+        uint4* st = sstage + (size_t)(b & 1u) * kPullDepth * kBucketThreads;
+        const uint32_t it0 = lo + tid + b * kBucketThreads * kPullDepth;
+        uint32_t rrow = rk_i;
+        const uint8_t* row = row_of(rk_i);
+#pragma unroll
+        for (int m = 0; m < kPullDepth; ++m) {
+          if (it0 + m * kBucketThreads < hi) {
+            if (rk_i != rrow) {
+              rrow = rk_i;
+              row = row_of(rk_i);
+            }
+            cp_async16(&st[m * kBucketThreads + tid], row + ch_i * 16);
+          }
+          advance(rk_i, ch_i);
+        }
+        cp_async_commit();
+      };
       uint32_t cur = 0xFFFFFFFFu;
       K run = KT::kNone;
-      for (uint32_t it0 = lo + tid; it0 < hi; it0 += kBucketThreads * kPullDepth) {
-        uint4 v4[kPullDepth];
-        {
-          uint32_t rk = rk_t, ch = ch_t, rrow = rk_t;
-          const uint8_t* row = row_of(rk);
-#pragma unroll
-          for (int m = 0; m < kPullDepth; ++m) {
-            if (it0 + m * kBucketThreads < hi) {
-              if (rk != rrow) {
-                rrow = rk;
-                row = row_of(rk);
-              }
-              v4[m] = __ldg(reinterpret_cast<const uint4*>(row + ch * 16));
-            }
-            advance(rk, ch);
-          }
-        }
+      if (nbatch) issue(0);
+      for (uint32_t b = 0; b < nbatch; ++b) {
+        if (b + 1 < nbatch) issue(b + 1);
+        else cp_async_commit();  // empty group: the wait below leaves one group pending
+        cp_async_wait<1>();
+        const uint4* st = sstage + (size_t)(b & 1u) * kPullDepth * kBucketThreads;
+        const uint32_t it0 = lo + tid + b * kBucketThreads * kPullDepth;
 #pragma unroll
         for (int m = 0; m < kPullDepth; ++m) {
           const uint32_t item = it0 + m * kBucketThreads;
@@ -579,21 +597,45 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
           if (!bits) continue;
           // consecutive positions of one participant: vertex ids step by Q
           const uint32_t vid0 = gvid(pos0);
-          const uint32_t wd[4] = {v4[m].x, v4[m].y, v4[m].z, v4[m].w};
-          // scalar and branch-free: measured faster than 16x2/byte-SIMD
-          // variants with a data-dependent skip (profiles/r01_bucket_phase_trace_v2.txt)
+          const uint4 v4m = st[m * kBucketThreads + tid];
+          const uint32_t wd[4] = {v4m.x, v4m.y, v4m.z, v4m.w};
+          if constexpr (sizeof(W) == 1) {
+            // u8, branch-free: the chunk's minimum (w, position) pair on the
+            // native 16x2 min.  Non-class bytes -> 0xFF (INF); one PRMT packs
+            // two bytes with their in-chunk index as (w << 8 | cc) lanes; the
+            // min lane gives the smallest w at the lowest cc = lowest vertex id
+            // (ids rise with cc).  (A data-dependent skip here measured slower.)
+            uint32_t lanes[8];
 #pragma unroll
-          for (int cc = 0; cc < CPT; ++cc) {
-            const K kk = ((bits >> cc) & 1u) ? chunk_key<W>(wd[(cc * sizeof(W)) / 4], cc, vid0 + cc * p.Q)
-                                              : KT::kNone;
+            for (int k2 = 0; k2 < 4; ++k2) {
+              const uint32_t b4 = (bits >> (4 * k2)) & 0xFu;
+              const uint32_t mw = wd[k2] | ~(((b4 * 0x00204081u) & 0x01010101u) * 0xFFu);
+              const uint32_t ccs = 0x03020100u + 0x04040404u * (uint32_t)k2;
+              lanes[2 * k2] = __byte_perm(mw, ccs, 0x1504u);
+              lanes[2 * k2 + 1] = __byte_perm(mw, ccs, 0x3726u);
+            }
+            uint32_t mv = __vminu2(__vminu2(__vminu2(lanes[0], lanes[1]), __vminu2(lanes[2], lanes[3])),
+                                   __vminu2(__vminu2(lanes[4], lanes[5]), __vminu2(lanes[6], lanes[7])));
+            mv = min(mv & 0xFFFFu, mv >> 16);
+            const K kk = ((mv >> 8) << 24) | (vid0 + (mv & 0xFFu) * p.Q);
             run = kk < run ? kk : run;
+          } else {
+#pragma unroll
+            for (int cc = 0; cc < CPT; ++cc) {
+              const K kk = ((bits >> cc) & 1u) ? chunk_key<W>(wd[(cc * sizeof(W)) / 4], cc, vid0 + cc * p.Q)
+                                                : KT::kNone;
+              run = kk < run ? kk : run;
+            }
           }
         }
       }
+      cp_async_wait<0>();
       if (cur != 0xFFFFFFFFu && run != KT::kNone) smem_min(&sk[cur], run);
       __syncthreads();
       for (uint32_t i = tid; i < ncols; i += kBucketThreads)
         if (sk[i] != KT::kNone) smem_min(&pkey[scol[i]], sk[i]);
+      if (p.trace && tid == 0 && p.shard == 0 && blockIdx.x < 1024)
+        p.trace[64 + 2 * blockIdx.x + 1] = globaltimer();
       stamp();
       barrier();  // every partial minimum is in pkey
       stamp();

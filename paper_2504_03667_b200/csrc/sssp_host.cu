@@ -599,7 +599,7 @@ int plan_bucket(sssp_graph* g) {
       fits = per_sm > 0 && (uint64_t)g->bG * same <= (uint64_t)per_sm * sms;
     }
     if (fits) break;
-    if (T * g->wbytes >= 2048 || T >= s0.row_stride) {  // pull keys: T + 2 <= 4096 / wbytes
+    if (T * g->wbytes >= 1024 || T >= s0.row_stride) {  // pull: (T + 2) keys + ids fit the combine region
       if (want == SSSP_ENGINE_BUCKET) return fail(SSSP_ERR_UNSUPPORTED, "bucket grid does not fit");
       return SSSP_OK;  // AUTO: stay on the scan engine
     }
@@ -838,8 +838,8 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.info = s.d_info + (uint64_t)i * 4;
         bp.info2 = s.d_info2 + (uint64_t)i * 2;
         if (getenv("SSSP_BUCKET_TRACE") && s.k == 0) {  // debug: per-barrier timestamps
-          if (!s.d_trace) CK(cudaMalloc(&s.d_trace, 64 * 8));
-          CK(cudaMemsetAsync(s.d_trace, 0, 64 * 8, s.stream));
+          if (!s.d_trace) CK(cudaMalloc(&s.d_trace, (64 + 2048) * 8));
+          CK(cudaMemsetAsync(s.d_trace, 0, (64 + 2048) * 8, s.stream));
           bp.trace = s.d_trace;
         }
         bp.seq = g->bseq + 1 + i;
@@ -976,11 +976,22 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     g->bucket = false;
   if (g->multiproc) g->exch_base = last + 1;
   if (g->bucket && g->sh[0].d_trace) {
-    uint64_t tr[64];
-    CK(cudaMemcpy(tr, g->sh[0].d_trace, sizeof(tr), cudaMemcpyDeviceToHost));
-    fprintf(stderr, "bucket trace (us since init barrier):");
+    std::vector<uint64_t> tr(64 + 2048);
+    CK(cudaMemcpy(tr.data(), g->sh[0].d_trace, tr.size() * 8, cudaMemcpyDeviceToHost));
+    fprintf(stderr, "bucket trace (us since kernel start):");
     for (int i = 1; i < 64 && tr[i]; ++i) fprintf(stderr, " %.2f", (tr[i] - tr[0]) * 1e-3);
     fprintf(stderr, "\n");
+    // per-CTA span of the last pull step (start, end relative to kernel start)
+    double smin = 1e30, smax = 0, emin = 1e30, emax = 0, dsum = 0;
+    int nc = 0;
+    for (int c = 0; c < 1024 && tr[64 + 2 * c]; ++c, ++nc) {
+      const double a = (tr[64 + 2 * c] - tr[0]) * 1e-3, b = (tr[64 + 2 * c + 1] - tr[0]) * 1e-3;
+      smin = std::min(smin, a); smax = std::max(smax, a);
+      emin = std::min(emin, b); emax = std::max(emax, b);
+      dsum += b - a;
+    }
+    if (nc) fprintf(stderr, "pull per CTA (%d): start %.2f..%.2f end %.2f..%.2f mean %.2f us\n", nc, smin,
+                    smax, emin, emax, dsum / nc);
   }
   if (st) {
     st->transfer_in_s = g->transfer_in_s;

@@ -171,6 +171,32 @@ __global__ void __launch_bounds__(256, 2) slice_kernel(const uint8_t* __restrict
   if (acc == 0x12345678u) out[0] = acc;
 }
 
+// The bucket pull's access pattern: `nrows` rows of `rowbytes` each, at the
+// given row indices of a large matrix, split as one contiguous item range per
+// CTA (16 B items, 8 in flight per thread); in-kernel span like stream_kernel.
+__global__ void __launch_bounds__(256, 2) rows_kernel(const uint8_t* __restrict__ m, const uint32_t* rows,
+                                                      uint32_t nrows, uint32_t rowbytes, uint32_t* out) {
+  if (threadIdx.x == 0) atomicMin(&g_t[0], (unsigned long long)gtimer());
+  const uint32_t cpr = rowbytes / 16, total = nrows * cpr;
+  const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
+  const uint32_t lo = min(total, blockIdx.x * per), hi = min(total, lo + per);
+  uint32_t acc = 0;
+  for (uint32_t i0 = lo + threadIdx.x; i0 < hi; i0 += 256 * 8) {
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t i = i0 + k * 256;
+      v[k] = i < hi ? __ldg(reinterpret_cast<const uint4*>(m + (size_t)rows[i / cpr] * rowbytes) + i % cpr)
+                    : make_uint4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) acc = min(acc ^ v[k].x, v[k].y ^ v[k].z ^ v[k].w);
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) atomicMax(&g_t[1], (unsigned long long)gtimer());
+}
+
 int main() {
   int sms = 0;
   CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
@@ -264,6 +290,35 @@ int main() {
       const double bytes = (double)rows * rowbytes;
       printf("{\"bench\": \"slice\", \"col_blocks\": %u, \"slice_bytes\": %u, \"us\": %.1f, \"GBps\": %.0f}\n",
              nb, rowbytes / nb, best * 1e3, bytes / (best * 1e-3) / 1e9);
+    }
+  }
+  {
+    // 1073 rows of 32 KB: contiguous block vs random rows of a 1 GiB matrix
+    const uint32_t nrows = 1073, rowbytes = 32768;
+    uint32_t h[1073];
+    uint32_t* drows;
+    CK(cudaMalloc(&drows, sizeof(h)));
+    for (int variant = 0; variant < 2; ++variant) {
+      uint64_t x = 88172645463325252ull;
+      for (uint32_t i = 0; i < nrows; ++i) {
+        x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+        h[i] = variant ? (uint32_t)(x % 32768) : i;
+      }
+      CK(cudaMemcpy(drows, h, sizeof(h), cudaMemcpyHostToDevice));
+      uint64_t best = ~0ull;
+      for (int it = 0; it < 8; ++it) {
+        stream_kernel<8, false><<<296, 256, 0>>>((const uint4*)(buf + (512ull << 20)), (256ull << 20) / 16, (uint32_t*)out);
+        unsigned long long init[2] = {~0ull, 0ull};
+        CK(cudaMemcpyToSymbol(g_t, init, 16));
+        rows_kernel<<<256, 256>>>(buf, drows, nrows, rowbytes, (uint32_t*)out);
+        CK(cudaDeviceSynchronize());
+        unsigned long long t[2];
+        CK(cudaMemcpyFromSymbol(t, g_t, 16));
+        if (t[1] - t[0] < best) best = t[1] - t[0];
+      }
+      printf("{\"bench\": \"rows\", \"rows\": \"%s\", \"bytes\": %u, \"us\": %.2f, \"GBps\": %.0f}\n",
+             variant ? "random of 32768 (1 GiB)" : "contiguous", nrows * rowbytes, best * 1e-3,
+             (double)nrows * rowbytes / (best * 1e-9) / 1e9);
     }
   }
   printf("{\"bench\": \"info\", \"sms\": %d}\n", sms);
