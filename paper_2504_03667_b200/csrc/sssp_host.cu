@@ -580,6 +580,8 @@ int plan_bucket(sssp_graph* g) {
   if (!(exact && shape)) return SSSP_OK;
   void* fn = bucket_fn(g->wbytes);
   uint32_t T = 128 / g->wbytes;
+  if (const char* e = getenv("SSSP_BUCKET_TILE_BYTES"))  // tuning experiments: bytes of each row per CTA
+    T = std::max<uint32_t>(32, (uint32_t)atoi(e) / g->wbytes);
   while (true) {
     if (T > s0.row_stride) T = (uint32_t)s0.row_stride;
     g->bT = T;
