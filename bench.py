@@ -330,6 +330,22 @@ def main():
             r1 = sdg.solve(args.source)
             assert r1 == res0, "scan engine != default engine"
         sdg.close()
+        # per-round latency histogram (%globaltimer at every round end; one
+        # extra traced solve, outside the timed region)
+        if world == 1:
+            with P.DeviceGraph(g, (local_rank,), flags=args.flags, engine="cluster",
+                               round_times=True) as tdg:
+                tdg.solve(args.source)
+                d = np.diff(tdg.round_times().astype(np.int64)) / 1e3  # us
+            edges = [0, 0.3, 0.4, 0.5, 0.6, 0.8, 1.0, 2.0, 5.0, float("inf")]
+            hist, _ = np.histogram(d, bins=edges)
+            scan["round_latency_us"] = {
+                "rounds": int(d.size + 1), "p50": round(float(np.percentile(d, 50)), 4),
+                "p90": round(float(np.percentile(d, 90)), 4),
+                "p99": round(float(np.percentile(d, 99)), 4), "max": round(float(d.max()), 3),
+                "mean": round(float(d.mean()), 4),
+                "histogram": {f"{a}-{b}": int(c) for a, b, c in zip(edges[:-1], edges[1:], hist)},
+                "note": "%globaltimer deltas between consecutive round ends (CTA 0 of the cluster)"}
 
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,

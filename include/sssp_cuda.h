@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define SSSP_ABI_VERSION 1
+#define SSSP_ABI_VERSION 2 /* 2: sssp_options.record_round_times, sssp_solve_dataparallel, sssp_round_times */
 #define SSSP_IPC_HANDLE_BYTES 64 /* sizeof(cudaIpcMemHandle_t) */
 #define SSSP_MAX_SHARDS 8
 
@@ -75,6 +75,8 @@ typedef struct {
   int64_t global_min_weight; /* shard mode: smallest finite off-diagonal weight of the WHOLE
                                 graph (sssp_block_weight_range + an allreduce), -1 = unknown;
                                 the bucket engine needs it >= 1 on every rank */
+  int record_round_times; /* scan engines: %globaltimer at the end of every round of the
+                             last solve (sssp_round_times; SURVEY §8d latency histogram) */
 } sssp_options;
 
 #define SSSP_FLAGS_DEFAULT 3u /* bit2 (4): speculative relax, off by default */
@@ -185,6 +187,11 @@ int sssp_validate(sssp_graph* g, uint64_t source, const uint64_t* dist, const ui
  * stats.classes = pass-number sweeps needed by zero-weight ties (0: none). */
 int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out,
                             uint64_t* pred_out, uint64_t* rounds_out, sssp_solve_stats* st);
+
+/* Per-round %globaltimer stamps (ns) of the last scan-engine solve (needs
+ * record_round_times; source's shard 0): *count = rounds recorded, at most
+ * cap written.  Differences of consecutive stamps = per-round latency. */
+int sssp_round_times(sssp_graph* g, uint64_t* ns_out, uint64_t cap, uint64_t* count);
 
 /* t_sync_min microbenchmark (the roofline's sync term): runs
  * `rounds` exchange rounds with the solve's launch shape and exchange code

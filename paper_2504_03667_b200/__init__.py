@@ -210,8 +210,9 @@ ENGINES = {"auto": 0, "grid": 1, "cluster": 2, "bucket": 3}
 
 def _options(flags: Optional[int], ctas: int, max_batch: int, timeout_ms: int,
              visit_order: bool, replicas: int = 0, engine: str = "auto",
-             warps: int = 0, global_min_weight: int = -1) -> Options:
+             warps: int = 0, global_min_weight: int = -1, round_times: bool = False) -> Options:
     o = Options()
+    o.record_round_times = int(round_times)
     o.global_min_weight = global_min_weight
     o.engine = ENGINES[engine]
     o.warps_per_cta = warps
@@ -233,10 +234,10 @@ class DeviceGraph:
     def __init__(self, g: Graph, devices: Sequence[int] = (0,), *, flags: Optional[int] = None,
                  ctas: int = 0, max_batch: int = 0, timeout_ms: int = 0,
                  visit_order: bool = False, replicas: int = 0, engine: str = "auto",
-                 warps: int = 0):
+                 warps: int = 0, round_times: bool = False):
         self.n = g.n
         self._opt = _options(flags, ctas, max_batch, timeout_ms, visit_order, replicas, engine,
-                             warps)
+                             warps, round_times=round_times)
         devs = (ctypes.c_int * len(devices))(*devices)
         h = ctypes.c_void_p()
         check(lib.sssp_graph_create(_p64(g.adj), g.n, int(g.directed), devs, len(devices),
@@ -351,6 +352,14 @@ class DeviceGraph:
         check(lib.sssp_validate(self._h, r.source, _p64(d), _p64(p), ctypes.byref(out)),
               "sssp_validate")
         return out.value
+
+    def round_times(self) -> np.ndarray:
+        """Per-round %globaltimer stamps (ns) of the last scan-engine solve
+        (needs ``round_times=True``); np.diff gives the per-round latency."""
+        out = np.empty(self.n, dtype=np.uint64)
+        cnt = ctypes.c_uint64()
+        check(lib.sssp_round_times(self._h, _p64(out), self.n, ctypes.byref(cnt)), "sssp_round_times")
+        return out[: cnt.value].copy()
 
     def probe_sync(self, rounds: int = 20000) -> float:
         """Seconds per exchange round of the solve's own launch shape (t_sync_min)."""

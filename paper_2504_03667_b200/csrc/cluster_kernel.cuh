@@ -310,6 +310,8 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
       ++iters;
       if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
         p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
+      if (p.round_ns != nullptr && solve == 0 && p.shard == 0 && q == 0 && lane == 0)
+        p.round_ns[iters - 1] = globaltimer();  // per-round latency trace (optional)
       // ---- speculate on the next round: runner-up of the last exchange
       spec_u = 0xFFFFFFFFu;
       const uint64_t r2 = next_key(best_key);
@@ -409,6 +411,8 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
       ++iters;
       if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
         p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
+      if (p.round_ns != nullptr && solve == 0 && p.shard == 0 && q == 0 && lane == 0)
+        p.round_ns[iters - 1] = globaltimer();  // per-round latency trace (optional)
 
       // ---- warp election (serial.hpp:42-48)
       uint32_t bd, bs;
@@ -604,6 +608,8 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_hier_kernel(const ScanPara
     ++iters;
     if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
       p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
+    if (p.round_ns != nullptr && solve == 0 && p.shard == 0 && q == 0 && lane == 0)
+      p.round_ns[iters - 1] = globaltimer();  // per-round latency trace (optional)
 
     // ---- warp election, then the CTA minimum through shared memory
     ++E;

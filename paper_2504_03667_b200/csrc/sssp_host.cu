@@ -177,6 +177,7 @@ struct Shard {
   uint64_t* d_info = nullptr;
   uint32_t* d_sources = nullptr;
   uint32_t* d_visit = nullptr;
+  uint64_t* d_round_ns = nullptr;  // [n] per-round stamps (record_round_times, shard 0)
   uint32_t* h_sources = nullptr;  // pinned
   uint64_t* h_info = nullptr;     // pinned
   uint64_t* peer[kMaxShards] = {};
@@ -456,6 +457,10 @@ int alloc_state(sssp_graph* g, Shard& s) {
   CK(cudaHostAlloc(&s.h_info, B * 4 * sizeof(uint64_t), cudaHostAllocDefault));
   if (g->opt.record_visit_order && s.k == 0)
     CK(cudaMalloc(&s.d_visit, B * g->n * sizeof(uint32_t)));
+  if (g->opt.record_round_times && s.k == 0) {
+    CK(cudaMalloc(&s.d_round_ns, g->n * sizeof(uint64_t)));
+    CK(cudaMemset(s.d_round_ns, 0, g->n * sizeof(uint64_t)));
+  }
   return SSSP_OK;
 }
 
@@ -573,6 +578,7 @@ int plan_bucket(sssp_graph* g) {
   const bool exact = g->min_w >= 1;
   const Shard& s0 = g->sh[0];
   const bool shape = g->cluster && g->n > 1 && !g->opt.record_visit_order &&
+                     !g->opt.record_round_times &&
                      !(s0.G & (s0.G - 1)) && !(s0.L & (s0.L - 1));
   if (want == SSSP_ENGINE_BUCKET && !(exact && shape))
     return fail(SSSP_ERR_UNSUPPORTED, exact ? "bucket engine needs the cluster layout"
@@ -747,6 +753,7 @@ void destroy_graph(sssp_graph* g) {
     cudaFree(s.d_info);
     cudaFree(s.d_sources);
     cudaFree(s.d_visit);
+    cudaFree(s.d_round_ns);
     pool_free(s, s.d_adjT);
     if (s.stream) cudaStreamSynchronize(s.stream);
     cudaFree(s.d_info2);
@@ -916,6 +923,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
     p.dist_out = s.d_dist;
     p.pred_out = s.d_pred;
     p.visit_order = s.d_visit;
+    p.round_ns = s.d_round_ns;
     p.info = s.d_info;
     p.timeout_ns = g->opt.timeout_ms * 1000000ull;
     if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
@@ -1710,6 +1718,24 @@ int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, 
     st->engine = SSSP_ENGINE_DATAPARALLEL;
     st->classes = (uint32_t)(flag ? info[2] : 0);  // pass-number sweeps (0: none needed)
   }
+  return SSSP_OK;
+}
+
+int sssp_round_times(sssp_graph* g, uint64_t* ns_out, uint64_t cap, uint64_t* count) {
+  if (!g || !count) return fail(SSSP_ERR_BAD_ARG, "null argument");
+  if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
+  Shard* s0 = nullptr;
+  for (auto& s : g->sh)
+    if (s.d_round_ns) s0 = &s;
+  if (!s0) return fail(SSSP_ERR_BAD_ARG, "record_round_times was not set (or not shard 0)");
+  CK(cudaSetDevice(s0->device));
+  std::vector<uint64_t> t(g->n);
+  CK(cudaMemcpy(t.data(), s0->d_round_ns, g->n * 8, cudaMemcpyDeviceToHost));
+  uint64_t k = 0;
+  while (k < g->n && t[k] != 0) ++k;
+  *count = k;
+  if (ns_out) std::copy(t.begin(), t.begin() + std::min(k, cap), ns_out);
+  CK(cudaMemset(s0->d_round_ns, 0, g->n * 8));  // the next solve records afresh
   return SSSP_OK;
 }
 

@@ -364,3 +364,19 @@ def test_hierarchical_cluster_variant(gpu, oracle_c, warps, P):
         d, p = serial(oracle_c, g, s)
         with gpu.DeviceGraph(g, [0] * P, engine="cluster", flags=3 | 8, warps=warps) as dg:
             assert_same(dg.solve(s), d, p, f"hier n={n} warps={warps} P={P}")
+
+
+def test_round_times_trace(gpu, oracle_c):
+    # per-round %globaltimer stamps of the n-round kernel; tracing
+    # must not change the result, and AUTO stays on a scan engine with it
+    g = gpu.generate_dense(3000, 77)
+    d, p = oracle_c.serial(g.adj, g.n, 5)
+    with gpu.DeviceGraph(g, round_times=True) as dg:
+        r = dg.solve(5)
+        t = dg.round_times()
+        assert r.stats["engine"] in (1, 2)
+        assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p)
+        assert len(t) == r.stats["iterations"] == g.n
+        assert np.all(np.diff(t.astype(np.int64)) > 0)
+        r2 = dg.solve(6)  # stamps restart for every solve
+        assert len(dg.round_times()) == r2.stats["iterations"]
