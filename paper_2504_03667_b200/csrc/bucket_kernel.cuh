@@ -293,13 +293,11 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   // without a barrier (every CTA knows the source): dist = w(s,v), pred = s
   // for each finite w, exactly the serial engine's first round.
   const uint32_t vbase = p.shard * p.loc_n;
-  for (uint32_t i = tid; i < TW; i += kBucketThreads) {
-    uint32_t m = 0;
-    for (uint32_t b = 0; b < 32; ++b) {
-      const uint32_t vl = pos_to_vid(p0 + i * 32 + b, p.Q, p.lbits, p.qbits);
-      if (vl >= p.loc_n || vbase + vl >= p.n || vbase + vl == p.source) m |= 1u << b;
-    }
-    ssettled[i] = m;
+  for (uint32_t i = warp; i < TW; i += kBucketThreads / 32) {  // one ballot per bitmap word
+    const uint32_t vl = pos_to_vid(p0 + i * 32 + lane, p.Q, p.lbits, p.qbits);
+    const uint32_t m =
+        __ballot_sync(0xFFFFFFFFu, vl >= p.loc_n || vbase + vl >= p.n || vbase + vl == p.source);
+    if (lane == 0) ssettled[i] = m;
   }
   for (uint32_t i = tid; i < T; i += kBucketThreads) {
     const uint32_t vl = pos_to_vid(p0 + i, p.Q, p.lbits, p.qbits);

@@ -165,3 +165,18 @@ def test_device_build_config1_and_shards(gpu, oracle_c):
         with gpu.DeviceGraph.from_edges(1000, e, False, devs) as dg:
             r = dg.solve(0)
         assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p)
+
+
+@pytest.mark.parametrize("tile_bytes", [256, 512, 1024])
+def test_bucket_tile_sizes(gpu, oracle_c, tile_bytes, monkeypatch):
+    # wider tiles (fewer CTAs, more positions per CTA): push slices of 16 B
+    # per thread over more row groups, more pulled columns per CTA range
+    monkeypatch.setenv("SSSP_BUCKET_TILE_BYTES", str(tile_bytes))
+    rng = np.random.default_rng(tile_bytes)
+    for directed in (False, True):
+        g = gpu.Graph(1500, directed, rand_graph(rng, 1500, 1, 9, 0.3, directed).ravel())
+        info, _ = check(gpu, oracle_c, g, 11, engine="bucket")
+        assert info["engine"] == 3
+    g = gpu.generate_dense(4096, 4096)
+    info, _ = check(gpu, oracle_c, g, 0, engine="bucket")
+    assert info["engine"] == 3
