@@ -42,6 +42,8 @@ namespace sssp_b200 {
 // g = j*row_stride + p, i.e. vertex j*loc_n + vid(p).  Tiles are numbered
 // globally (shard j, CTA c) -> j*G + c.  With one shard this is the plain
 // position order.
+constexpr int kBucketMaxSlots = 8;
+
 struct BucketParams {
   const void* adj;      // [n rows][row_stride]: this shard's columns, positions
   const void* adjT;     // PULL source (nullptr: push only); row r, global positions
@@ -53,7 +55,6 @@ struct BucketParams {
   uint32_t Q, L;        // layout: position p = q*L + s  <->  local vertex s*Q + q
   uint32_t qbits, lbits;
   uint32_t T;           // positions per CTA
-  uint32_t source;      // global vertex id
   uint32_t nshards, shard, loc_n;
   uint32_t* peer_bitmap[kMaxShards];  // every shard's [2][nshards*row_stride/32] (self incl.)
   uint32_t* peer_ctrl[kMaxShards];    // every shard's [2][3][nshards*G]: tile lmin, cand, uns
@@ -69,6 +70,14 @@ struct BucketParams {
   uint64_t* info2;      // [2]: barriers used, error
   uint64_t* trace;      // optional [64]: %globaltimer after every barrier (CTA 0 of shard 0)
   uint64_t seq;         // launch tag: a watchdog failure writes it to info2[1] (no reset needed)
+  // Independent solves sharing one launch (one shard only): the grid is
+  // nslots x tiles CTAs, slot s solves from slot_src[s] with its own exchange
+  // region (slot_bytes apart) and its own outputs (out_stride / info strides).
+  uint32_t nslots;
+  uint32_t slot_src[kBucketMaxSlots];
+  uint64_t slot_bytes;
+  uint64_t out_stride;
+  uint32_t* done;       // [kBucketMaxSlots] per-slot done flags (nslots > 1)
 };
 
 __device__ __forceinline__ uint32_t pos_to_vid(uint32_t pos, uint32_t Q, uint32_t lbits,
@@ -162,7 +171,9 @@ constexpr int kBucketChunk = kBucketThreads * 32 * 2;  // ids of one pass over 5
 // counts.  After the barrier every CTA derives d = min(lmin); the candidates
 // of the tiles with lmin == d form B_d -- no second barrier is needed to
 // build the class.
-template <typename W>
+// MULTI: several independent solves (slots) share the launch; the single-solve
+// instance compiles the slot bookkeeping away.
+template <typename W, bool MULTI>
 __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketParams p) {
   namespace cg = cooperative_groups;
   using KT = BucketKey<W>;
@@ -172,7 +183,16 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   constexpr int CPT = 16 / (int)sizeof(W);  // columns per thread (one 16 B load)
 
   extern __shared__ __align__(16) uint32_t smem[];
-  const uint32_t T = p.T, G = gridDim.x * p.nshards;  // G = tiles of ALL shards
+  // slot (independent solve) of this CTA and its tile within the slot
+  const uint32_t Gs = MULTI ? gridDim.x / p.nslots : gridDim.x;
+  const uint32_t slot = MULTI ? blockIdx.x / Gs : 0u, bx = blockIdx.x - slot * Gs;
+  auto at = [&](auto* ptr) {  // this slot's copy of an exchange-region array
+    return reinterpret_cast<decltype(ptr)>(reinterpret_cast<char*>(const_cast<void*>(
+                                               static_cast<const void*>(ptr))) + slot * p.slot_bytes);
+  };
+  const uint32_t source = p.slot_src[slot];
+  uint32_t* const ubm = at(p.ubm);
+  const uint32_t T = p.T, G = Gs * p.nshards;  // G = tiles of ALL shards
   const uint32_t TW = T / 32;  // bitmap words per tile
   const uint32_t lwords = (uint32_t)(p.row_stride / 32);
   const uint32_t words = lwords * p.nshards;  // global bitmap words
@@ -189,17 +209,17 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   __shared__ uint32_t s_cnt[2];
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t me = p.shard * gridDim.x + blockIdx.x;  // global tile id
-  const uint32_t p0 = blockIdx.x * T;                    // first LOCAL position of the tile
+  const uint32_t me = p.shard * Gs + bx;  // global tile id
+  const uint32_t p0 = bx * T;             // first LOCAL position of the tile
   const uint32_t tbits = 31u - __clz(T);  // T is a power of two
   const W* adj = static_cast<const W*>(p.adj);
   const W* adjT = static_cast<const W*>(p.adjT);
   const uint32_t TPR = T * sizeof(W) / 16;  // threads per row slice
   const uint32_t RG = kBucketThreads / TPR; // row groups
   // global per-step arrays: ctrl = [2][3][G] (lmin, candidates, unsettled)
-  uint32_t* const glob = p.peer_ctrl[p.shard];
-  const uint32_t* const gbm = p.peer_bitmap[p.shard];
-  K* const pkey = static_cast<K*>(p.pkey);
+  uint32_t* const glob = at(p.peer_ctrl[p.shard]);
+  const uint32_t* const gbm = at(p.peer_bitmap[p.shard]);
+  K* const pkey = at(static_cast<K*>(p.pkey));
   // global position -> global vertex id
   auto gvid = [&](uint32_t g) -> uint32_t {
     const uint32_t j = g >> (p.qbits + p.lbits);  // row_stride = Q*L = 2^(qbits+lbits)
@@ -208,7 +228,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
 
   uint32_t ntr = 0;
   auto stamp = [&]() {
-    if (p.trace && me == 0 && tid == 0 && ntr < 64) p.trace[ntr++] = globaltimer();
+    if (p.trace && me == 0 && slot == 0 && tid == 0 && ntr < 64) p.trace[ntr++] = globaltimer();
   };
   // One barrier over every CTA of every shard: the cooperative grid barrier
   // with one shard (1.29 us at 256 CTAs, the fastest measured variant:
@@ -239,7 +259,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
           if (v >= target) break;
           if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) {
             s_fail = 1;
-            p.info2[1] = p.seq;
+            p.info2[slot * 2 + 1] = p.seq + slot;
             break;
           }
         }
@@ -271,16 +291,16 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       const uint32_t cm =
           __ballot_sync(0xFFFFFFFFu, m != DINF && !((sm >> lane) & 1u) && sdist[i * 32 + lane] == m);
       if (lane < p.nshards)  // remote shards: P2P stores
-        p.peer_bitmap[lane][par * words + me * TW + i] = cm;
+        at(p.peer_bitmap[lane])[par * words + me * TW + i] = cm;
       if (lane == 31) {
-        p.ubm[par * lwords + blockIdx.x * TW + i] = ~sm;  // local only (pull work list)
+        ubm[par * lwords + bx * TW + i] = ~sm;  // local only (pull work list)
         if (cm) atomicAdd(&s_cnt[0], __popc(cm));
       }
     }
     for (uint32_t col = tid; col < T; col += kBucketThreads) pkey[p0 + col] = KT::kNone;
     __syncthreads();
     if (tid < p.nshards) {
-      uint32_t* c = p.peer_ctrl[tid];
+      uint32_t* c = at(p.peer_ctrl[tid]);
       c[(par * 3 + 0) * G + me] = m;
       c[(par * 3 + 1) * G + me] = s_cnt[0];
       c[(par * 3 + 2) * G + me] = s_cnt[1];
@@ -296,16 +316,16 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   for (uint32_t i = warp; i < TW; i += kBucketThreads / 32) {  // one ballot per bitmap word
     const uint32_t vl = pos_to_vid(p0 + i * 32 + lane, p.Q, p.lbits, p.qbits);
     const uint32_t m =
-        __ballot_sync(0xFFFFFFFFu, vl >= p.loc_n || vbase + vl >= p.n || vbase + vl == p.source);
+        __ballot_sync(0xFFFFFFFFu, vl >= p.loc_n || vbase + vl >= p.n || vbase + vl == source);
     if (lane == 0) ssettled[i] = m;
   }
   for (uint32_t i = tid; i < T; i += kBucketThreads) {
     const uint32_t vl = pos_to_vid(p0 + i, p.Q, p.lbits, p.qbits);
     const bool real = vl < p.loc_n && vbase + vl < p.n;
-    const uint32_t w = real ? (uint32_t)adj[(size_t)p.source * p.row_stride + p0 + i] : WINF;
-    const bool src = real && vbase + vl == p.source;
+    const uint32_t w = real ? (uint32_t)adj[(size_t)source * p.row_stride + p0 + i] : WINF;
+    const bool src = real && vbase + vl == source;
     sdist[i] = src ? 0u : (w != WINF ? w : DINF);
-    spred[i] = (!src && w != WINF) ? p.source : 0xFFFFFFFFu;
+    spred[i] = (!src && w != WINF) ? source : 0xFFFFFFFFu;
   }
   __syncthreads();
   // Buffer parity = parity of the barrier that follows the publish, counted
@@ -313,78 +333,92 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   // launch then publishes into the buffer the slow shard is NOT reading after
   // its final barrier, and a step's extra (pull) barrier never lets a publish
   // overwrite a buffer some CTA may still read.
+  if (MULTI && bx == 0 && tid == 0) p.done[slot] = 0;  // read after the first barrier
   publish((uint32_t)(bar_base & 1ull));
   barrier();
   stamp();
 
+  bool done = false;  // this slot's solve has settled every reachable vertex
   uint64_t pushed = 1, pulled = 0, settled = 1;
   uint32_t step = 1;
   while (!failed) {
     const uint32_t par = (uint32_t)((bar_base + nbar - 1) & 1ull);
-    // ---- the class: d = min over tiles, B_d = candidates of the tiles at d.
-    // One memory round trip: every tile's (lmin, candidates, unsettled) and
-    // the whole candidate bitmap are loaded together, then reduced in smem.
-    {
-      const uint32_t* bm = gbm + par * words;
-      for (uint32_t i = tid; i < words; i += kBucketThreads) sbm[i] = __ldcg(&bm[i]);
-      // this shard's published unsettled bitmap, staged for a pull step
-      const uint32_t* ub = p.ubm + par * lwords;
-      for (uint32_t i = tid; i < lwords; i += kBucketThreads) sub[i] = __ldcg(&ub[i]);
-    }
-    uint32_t lm_r[4], cc_r[4], uu_r[4];  // G <= 4 * kBucketThreads tiles (host-checked)
+    bool relax = false, pull = false;
+    uint32_t dk = 0, bcount = 0, ucount = 0;
+    if (!done) {
+      // ---- the class: d = min over tiles, B_d = candidates of the tiles at d.
+      // One memory round trip: every tile's (lmin, candidates, unsettled) and
+      // the whole candidate bitmap are loaded together, then reduced in smem.
+      {
+        const uint32_t* bm = gbm + par * words;
+        for (uint32_t i = tid; i < words; i += kBucketThreads) sbm[i] = __ldcg(&bm[i]);
+        // this shard's published unsettled bitmap, staged for a pull step
+        const uint32_t* ub = ubm + par * lwords;
+        for (uint32_t i = tid; i < lwords; i += kBucketThreads) sub[i] = __ldcg(&ub[i]);
+      }
+      uint32_t lm_r[4], cc_r[4], uu_r[4];  // G <= 4 * kBucketThreads tiles (host-checked)
 #pragma unroll
-    for (int k2 = 0; k2 < 4; ++k2) {
-      const uint32_t c = tid + k2 * kBucketThreads;
-      lm_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 0) * G + c]) : DINF;
-      cc_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 1) * G + c]) : 0u;
-      uu_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 2) * G + c]) : 0u;
-    }
-    uint32_t d = DINF;
+      for (int k2 = 0; k2 < 4; ++k2) {
+        const uint32_t c = tid + k2 * kBucketThreads;
+        lm_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 0) * G + c]) : DINF;
+        cc_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 1) * G + c]) : 0u;
+        uu_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 2) * G + c]) : 0u;
+      }
+      uint32_t d = DINF;
 #pragma unroll
-    for (int k2 = 0; k2 < 4; ++k2) {
-      const uint32_t c = tid + k2 * kBucketThreads;
-      if (c < G) slmin[c] = lm_r[k2];
-      d = min(d, lm_r[k2]);
-    }
-    d = __reduce_min_sync(0xFFFFFFFFu, d);
-    if (lane == 0) s_red[warp] = d;
-    __syncthreads();
-    for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) d = min(d, s_red[w2]);
-    if (d == DINF) break;  // uniform: every CTA reads the same values
-    uint32_t bcount = 0, uns = 0;
+      for (int k2 = 0; k2 < 4; ++k2) {
+        const uint32_t c = tid + k2 * kBucketThreads;
+        if (c < G) slmin[c] = lm_r[k2];
+        d = min(d, lm_r[k2]);
+      }
+      d = __reduce_min_sync(0xFFFFFFFFu, d);
+      if (lane == 0) s_red[warp] = d;
+      __syncthreads();
+      for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) d = min(d, s_red[w2]);
+      if (d == DINF) {  // uniform within the slot: every CTA reads the same values
+        done = true;
+      } else {
+        uint32_t uns = 0;
 #pragma unroll
-    for (int k2 = 0; k2 < 4; ++k2) {
-      bcount += lm_r[k2] == d ? cc_r[k2] : 0u;
-      uns += uu_r[k2];
+        for (int k2 = 0; k2 < 4; ++k2) {
+          bcount += lm_r[k2] == d ? cc_r[k2] : 0u;
+          uns += uu_r[k2];
+        }
+        bcount = __reduce_add_sync(0xFFFFFFFFu, bcount);
+        uns = __reduce_add_sync(0xFFFFFFFFu, uns);
+        if (lane == 0) {
+          s_red2[warp] = bcount;
+          s_red3[warp] = uns;
+        }
+        // mask the staged bitmap to the tiles at d
+        for (uint32_t i = tid; i < words; i += kBucketThreads)
+          if (slmin[i >> (tbits - 5)] != d) sbm[i] = 0u;  // TW = T/32 words per tile
+        __syncthreads();
+        bcount = 0;
+        uns = 0;
+        for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) {
+          bcount += s_red2[w2];
+          uns += s_red3[w2];
+        }
+        ucount = uns - bcount;  // unsettled after settling B_d
+        // settle my candidates if my tile is in the class
+        for (uint32_t i = tid; i < TW; i += kBucketThreads) ssettled[i] |= sbm[me * TW + i];
+        __syncthreads();
+        stamp();
+        ++step;
+        settled += bcount;
+        if (ucount == 0) {
+          done = true;  // nothing left to relax (the last class needs no rows)
+        } else {
+          relax = true;
+          pull = adjT != nullptr && ucount < bcount;
+          dk = d;
+        }
+      }
     }
-    bcount = __reduce_add_sync(0xFFFFFFFFu, bcount);
-    uns = __reduce_add_sync(0xFFFFFFFFu, uns);
-    if (lane == 0) {
-      s_red2[warp] = bcount;
-      s_red3[warp] = uns;
-    }
-    // mask the staged bitmap to the tiles at d
-    for (uint32_t i = tid; i < words; i += kBucketThreads)
-      if (slmin[i >> (tbits - 5)] != d) sbm[i] = 0u;  // TW = T/32 words per tile
-    __syncthreads();
-    bcount = 0;
-    uns = 0;
-    for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) {
-      bcount += s_red2[w2];
-      uns += s_red3[w2];
-    }
-    const uint32_t ucount = uns - bcount;  // unsettled after settling B_d
-    // settle my candidates if my tile is in the class
-    for (uint32_t i = tid; i < TW; i += kBucketThreads) ssettled[i] |= sbm[me * TW + i];
-    __syncthreads();
-    stamp();
-    ++step;
-    settled += bcount;
-    if (ucount == 0) break;  // nothing left to relax (the last class needs no rows)
-    const bool pull = adjT != nullptr && ucount < bcount;
-    const uint32_t dk = d;
+    if (!MULTI && done) break;
 
-    if (!pull) {
+    if (relax && !pull) {
       // ---- PUSH: stream the rows of B_d (ascending ids), per-column min key
       pushed += bcount;
       const uint32_t rg = tid / TPR, ct = tid - rg * TPR;  // row group, column thread
@@ -468,7 +502,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         }
       }
       __syncthreads();
-    } else {
+    } else if (relax && pull) {
       // ---- PULL, balanced over the whole shard: U = this shard's unsettled
       // columns after B_d (the published unsettled bitmaps minus the class).
       // The (column of U, 16 B chunk of its transposed row) items are split
@@ -510,8 +544,8 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       const bool cpow2 = (cpr & (cpr - 1u)) == 0;  // uniform: shifts instead of divisions
       const uint32_t cbits = 31u - __clz(cpr);
       const uint32_t total = nuL * cpr;
-      const uint32_t per = (total + gridDim.x - 1) / gridDim.x;
-      const uint32_t lo = min(total, blockIdx.x * per), hi = min(total, lo + per);
+      const uint32_t per = (total + Gs - 1) / Gs;
+      const uint32_t lo = min(total, bx * per), hi = min(total, lo + per);
       const uint32_t r0 = cpow2 ? lo >> cbits : lo / cpr;
       const uint32_t ncols = lo < hi ? (cpow2 ? (hi - 1) >> cbits : (hi - 1) / cpr) - r0 + 1 : 0;
       if (ncols && base < r0 + ncols && base + c > r0) {
@@ -523,8 +557,8 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       for (uint32_t i = tid; i < ncols; i += kBucketThreads) sk[i] = KT::kNone;
       __syncthreads();
       stamp();
-      if (p.trace && tid == 0 && p.shard == 0 && blockIdx.x < 1024)  // per-CTA pull span (debug)
-        p.trace[64 + 2 * blockIdx.x] = globaltimer();
+      if (p.trace && tid == 0 && p.shard == 0 && slot == 0 && bx < 1024)  // per-CTA pull span (debug)
+        p.trace[64 + 2 * bx] = globaltimer();
       // Two-stage cp.async pipeline: a thread's items are lo + tid + k*256;
       // batch b+1's 16 B chunks stream into the thread's stage slots while
       // batch b is consumed.  (column rank, chunk) pairs are walked
@@ -632,11 +666,17 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       __syncthreads();
       for (uint32_t i = tid; i < ncols; i += kBucketThreads)
         if (sk[i] != KT::kNone) smem_min(&pkey[scol[i]], sk[i]);
-      if (p.trace && tid == 0 && p.shard == 0 && blockIdx.x < 1024)
-        p.trace[64 + 2 * blockIdx.x + 1] = globaltimer();
+      if (p.trace && tid == 0 && p.shard == 0 && slot == 0 && bx < 1024)
+        p.trace[64 + 2 * bx + 1] = globaltimer();
+    }
+    // the pull's extra barrier (every partial minimum is in pkey); with
+    // several slots every step has it, so all CTAs count the same barriers
+    if (pull || MULTI) {
       stamp();
-      barrier();  // every partial minimum is in pkey
+      barrier();
       stamp();
+    }
+    if (relax && pull) {
       for (uint32_t col = tid; col < T; col += kBucketThreads) {
         if ((ssettled[col >> 5] >> (col & 31)) & 1u) continue;
         const K k = ld_cg(&pkey[p0 + col]);
@@ -651,27 +691,37 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       __syncthreads();
     }
     // ---- publish the next class's candidates, one barrier per class
-    stamp();
-    publish((uint32_t)((bar_base + nbar) & 1ull));
+    if (!done) {
+      stamp();
+      publish((uint32_t)((bar_base + nbar) & 1ull));
+    } else if (MULTI && bx == 0 && tid == 0) {
+      p.done[slot] = 1;  // read by every slot after the barrier
+    }
     barrier();
     stamp();
+    if (MULTI) {  // all slots done: leave together (uniform)
+      bool all = true;
+      for (uint32_t s2 = 0; s2 < p.nslots; ++s2) all &= __ldcg(&p.done[s2]) != 0;
+      if (all) break;
+    }
   }
 
   // ---- write back (positions -> local vertex ids)
   for (uint32_t i = tid; i < T; i += kBucketThreads) {
     const uint32_t v = pos_to_vid(p0 + i, p.Q, p.lbits, p.qbits);
     if (v < p.loc_n && vbase + v < p.n) {
-      p.dist_out[v] = sdist[i] == DINF ? ~0ull : (uint64_t)sdist[i];
-      p.pred_out[v] = spred[i] == 0xFFFFFFFFu ? ~0ull : (uint64_t)spred[i];
+      p.dist_out[slot * p.out_stride + v] = sdist[i] == DINF ? ~0ull : (uint64_t)sdist[i];
+      p.pred_out[slot * p.out_stride + v] = spred[i] == 0xFFFFFFFFu ? ~0ull : (uint64_t)spred[i];
     }
   }
   stamp();
-  if (blockIdx.x == 0 && tid == 0) {
-    p.info[0] = settled;
-    p.info[1] = step;
-    p.info[2] = pushed;
-    p.info[3] = pulled;
-    p.info2[0] = nbar;
+  if (bx == 0 && tid == 0) {
+    uint64_t* const info = p.info + slot * 4;
+    info[0] = settled;
+    info[1] = step;
+    info[2] = pushed;
+    info[3] = pulled;
+    p.info2[slot * 2] = nbar;
     if (p.nshards > 1) *p.bar_epoch = bar_base + nbar;  // every CTA read it before barrier 1
   }
 }

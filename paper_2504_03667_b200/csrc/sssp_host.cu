@@ -209,6 +209,8 @@ struct sssp_graph {
   // bucket engine layout (identical on every shard)
   uint32_t bT = 0, bG = 0;               // positions per CTA, CTAs per shard
   uint64_t bseq = 0;                     // bucket launch tags (watchdog reports)
+  uint32_t bslots = 1;                   // bucket: independent solves per launch (one shard)
+  uint64_t done_off = 0;                 // bucket: per-slot done flags (after the slot regions)
   uint64_t slots_bytes = 0;              // scan-engine exchange region (start of d_slots)
   uint64_t bar_off = 0, epoch_off = 0, ctrl_off = 0, bm_off = 0, ubm_off = 0, pkey_off = 0,
            region_bytes = 0;
@@ -444,7 +446,7 @@ int alloc_state(sssp_graph* g, Shard& s) {
   CK(cudaSetDevice(s.device));
   const uint64_t B = g->max_batch;
   g->slots_bytes = (B * g->slot_stride * sizeof(uint64_t) + 255) & ~255ull;
-  const uint64_t bytes = g->slots_bytes + (g->bucket ? g->region_bytes : 0);
+  const uint64_t bytes = g->slots_bytes + (g->bucket ? g->region_bytes * g->bslots + 256 : 0);
   CK(cudaMalloc(&s.d_slots, bytes));
   CK(cudaMemset(s.d_slots, 0, bytes));
   CK(cudaMalloc(&s.d_info2, B * 2 * sizeof(uint64_t)));
@@ -556,9 +558,12 @@ int compute_max_batch(sssp_graph* g) {
   return SSSP_OK;
 }
 
-void* bucket_fn(uint32_t wbytes) {
-  return wbytes == 1 ? (void*)bucket_kernel<uint8_t>
-         : wbytes == 2 ? (void*)bucket_kernel<uint16_t> : (void*)bucket_kernel<uint32_t>;
+void* bucket_fn(uint32_t wbytes, bool multi = false) {
+  if (multi)
+    return wbytes == 1 ? (void*)bucket_kernel<uint8_t, true>
+           : wbytes == 2 ? (void*)bucket_kernel<uint16_t, true> : (void*)bucket_kernel<uint32_t, true>;
+  return wbytes == 1 ? (void*)bucket_kernel<uint8_t, false>
+         : wbytes == 2 ? (void*)bucket_kernel<uint16_t, false> : (void*)bucket_kernel<uint32_t, false>;
 }
 
 size_t bucket_smem(const sssp_graph* g) {
@@ -595,18 +600,29 @@ int plan_bucket(sssp_graph* g) {
     const size_t smem = bucket_smem(g);
     bool fits = T * g->wbytes / 16 <= kBucketThreads && smem <= 200 * 1024 &&
                 (uint64_t)g->bG * g->P <= 4ull * kBucketThreads;  // kernel: 4 tiles per thread
+    uint64_t capacity = 0;  // co-resident CTAs of this kernel on one device
     for (const auto& s : g->sh) {
       if (!fits) break;
       CK(cudaSetDevice(s.device));
       CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      CK(cudaFuncSetAttribute(bucket_fn(g->wbytes, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
       uint32_t same = 0;
       for (const auto& t : g->sh) same += t.device == s.device ? 1 : 0;
       int per_sm = 0, sms = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kBucketThreads, smem));
       CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s.device));
       fits = per_sm > 0 && (uint64_t)g->bG * same <= (uint64_t)per_sm * sms;
+      capacity = (uint64_t)per_sm * sms;
     }
-    if (fits) break;
+    if (fits) {
+      // batches on one shard: as many independent solves per launch as fit
+      // co-resident (config 5: n=16384 -> 128 CTAs per solve, 2 per launch)
+      g->bslots = g->P == 1 ? (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(
+                                  {capacity / g->bG, (uint64_t)kBucketMaxSlots, g->max_batch}))
+                            : 1u;
+      break;
+    }
     if (T * g->wbytes >= 1024 || T >= s0.row_stride) {  // pull: (T + 2) keys + ids fit the combine region
       if (want == SSSP_ENGINE_BUCKET) return fail(SSSP_ERR_UNSUPPORTED, "bucket grid does not fit");
       return SSSP_OK;  // AUTO: stay on the scan engine
@@ -624,6 +640,7 @@ int plan_bucket(sssp_graph* g) {
   g->ubm_off = (g->bm_off + 2 * words * 4 + 255) & ~255ull;
   g->pkey_off = (g->ubm_off + 2 * (s0.row_stride / 32) * 4 + 255) & ~255ull;
   g->region_bytes = (g->pkey_off + s0.row_stride * 8 + 255) & ~255ull;
+  g->done_off = g->region_bytes * g->bslots;  // [kBucketMaxSlots] u32 after the slot regions
   g->bucket = true;
   return SSSP_OK;
 }
@@ -811,10 +828,15 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
       CK(cudaSetDevice(s.device));
       if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
     }
-    for (uint32_t i = 0; i < k; ++i) {
+    for (uint32_t i = 0; i < k; i += g->bslots) {  // solves i .. i+ns-1 share a launch
+      const uint32_t ns = std::min<uint32_t>(g->bslots, k - i);
       for (auto& s : g->sh) {
         CK(cudaSetDevice(s.device));
         BucketParams bp{};
+        bp.nslots = ns;
+        for (uint32_t j = 0; j < ns; ++j) bp.slot_src[j] = (uint32_t)sources[i + j];
+        bp.slot_bytes = g->region_bytes;
+        bp.out_stride = s.loc_n;
         bp.adj = s.d_adj;
         bp.adjT = s.pull_src;
         bp.adjT_by_pos = s.pull_src == s.d_adj ? 0u : 1u;  // transpose rows: local positions
@@ -826,7 +848,6 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.qbits = bitlen(s.G) - 1;
         bp.lbits = bitlen(s.L) - 1;
         bp.T = g->bT;
-        bp.source = (uint32_t)sources[i];
         bp.nshards = g->P;
         bp.shard = s.k;
         bp.loc_n = (uint32_t)s.loc_n;
@@ -841,6 +862,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.bar_epoch = reinterpret_cast<uint64_t*>(own + g->epoch_off);
         bp.ubm = reinterpret_cast<uint32_t*>(own + g->ubm_off);
         bp.pkey = own + g->pkey_off;
+        bp.done = reinterpret_cast<uint32_t*>(own + g->done_off);
         bp.timeout_ns = g->opt.timeout_ms * 1000000ull;
         bp.dist_out = s.d_dist + (uint64_t)i * s.loc_n;
         bp.pred_out = s.d_pred + (uint64_t)i * s.loc_n;
@@ -854,7 +876,8 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.seq = g->bseq + 1 + i;
         void* args[] = {&bp};
         if (g->P == 1) {
-          CK(cudaLaunchCooperativeKernel(fn, dim3(g->bG), dim3(kBucketThreads), args, smem, s.stream));
+          CK(cudaLaunchCooperativeKernel(ns > 1 ? bucket_fn(g->wbytes, true) : fn, dim3(g->bG * ns),
+                                         dim3(kBucketThreads), args, smem, s.stream));
         } else {  // co-residency was checked in plan_bucket; cross-shard barrier in-kernel
           cudaLaunchConfig_t cfg{};
           cfg.gridDim = dim3(g->bG);

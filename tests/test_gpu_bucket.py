@@ -180,3 +180,26 @@ def test_bucket_tile_sizes(gpu, oracle_c, tile_bytes, monkeypatch):
     g = gpu.generate_dense(4096, 4096)
     info, _ = check(gpu, oracle_c, g, 0, engine="bucket")
     assert info["engine"] == 3
+
+
+@pytest.mark.parametrize("directed", [False, True])
+def test_bucket_multislot_batches(gpu, oracle_c, directed):
+    # several independent solves share one launch (slots); sources finish after
+    # different class counts (one isolated, one on a long path), k is not a
+    # multiple of the slot count, and pull steps occur in some slots only
+    rng = np.random.default_rng(77 + directed)
+    n = 1200
+    adj = rand_graph(rng, n, 1, 30, 0.05, directed)
+    adj[7, :] = INF
+    adj[:, 7] = INF
+    adj[7, 7] = 0  # vertex 7 isolated: its solve ends after class 0
+    for u in range(100, 140):  # a light path: many classes from vertex 100
+        adj[u, u + 1] = 1
+    g = gpu.Graph(n, directed, adj.ravel())
+    srcs = [0, 7, 100, 5, 999, 3, 100, 42, 1199, 7, 64, 12, 300]
+    with gpu.DeviceGraph(g, engine="bucket") as dg:
+        res = dg.solve_batch(srcs)
+        assert dg.info()["engine"] == 3
+    for s, r in zip(srcs, res):
+        d, p = oracle_c.serial(g.adj, n, s)
+        assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p), s
