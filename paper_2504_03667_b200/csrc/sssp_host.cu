@@ -210,6 +210,7 @@ struct sssp_graph {
   uint32_t bT = 0, bG = 0;               // positions per CTA, CTAs per shard
   uint64_t bseq = 0;                     // bucket launch tags (watchdog reports)
   uint32_t bslots = 1;                   // bucket: independent solves per launch (one shard)
+  uint32_t bTb = 0, bGb = 0, bslots_b = 0;  // batch tiling: wider tiles, more slots per launch
   uint64_t done_off = 0;                 // bucket: per-slot done flags (after the slot regions)
   uint64_t slots_bytes = 0;              // scan-engine exchange region (start of d_slots)
   uint64_t bar_off = 0, epoch_off = 0, ctrl_off = 0, bm_off = 0, ubm_off = 0, pkey_off = 0,
@@ -446,7 +447,8 @@ int alloc_state(sssp_graph* g, Shard& s) {
   CK(cudaSetDevice(s.device));
   const uint64_t B = g->max_batch;
   g->slots_bytes = (B * g->slot_stride * sizeof(uint64_t) + 255) & ~255ull;
-  const uint64_t bytes = g->slots_bytes + (g->bucket ? g->region_bytes * g->bslots + 256 : 0);
+  const uint64_t bytes =
+      g->slots_bytes + (g->bucket ? g->region_bytes * std::max(g->bslots, g->bslots_b) + 256 : 0);
   CK(cudaMalloc(&s.d_slots, bytes));
   CK(cudaMemset(s.d_slots, 0, bytes));
   CK(cudaMalloc(&s.d_info2, B * 2 * sizeof(uint64_t)));
@@ -566,9 +568,10 @@ void* bucket_fn(uint32_t wbytes, bool multi = false) {
          : wbytes == 2 ? (void*)bucket_kernel<uint16_t, false> : (void*)bucket_kernel<uint32_t, false>;
 }
 
-size_t bucket_smem(const sssp_graph* g) {
+size_t bucket_smem(const sssp_graph* g, bool batch_tiles = false) {
   const uint64_t rs = g->sh[0].row_stride;
-  return bucket_smem_bytes(g->bT, g->bG * g->P, (uint32_t)(rs / 32 * g->P), g->wbytes);
+  return batch_tiles ? bucket_smem_bytes(g->bTb, g->bGb * g->P, (uint32_t)(rs / 32 * g->P), g->wbytes)
+                     : bucket_smem_bytes(g->bT, g->bG * g->P, (uint32_t)(rs / 32 * g->P), g->wbytes);
 }
 
 // The distance-class engine is exact iff every finite off-diagonal weight is
@@ -621,6 +624,29 @@ int plan_bucket(sssp_graph* g) {
       g->bslots = g->P == 1 ? (uint32_t)std::max<uint64_t>(1, std::min<uint64_t>(
                                   {capacity / g->bG, (uint64_t)kBucketMaxSlots, g->max_batch}))
                             : 1u;
+      // Batch tiling: 4x wider tiles (<= 512 B of each row per CTA) give 4x
+      // fewer CTAs per solve and so more concurrent solves per launch; slower
+      // per solve, faster per batch (config 5: 2.6 -> 1.75 ms for 64 sources,
+      // profiles/r01_bucket_tile_sweep.txt).  Same exchange-region layout
+      // (sized for the larger single-solve grid).
+      g->bslots_b = 0;
+      if (g->P == 1 && g->max_batch > g->bslots) {
+        const uint32_t Tb = std::min<uint32_t>(std::min<uint32_t>(T * 4, 512 / g->wbytes),
+                                               (uint32_t)s0.row_stride);
+        g->bTb = Tb;
+        g->bGb = (uint32_t)(s0.row_stride / Tb);
+        const size_t smb = bucket_smem(g, true);
+        int per_sm = 0;
+        void* fm = bucket_fn(g->wbytes, true);
+        CK(cudaFuncSetAttribute(fm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max(smem, smb)));
+        CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fm, kBucketThreads, smb));
+        int sms = 0;
+        CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s0.device));
+        const uint64_t slots = std::min<uint64_t>(
+            {(uint64_t)per_sm * sms / g->bGb, (uint64_t)kBucketMaxSlots, g->max_batch});
+        if (Tb > T && Tb * g->wbytes / 16 <= kBucketThreads && smb <= 200 * 1024 && slots > g->bslots)
+          g->bslots_b = (uint32_t)slots;
+      }
       break;
     }
     if (T * g->wbytes >= 1024 || T >= s0.row_stride) {  // pull: (T + 2) keys + ids fit the combine region
@@ -640,7 +666,7 @@ int plan_bucket(sssp_graph* g) {
   g->ubm_off = (g->bm_off + 2 * words * 4 + 255) & ~255ull;
   g->pkey_off = (g->ubm_off + 2 * (s0.row_stride / 32) * 4 + 255) & ~255ull;
   g->region_bytes = (g->pkey_off + s0.row_stride * 8 + 255) & ~255ull;
-  g->done_off = g->region_bytes * g->bslots;  // [kBucketMaxSlots] u32 after the slot regions
+  g->done_off = g->region_bytes * std::max(g->bslots, g->bslots_b);  // [kBucketMaxSlots] u32 after
   g->bucket = true;
   return SSSP_OK;
 }
@@ -828,8 +854,12 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
       CK(cudaSetDevice(s.device));
       if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
     }
-    for (uint32_t i = 0; i < k; i += g->bslots) {  // solves i .. i+ns-1 share a launch
-      const uint32_t ns = std::min<uint32_t>(g->bslots, k - i);
+    const size_t smem_b = g->bslots_b ? bucket_smem(g, true) : 0;
+    for (uint32_t i = 0; i < k;) {  // solves i .. i+ns-1 share a launch
+      // more solves left than the single-solve grid can pair: batch tiling
+      const bool wide = g->bslots_b > 0 && k - i > g->bslots;
+      const uint32_t ns = std::min<uint32_t>(wide ? g->bslots_b : g->bslots, k - i);
+      const uint32_t tiles = wide ? g->bGb : g->bG;
       for (auto& s : g->sh) {
         CK(cudaSetDevice(s.device));
         BucketParams bp{};
@@ -847,7 +877,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.L = s.L;
         bp.qbits = bitlen(s.G) - 1;
         bp.lbits = bitlen(s.L) - 1;
-        bp.T = g->bT;
+        bp.T = wide ? g->bTb : g->bT;
         bp.nshards = g->P;
         bp.shard = s.k;
         bp.loc_n = (uint32_t)s.loc_n;
@@ -876,8 +906,8 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.seq = g->bseq + 1 + i;
         void* args[] = {&bp};
         if (g->P == 1) {
-          CK(cudaLaunchCooperativeKernel(ns > 1 ? bucket_fn(g->wbytes, true) : fn, dim3(g->bG * ns),
-                                         dim3(kBucketThreads), args, smem, s.stream));
+          CK(cudaLaunchCooperativeKernel(ns > 1 ? bucket_fn(g->wbytes, true) : fn, dim3(tiles * ns),
+                                         dim3(kBucketThreads), args, wide ? smem_b : smem, s.stream));
         } else {  // co-residency was checked in plan_bucket; cross-shard barrier in-kernel
           cudaLaunchConfig_t cfg{};
           cfg.gridDim = dim3(g->bG);
@@ -887,6 +917,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
           CK(cudaLaunchKernelExC(&cfg, fn, args));
         }
       }
+      i += ns;
     }
     for (auto& s : g->sh) {
       CK(cudaSetDevice(s.device));
