@@ -208,14 +208,29 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpPar
           if (b * per_batch + rg + m * RG >= tot) break;
           const uint4 v4 = st[m * kBucketThreads + tid];
           const uint32_t wd[4] = {v4.x, v4.y, v4.z, v4.w};
+          // u8 chunks without an INF byte (every chunk of a complete graph):
+          // min(du + w, best) is one PRMT + one VIADDMNMX per weight
+          bool inf_free = false;
+          if constexpr (sizeof(W) == 1) {
+            uint32_t z = 0;
 #pragma unroll
-          for (int j = 0; j < CPT; ++j) {
-            const uint32_t w = dp_weight<W>(wd[(j * sizeof(W)) / 4], j);
-            // min(du + w, best) in one VIADDMNMX; an INF weight gets the base
-            // INF - WINF so its candidate is exactly INF (du + w < 2^32 - 1
-            // for finite operands: host-checked n * max_w)
-            const uint32_t base = w == WINF ? kDpInf - WINF : dum;
-            best[j] = __viaddmin_u32(base, w, best[j]);
+            for (int k2 = 0; k2 < 4; ++k2) z |= (~wd[k2] - 0x01010101u) & wd[k2] & 0x80808080u;
+            inf_free = z == 0;  // no byte == 0xFF (haszero(~x))
+          }
+          if (inf_free) {
+#pragma unroll
+            for (int j = 0; j < CPT; ++j)
+              best[j] = __viaddmin_u32(dum, dp_weight<W>(wd[(j * sizeof(W)) / 4], j), best[j]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < CPT; ++j) {
+              const uint32_t w = dp_weight<W>(wd[(j * sizeof(W)) / 4], j);
+              // min(du + w, best) in one VIADDMNMX; an INF weight gets the base
+              // INF - WINF so its candidate is exactly INF (du + w < 2^32 - 1
+              // for finite operands: host-checked n * max_w)
+              const uint32_t base = w == WINF ? kDpInf - WINF : dum;
+              best[j] = __viaddmin_u32(base, w, best[j]);
+            }
           }
         }
       }
