@@ -75,8 +75,9 @@ typedef struct {
   int64_t global_min_weight; /* shard mode: smallest finite off-diagonal weight of the WHOLE
                                 graph (sssp_block_weight_range + an allreduce), -1 = unknown;
                                 the bucket engine needs it >= 1 on every rank */
-  int record_round_times; /* scan engines: %globaltimer at the end of every round of the
-                             last solve (sssp_round_times; SURVEY §8d latency histogram) */
+  int record_round_times; /* cluster engine: %globaltimer at the end of every round of the
+                             last solve (sssp_round_times; SURVEY §8d latency histogram);
+                             runs a traced kernel instance, the untraced one is unchanged */
 } sssp_options;
 
 #define SSSP_FLAGS_DEFAULT 3u /* bit2 (4): speculative relax, off by default */

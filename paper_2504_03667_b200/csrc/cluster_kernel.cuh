@@ -73,7 +73,10 @@ __device__ __forceinline__ uint64_t ld_smem_pair(uint32_t addr, uint64_t& hi) {
 // The +1 keeps the encoding monotone; finite keys stay below 2^32 - 2^SB.
 // Without PACKED, dist and a visited mask are kept apart and the election is
 // a 2-stage redux (dist, then slot).
-template <typename W, int EPL, int NW, bool PACKED>
+// TRACE: record %globaltimer at every round end (record_round_times); a
+// separate instance because even an untaken trace branch in the round loop
+// cost ~4 % of the solve (18.6 vs 17.85 ms at n=32768)
+template <typename W, int EPL, int NW, bool PACKED, bool TRACE = false>
 __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanParams p) {
   using Row = RowSlice<W, EPL>;
   constexpr int NP = NW / 4;  // key pairs per lane: Q <= 16*NW = 64*NP
@@ -310,8 +313,9 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
       ++iters;
       if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
         p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
-      if (p.round_ns != nullptr && solve == 0 && p.shard == 0 && q == 0 && lane == 0)
-        p.round_ns[iters - 1] = globaltimer();  // per-round latency trace (optional)
+      if constexpr (TRACE)
+        if (p.round_ns != nullptr && solve == 0 && p.shard == 0 && q == 0 && lane == 0)
+          p.round_ns[iters - 1] = globaltimer();  // per-round latency trace
       // ---- speculate on the next round: runner-up of the last exchange
       spec_u = 0xFFFFFFFFu;
       const uint64_t r2 = next_key(best_key);
@@ -411,8 +415,9 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
       ++iters;
       if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
         p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
-      if (p.round_ns != nullptr && solve == 0 && p.shard == 0 && q == 0 && lane == 0)
-        p.round_ns[iters - 1] = globaltimer();  // per-round latency trace (optional)
+      if constexpr (TRACE)
+        if (p.round_ns != nullptr && solve == 0 && p.shard == 0 && q == 0 && lane == 0)
+          p.round_ns[iters - 1] = globaltimer();  // per-round latency trace
 
       // ---- warp election (serial.hpp:42-48)
       uint32_t bd, bs;
@@ -608,8 +613,6 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_hier_kernel(const ScanPara
     ++iters;
     if (p.visit_order != nullptr && p.shard == 0 && q == 0 && lane == 0)
       p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
-    if (p.round_ns != nullptr && solve == 0 && p.shard == 0 && q == 0 && lane == 0)
-      p.round_ns[iters - 1] = globaltimer();  // per-round latency trace (optional)
 
     // ---- warp election, then the CTA minimum through shared memory
     ++E;

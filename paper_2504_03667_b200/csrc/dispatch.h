@@ -14,7 +14,7 @@ KernelFn get_grid_kernel(int wbytes, int epl, int np);
 ProbeFn get_grid_probe(int np);
 
 // cluster engine (cluster_kernel.cuh): one cluster per solve, DSMEM exchange
-KernelFn get_cluster_kernel(int wbytes, int epl, int nw, bool packed);
+KernelFn get_cluster_kernel(int wbytes, int epl, int nw, bool packed, bool trace = false);
 ProbeFn get_cluster_probe(int nw, bool hier);
 // hierarchical cluster variant (CTA pre-reduction, PACKED state only)
 KernelFn get_cluster_hier_kernel(int wbytes, int epl, int nw);

@@ -5,41 +5,42 @@
 namespace sssp_b200 {
 namespace {
 
-template <typename W, int EPL, bool PK>
+template <typename W, int EPL, bool PK, bool TR>
 KernelFn pick_nw(int nw) {
   switch (nw) {
-    case 4: return cluster_scan_kernel<W, EPL, 4, PK>;
-    case 8: return cluster_scan_kernel<W, EPL, 8, PK>;
-    case 16: return cluster_scan_kernel<W, EPL, 16, PK>;
+    case 4: return cluster_scan_kernel<W, EPL, 4, PK, TR>;
+    case 8: return cluster_scan_kernel<W, EPL, 8, PK, TR>;
+    case 16: return cluster_scan_kernel<W, EPL, 16, PK, TR>;
   }
   return nullptr;
 }
 
-template <typename W, bool PK>
+template <typename W, bool PK, bool TR>
 KernelFn pick_epl(int epl, int nw) {
   switch (epl) {
-    case 4: return pick_nw<W, 4, PK>(nw);
-    case 8: return pick_nw<W, 8, PK>(nw);
-    case 16: return pick_nw<W, 16, PK>(nw);
-    case 32: return pick_nw<W, 32, PK>(nw);
+    case 4: return pick_nw<W, 4, PK, TR>(nw);
+    case 8: return pick_nw<W, 8, PK, TR>(nw);
+    case 16: return pick_nw<W, 16, PK, TR>(nw);
+    case 32: return pick_nw<W, 32, PK, TR>(nw);
   }
   return nullptr;
 }
 
-template <bool PK>
+template <bool PK, bool TR>
 KernelFn pick_w(int wbytes, int epl, int nw) {
   switch (wbytes) {
-    case 1: return pick_epl<uint8_t, PK>(epl, nw);
-    case 2: return pick_epl<uint16_t, PK>(epl, nw);
-    case 4: return pick_epl<uint32_t, PK>(epl, nw);
+    case 1: return pick_epl<uint8_t, PK, TR>(epl, nw);
+    case 2: return pick_epl<uint16_t, PK, TR>(epl, nw);
+    case 4: return pick_epl<uint32_t, PK, TR>(epl, nw);
   }
   return nullptr;
 }
 
 }  // namespace
 
-KernelFn get_cluster_kernel(int wbytes, int epl, int nw, bool packed) {
-  return packed ? pick_w<true>(wbytes, epl, nw) : pick_w<false>(wbytes, epl, nw);
+KernelFn get_cluster_kernel(int wbytes, int epl, int nw, bool packed, bool trace) {
+  if (trace) return packed ? pick_w<true, true>(wbytes, epl, nw) : pick_w<false, true>(wbytes, epl, nw);
+  return packed ? pick_w<true, false>(wbytes, epl, nw) : pick_w<false, false>(wbytes, epl, nw);
 }
 
 ProbeFn get_cluster_probe(int nw, bool hier) {

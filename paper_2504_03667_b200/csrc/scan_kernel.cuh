@@ -61,7 +61,7 @@ struct ScanParams {
   uint64_t* dist_out;       // [nsolve][loc_n]
   uint64_t* pred_out;       // [nsolve][loc_n]
   uint32_t* visit_order;    // optional [nsolve][n], shard 0 only
-  uint64_t* round_ns;       // optional [n]: %globaltimer at the end of every round (solve 0, shard 0)
+  uint64_t* round_ns;       // optional [n]: %globaltimer at every round end (cluster engine, TRACE instances)
   uint64_t* info;           // [nsolve][4]: iterations, last exchange, error, mispredicts
                             // (error word is OR-ed by any CTA that times out)
   uint64_t timeout_ns;
@@ -372,8 +372,6 @@ __global__ void __launch_bounds__(32, 1) scan_dijkstra_kernel(const ScanParams p
     ++iters;
     if (p.visit_order != nullptr && p.shard == 0 && c == 0 && lane == 0)
       p.visit_order[(size_t)solve * p.n + (iters - 1)] = u;
-    if (p.round_ns != nullptr && solve == 0 && p.shard == 0 && c == 0 && lane == 0)
-      p.round_ns[iters - 1] = globaltimer();  // per-round latency trace (optional)
 
     // ---- local election over unvisited owned columns (serial.hpp:42-48).
     uint32_t bd, bs;

@@ -10,6 +10,7 @@
 #include <algorithm>
 #include <atomic>
 #include <chrono>
+#include <map>
 #include <mutex>
 #include <cstdio>
 #include <cstdlib>
@@ -491,7 +492,8 @@ int finalize_encoding(sssp_graph* g) {
       s.NP = s.NW / 4;
       s.hier = g->packed && (g->opt.flags & kFlagHier) && s.C <= 16;
       s.fn = s.hier ? get_cluster_hier_kernel((int)g->wbytes, (int)s.EPL, (int)s.NW)
-                    : get_cluster_kernel((int)g->wbytes, (int)s.EPL, (int)s.NW, g->packed != 0);
+                    : get_cluster_kernel((int)g->wbytes, (int)s.EPL, (int)s.NW, g->packed != 0,
+                                         g->opt.record_round_times != 0);
       if (!s.fn) return fail(SSSP_ERR_UNSUPPORTED, "no cluster kernel instance for this layout");
     }
     return SSSP_OK;
@@ -515,6 +517,24 @@ int finalize_encoding(sssp_graph* g) {
 
 // Concurrent solves one launch may hold while keeping every CTA resident
 // (the persistent kernel spins, so all CTAs must be co-resident).
+// Raises (never lowers) a kernel's dynamic shared-memory limit on the current
+// device.  The limit is per function and process-wide: lowering it for one
+// graph would break launches of another graph that needs more
+// (tests/test_gpu_parity.py::test_interleaved_graphs_of_different_sizes).
+cudaError_t raise_smem(const void* fn, size_t bytes) {
+  static std::mutex m;
+  static std::map<std::pair<int, const void*>, size_t> cur;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return e;
+  std::lock_guard<std::mutex> lk(m);
+  size_t& c = cur[{dev, fn}];
+  if (bytes <= c) return cudaSuccess;
+  e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  if (e == cudaSuccess) c = bytes;
+  return e;
+}
+
 int compute_max_batch(sssp_graph* g) {
   uint32_t cap = ~0u;
   for (auto& s : g->sh) {
@@ -525,7 +545,7 @@ int compute_max_batch(sssp_graph* g) {
       if (s.C > 8) CK(cudaFuncSetAttribute(s.fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
       cudaLaunchConfig_t cfg{};
       const size_t dsm = (size_t)s.NW * s.L * 4;
-      CK(cudaFuncSetAttribute(s.fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dsm));
+      CK(raise_smem((const void*)s.fn, dsm));
       cfg.gridDim = dim3(s.C);
       cfg.blockDim = dim3(s.NW * 32);
       cfg.dynamicSmemBytes = dsm;
@@ -607,9 +627,8 @@ int plan_bucket(sssp_graph* g) {
     for (const auto& s : g->sh) {
       if (!fits) break;
       CK(cudaSetDevice(s.device));
-      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      CK(cudaFuncSetAttribute(bucket_fn(g->wbytes, true), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem));
+      CK(raise_smem(fn, smem));
+      CK(raise_smem(bucket_fn(g->wbytes, true), smem));
       uint32_t same = 0;
       for (const auto& t : g->sh) same += t.device == s.device ? 1 : 0;
       int per_sm = 0, sms = 0;
@@ -638,7 +657,7 @@ int plan_bucket(sssp_graph* g) {
         const size_t smb = bucket_smem(g, true);
         int per_sm = 0;
         void* fm = bucket_fn(g->wbytes, true);
-        CK(cudaFuncSetAttribute(fm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)std::max(smem, smb)));
+        CK(raise_smem(fm, std::max(smem, smb)));
         CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fm, kBucketThreads, smb));
         int sms = 0;
         CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, s0.device));
@@ -1671,7 +1690,7 @@ int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, 
     for (void* f : {frelax, fsweep}) {
       if (!fits) break;
       const size_t sm = f == frelax ? sm_relax : sm_tree;
-      CK(cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
+      CK(raise_smem(f, sm));
       int per_sm = 0;
       CK(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, f, kBucketThreads, sm));
       fits = per_sm > 0 && G <= (uint64_t)per_sm * sms;
@@ -1680,8 +1699,8 @@ int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, 
     if (T * wb >= 4096 || T >= rs) return fail(SSSP_ERR_UNSUPPORTED, "dataparallel grid does not fit");
     T *= 2;
   }
-  CK(cudaFuncSetAttribute(ftree, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tree));
-  CK(cudaFuncSetAttribute(ffast, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_tree));
+  CK(raise_smem(ftree, sm_tree));
+  CK(raise_smem(ffast, sm_tree));
   const uint32_t G = (uint32_t)(rs / T);
   const uint32_t max_sweeps = n + 2;
   // scratch: front [2][words] | cnt [2][G] | snap [2][rs] | dist_v [n] | pass_v [n] |

@@ -380,3 +380,21 @@ def test_round_times_trace(gpu, oracle_c):
         assert np.all(np.diff(t.astype(np.int64)) > 0)
         r2 = dg.solve(6)  # stamps restart for every solve
         assert len(dg.round_times()) == r2.stats["iterations"]
+
+
+@pytest.mark.parametrize("engine", ["auto", "cluster"])
+def test_interleaved_graphs_of_different_sizes(gpu, oracle_c, engine):
+    # the per-kernel dynamic shared-memory limit is process-wide: a small graph
+    # created after a large one must not break the large one's launches
+    big = gpu.generate_dense(8192, 5)
+    small = gpu.generate_dense(500, 6)
+    db, pb = oracle_c.serial(big.adj, big.n, 3)
+    ds, ps = oracle_c.serial(small.adj, small.n, 3)
+    with gpu.DeviceGraph(big, engine=engine) as gb:
+        r1 = gb.solve(3)
+        with gpu.DeviceGraph(small, engine=engine) as gs:
+            r2 = gs.solve(3)
+            r3 = gb.solve(3)
+    assert np.array_equal(r1.dist, db) and np.array_equal(r1.pred, pb)
+    assert np.array_equal(r2.dist, ds) and np.array_equal(r2.pred, ps)
+    assert np.array_equal(r3.dist, db) and np.array_equal(r3.pred, pb)
