@@ -179,6 +179,7 @@ struct Shard {
   uint32_t* d_sources = nullptr;
   uint32_t* d_visit = nullptr;
   uint64_t* d_round_ns = nullptr;  // [n] per-round stamps (record_round_times, shard 0)
+  bool slots_pooled = false;       // d_slots from the stream-ordered pool (not IPC-exported)
   uint32_t* h_sources = nullptr;  // pinned
   uint64_t* h_info = nullptr;     // pinned
   uint64_t* peer[kMaxShards] = {};
@@ -292,6 +293,8 @@ struct PinnedStaging {
   }
 };
 PinnedStaging g_staging;
+std::mutex g_pinned_m;
+std::multimap<size_t, void*> g_pinned;  // cached small pinned blocks (pinned_get)
 
 int pool_alloc(struct Shard& s, void** p, size_t bytes);
 
@@ -444,28 +447,60 @@ int upload_shard(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, uint64_
   }
 }
 
+// Small pinned host blocks (launch sources, solve info) cached process-wide:
+// cudaHostAlloc / cudaFreeHost per graph cost milliseconds, sometimes hundreds.
+void* pinned_get(size_t bytes) {
+  std::lock_guard<std::mutex> lk(g_pinned_m);
+  auto it = g_pinned.find(bytes);
+  if (it != g_pinned.end()) {
+    void* p = it->second;
+    g_pinned.erase(it);
+    return p;
+  }
+  void* p = nullptr;
+  return cudaHostAlloc(&p, bytes, cudaHostAllocDefault) == cudaSuccess ? p : nullptr;
+}
+void pinned_put(void* p, size_t bytes) {
+  if (!p) return;
+  std::lock_guard<std::mutex> lk(g_pinned_m);
+  g_pinned.emplace(bytes, p);
+}
+
+// Per-graph device state comes from the stream-ordered pool (cached across
+// graphs: cudaMalloc / cudaFree per graph cost 10-500 ms on the box), except
+// the exchange region of a one-process-per-GPU shard, which is exported by
+// CUDA IPC and so needs a plain cudaMalloc.
 int alloc_state(sssp_graph* g, Shard& s) {
   CK(cudaSetDevice(s.device));
   const uint64_t B = g->max_batch;
   g->slots_bytes = (B * g->slot_stride * sizeof(uint64_t) + 255) & ~255ull;
   const uint64_t bytes =
       g->slots_bytes + (g->bucket ? g->region_bytes * std::max(g->bslots, g->bslots_b) + 256 : 0);
-  CK(cudaMalloc(&s.d_slots, bytes));
-  CK(cudaMemset(s.d_slots, 0, bytes));
-  CK(cudaMalloc(&s.d_info2, B * 2 * sizeof(uint64_t)));
-  CK(cudaMemset(s.d_info2, 0, B * 2 * sizeof(uint64_t)));
-  CK(cudaMalloc(&s.d_dist, B * std::max<uint64_t>(1, s.loc_n) * sizeof(uint64_t)));
-  CK(cudaMalloc(&s.d_pred, B * std::max<uint64_t>(1, s.loc_n) * sizeof(uint64_t)));
-  CK(cudaMalloc(&s.d_info, B * 4 * sizeof(uint64_t)));
-  CK(cudaMalloc(&s.d_sources, B * sizeof(uint32_t)));
-  CK(cudaHostAlloc(&s.h_sources, B * sizeof(uint32_t), cudaHostAllocDefault));
-  CK(cudaHostAlloc(&s.h_info, B * 4 * sizeof(uint64_t), cudaHostAllocDefault));
-  if (g->opt.record_visit_order && s.k == 0)
-    CK(cudaMalloc(&s.d_visit, B * g->n * sizeof(uint32_t)));
-  if (g->opt.record_round_times && s.k == 0) {
-    CK(cudaMalloc(&s.d_round_ns, g->n * sizeof(uint64_t)));
-    CK(cudaMemset(s.d_round_ns, 0, g->n * sizeof(uint64_t)));
+  s.slots_pooled = !g->multiproc;
+  if (s.slots_pooled) {
+    if (pool_alloc(s, (void**)&s.d_slots, bytes)) return SSSP_ERR_OOM;
+  } else {
+    CK(cudaMalloc(&s.d_slots, bytes));
   }
+  CK(cudaMemsetAsync(s.d_slots, 0, bytes, s.stream));
+  void** bufs[] = {(void**)&s.d_info2, (void**)&s.d_dist, (void**)&s.d_pred, (void**)&s.d_info,
+                   (void**)&s.d_sources};
+  const uint64_t cols = std::max<uint64_t>(1, s.loc_n);
+  const uint64_t sizes[] = {B * 2 * sizeof(uint64_t), B * cols * sizeof(uint64_t),
+                            B * cols * sizeof(uint64_t), B * 4 * sizeof(uint64_t), B * sizeof(uint32_t)};
+  for (int i = 0; i < 5; ++i)
+    if (pool_alloc(s, bufs[i], sizes[i])) return SSSP_ERR_OOM;
+  CK(cudaMemsetAsync(s.d_info2, 0, B * 2 * sizeof(uint64_t), s.stream));
+  s.h_sources = static_cast<uint32_t*>(pinned_get(B * sizeof(uint32_t)));
+  s.h_info = static_cast<uint64_t*>(pinned_get(B * 4 * sizeof(uint64_t)));
+  if (!s.h_sources || !s.h_info) return fail(SSSP_ERR_OOM, "pinned host allocation failed");
+  if (g->opt.record_visit_order && s.k == 0)
+    if (pool_alloc(s, (void**)&s.d_visit, B * g->n * sizeof(uint32_t))) return SSSP_ERR_OOM;
+  if (g->opt.record_round_times && s.k == 0) {
+    if (pool_alloc(s, (void**)&s.d_round_ns, g->n * sizeof(uint64_t))) return SSSP_ERR_OOM;
+    CK(cudaMemsetAsync(s.d_round_ns, 0, g->n * sizeof(uint64_t), s.stream));
+  }
+  CK(cudaStreamSynchronize(s.stream));
   return SSSP_OK;
 }
 
@@ -809,19 +844,16 @@ void destroy_graph(sssp_graph* g) {
     for (int j = 0; j < kMaxShards; ++j)
       if (s.peer_ipc[j] && s.peer[j]) cudaIpcCloseMemHandle(s.peer[j]);
     pool_free(s, s.d_adj);
-    cudaFree(s.d_slots);
-    cudaFree(s.d_dist);
-    cudaFree(s.d_pred);
-    cudaFree(s.d_info);
-    cudaFree(s.d_sources);
-    cudaFree(s.d_visit);
-    cudaFree(s.d_round_ns);
-    pool_free(s, s.d_adjT);
+    if (s.slots_pooled) pool_free(s, s.d_slots);
+    else cudaFree(s.d_slots);
+    for (void* p : {(void*)s.d_dist, (void*)s.d_pred, (void*)s.d_info, (void*)s.d_sources,
+                    (void*)s.d_visit, (void*)s.d_round_ns, (void*)s.d_info2, s.d_adjT})
+      pool_free(s, p);
     if (s.stream) cudaStreamSynchronize(s.stream);
-    cudaFree(s.d_info2);
     cudaFree(s.d_trace);
-    if (s.h_sources) cudaFreeHost(s.h_sources);
-    if (s.h_info) cudaFreeHost(s.h_info);
+    const uint64_t B = g->max_batch;
+    pinned_put(s.h_sources, B * sizeof(uint32_t));
+    pinned_put(s.h_info, B * 4 * sizeof(uint64_t));
     if (s.ev0) cudaEventDestroy(s.ev0);
     if (s.ev1) cudaEventDestroy(s.ev1);
     if (s.stream) cudaStreamDestroy(s.stream);
