@@ -788,12 +788,15 @@ __global__ void __launch_bounds__(256) transpose_global_kernel(const W* __restri
 
 // flag = 1 if the stored matrix is not symmetric: compares every element
 // A[vid(p')][p] with its mirror A[vid(p)][p'] (same 64x64 tiling as the
-// transpose, no transpose buffer needed).
+// transpose, no transpose buffer needed; each tile pair once).
 template <typename W>
 __global__ void __launch_bounds__(256) symmetric_check_kernel(const W* __restrict__ a,
                                                               uint64_t row_stride, uint32_t n,
                                                               uint32_t Q, uint32_t qbits,
                                                               uint32_t lbits, uint32_t* flag) {
+  // block (x, y) compares the (y, x) tile with the transpose of the (x, y)
+  // tile, so (y, x) would repeat the comparison: half the blocks exit
+  if (blockIdx.y < blockIdx.x) return;
   __shared__ W tile[64][65];
   const uint32_t pb = blockIdx.x * 64, ppb = blockIdx.y * 64;
   const uint32_t tx = threadIdx.x & 63, ty = threadIdx.x >> 6;
