@@ -347,6 +347,25 @@ def main():
                 "histogram": {f"{a}-{b}": int(c) for a, b, c in zip(edges[:-1], edges[1:], hist)},
                 "note": "%globaltimer deltas between consecutive round ends (CTA 0 of the cluster)"}
 
+    # context for the per-round exchange: a host-driven NCCL
+    # 8-byte min-allreduce, the comparison path the device-initiated P2P
+    # exchange replaces (N > 1 only)
+    nccl_us = None
+    if dist is not None and not os.environ.get("SSSP_BENCH_ONE_GPU"):
+        x = torch.zeros(1, dtype=torch.int64, device="cuda")
+        for _ in range(20):
+            dist.all_reduce(x, op=dist.ReduceOp.MIN)
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        for _ in range(200):
+            dist.all_reduce(x, op=dist.ReduceOp.MIN)
+        e1.record()
+        torch.cuda.synchronize()
+        nccl_us = e0.elapsed_time(e1) / 200 * 1e3
+        if scan is not None:
+            scan["nccl_allreduce_8b_us"] = round(nccl_us, 2)
+
     line = {
         "metric": METRIC, "value": round(ms, 4), "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms, 4),
