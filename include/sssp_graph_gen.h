@@ -38,6 +38,17 @@ int sssp_gen_bernoulli(uint64_t n, uint64_t p_q53, uint64_t seed, int directed,
 int sssp_graph_from_edges(uint64_t n, const uint64_t* edges, uint64_t m, int directed,
                           uint64_t col_begin, uint64_t col_count, uint64_t ld, uint64_t* out);
 
+/* parse_edge_list_text (graph.hpp:126-170) on all host threads: the '<n> <m>'
+ * header then m '<u> <v> <w>' lines ('#' / blank lines skipped, CRLF
+ * tolerated).  Call with edges == NULL to read n and m from the header, then
+ * with a buffer of >= 3*m uint64.  On input the reference rejects, returns
+ * SSSP_ERR_BAD_ARG with *err_line = the reference's ParseError line and err =
+ * its what() text ("line N: ..."), the same first error a sequential scan
+ * reports; *err_line = 0 when only the buffer was too small. */
+int sssp_parse_edge_list(const char* text, uint64_t len, uint64_t* n, uint64_t* m,
+                         uint64_t* edges, uint64_t cap, uint64_t* err_line, char* err,
+                         uint64_t err_cap);
+
 #ifdef __cplusplus
 }
 #endif

@@ -27,7 +27,6 @@ failure raises :class:`SsspError`; nothing falls back to the CPU.
 from __future__ import annotations
 
 import ctypes
-import re
 from dataclasses import dataclass, field
 from typing import Iterable, Optional, Sequence
 
@@ -120,59 +119,29 @@ def graph_from_edges(n: int, edges: Iterable[Sequence[int]], directed: bool) -> 
     return Graph(n, directed, out)
 
 
-_INT_RE = re.compile(r"-?[0-9]+\Z")
-
-
-def _parse_int(tok: str, line: int, what: str) -> int:
-    """std::from_chars into long long (graph.hpp:104-111)."""
-    if not _INT_RE.match(tok) or not -(1 << 63) <= int(tok) < (1 << 63):
-        raise ParseError(line, f"malformed {what} '{tok}'")
-    return int(tok)
-
-
 def parse_edge_list(text: str, directed: bool) -> Graph:
     """graph.hpp:126-174: ``n m`` header then m ``u v w`` lines; '#' and blank
-    lines skipped; CRLF tolerated.  ``directed`` is the CLI's ``-w`` switch."""
-    n = m = None
-    edges = []
-    lines = text.split("\n")
-    if lines and lines[-1] == "":
-        lines.pop()  # std::getline yields no final empty line
-    for line_no, raw in enumerate(lines, start=1):
-        line = raw.lstrip(" \t").rstrip(" \t\r")
-        if not line or line.startswith("#"):
-            continue
-        fields = [f for f in re.split(r"[ \t]+", line) if f]
-        if n is None:
-            if len(fields) != 2:
-                raise ParseError(line_no, "expected header '<n> <m>'")
-            n = _parse_int(fields[0], line_no, "vertex count")
-            m = _parse_int(fields[1], line_no, "edge count")
-            if n < 0 or m < 0:
-                raise ParseError(line_no, "negative header value")
-            continue
-        if len(fields) != 3:
-            raise ParseError(line_no, "expected '<u> <v> <w>'")
-        u = _parse_int(fields[0], line_no, "vertex id")
-        v = _parse_int(fields[1], line_no, "vertex id")
-        w = _parse_int(fields[2], line_no, "weight")
-        if u < 0 or v < 0 or u >= n or v >= n:
-            raise ParseError(line_no, "vertex id out of range")
-        if u == v:
-            raise ParseError(line_no, "self-loop")
-        if w < 0:
-            raise ParseError(line_no, "negative weight")
-        if w > MAX_WEIGHT:
-            raise ParseError(line_no, "weight out of range")
-        if len(edges) == m:
-            raise ParseError(line_no, "more edges than declared in header")
-        edges.append((u, v, w))
-    line_no = len(lines)
-    if n is None:
-        raise ParseError(line_no, "missing header")
-    if len(edges) != m:
-        raise ParseError(line_no, f"expected {m} edges, found {len(edges)}")
-    return graph_from_edges(n, edges, directed)
+    lines skipped; CRLF tolerated.  ``directed`` is the CLI's ``-w`` switch.
+    Parsed by the library on all host threads (sssp_parse_edge_list), with the
+    reference's first error (ParseError line and message)."""
+    data = text.encode() if isinstance(text, str) else bytes(text)
+    n = ctypes.c_uint64()
+    m = ctypes.c_uint64()
+    line = ctypes.c_uint64()
+    err = ctypes.create_string_buffer(512)
+    rc = lib.sssp_parse_edge_list(data, len(data), ctypes.byref(n), ctypes.byref(m), None, 0,
+                                  ctypes.byref(line), err, len(err))
+    if rc == 0:
+        edges = np.empty(3 * m.value, dtype=np.uint64)
+        rc = lib.sssp_parse_edge_list(data, len(data), ctypes.byref(n), ctypes.byref(m),
+                                      _p64(edges), m.value, ctypes.byref(line), err, len(err))
+    if rc != 0:
+        if line.value:
+            msg = err.value.decode()
+            pe = ParseError(line.value, msg.split(": ", 1)[1] if ": " in msg else msg)
+            raise pe
+        check(rc, "sssp_parse_edge_list")
+    return graph_from_edges(n.value, edges.reshape(-1, 3), directed)
 
 
 def _gen(fn, n: int, *args, directed: bool, cols: Optional[tuple] = None) -> np.ndarray:

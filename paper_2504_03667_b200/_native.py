@@ -30,7 +30,7 @@ EXPORTED = (
     "sssp_graph_create", "sssp_graph_create_from_edges", "sssp_shard_create", "sssp_shard_export", "sssp_shard_connect",
     "sssp_shard_range", "sssp_graph_destroy", "sssp_graph_info", "sssp_solve",
     "sssp_solve_batch", "sssp_enqueue", "sssp_finish", "sssp_stream",
-    "sssp_probe_sync", "sssp_validate", "sssp_solve_dataparallel", "sssp_round_times", "sssp_block_weight_range", "sssp_gen_dense", "sssp_gen_sparse", "sssp_gen_bernoulli", "sssp_graph_from_edges",
+    "sssp_probe_sync", "sssp_validate", "sssp_solve_dataparallel", "sssp_round_times", "sssp_block_weight_range", "sssp_gen_dense", "sssp_gen_sparse", "sssp_gen_bernoulli", "sssp_graph_from_edges", "sssp_parse_edge_list",
 )
 
 
@@ -116,6 +116,9 @@ def _load() -> ctypes.CDLL:
         "sssp_round_times": (ctypes.c_int, [_vp, _u64p, ctypes.c_uint64, _u64p]),
         "sssp_block_weight_range": (ctypes.c_int, [_u64p, ctypes.c_uint64, ctypes.c_uint64,
                                                    ctypes.c_uint64, ctypes.c_uint64, _u64p, _u64p]),
+        "sssp_parse_edge_list": (ctypes.c_int, [ctypes.c_char_p, ctypes.c_uint64, _u64p, _u64p, _u64p,
+                                                 ctypes.c_uint64, _u64p, ctypes.c_char_p,
+                                                 ctypes.c_uint64]),
         "sssp_gen_dense": (ctypes.c_int, [ctypes.c_uint64, ctypes.c_uint64, ctypes.c_int,
                                           ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                                           _u64p]),

@@ -92,3 +92,45 @@ def test_parse_edge_list_four_vertex(ref):
         st, n, adj = ref.parse(text, directed)
         assert st == "ok"
         assert np.array_equal(P.parse_edge_list(text, directed).adj, adj)
+
+
+def _random_edge_text(rng, n, m, corrupt):
+    lines = []
+    if rng.random() < 0.3:
+        lines.append("# comment")
+    lines.append(f"{n} {m}")
+    for i in range(m + (1 if corrupt == "extra" else 0) - (1 if corrupt == "fewer" else 0)):
+        u, v = int(rng.integers(0, n)), int(rng.integers(0, n))
+        if u == v:
+            v = (u + 1) % n
+        w = int(rng.integers(0, 1000))
+        sep = "\t" if rng.random() < 0.2 else " "
+        lines.append(f"{u}{sep}{v} {w}" + ("\r" if rng.random() < 0.2 else ""))
+        if rng.random() < 0.1:
+            lines.append("" if rng.random() < 0.5 else "   # note")
+    if corrupt in ("token", "range", "self", "neg", "fields", "big"):
+        k = int(rng.integers(1, len(lines)))
+        lines[k] = {"token": "1 x 3", "range": f"0 {n} 1", "self": "2 2 5", "neg": "0 1 -3",
+                    "fields": "0 1", "big": "0 1 4294967296"}[corrupt]
+    return "\n".join(lines) + ("\n" if rng.random() < 0.7 else "")
+
+
+@pytest.mark.parametrize("seed", range(4))
+def test_native_parser_matches_reference(ref, seed):
+    # sssp_parse_edge_list splits the body over all host threads; the first
+    # error (line, message) and the matrix must equal the sequential reference
+    rng = np.random.default_rng(900 + seed)
+    kinds = [None, "extra", "fewer", "token", "range", "self", "neg", "fields", "big"]
+    for i in range(60):
+        n = int(rng.integers(3, 40))
+        m = int(rng.integers(0, 300))
+        text = _random_edge_text(rng, n, m, kinds[i % len(kinds)])
+        for directed in (False, True):
+            want = ref.parse(text, directed)
+            if want[0] == "ok":
+                g = P.parse_edge_list(text, directed)
+                assert g.n == want[1] and np.array_equal(g.adj, want[2]), (i, directed)
+            else:
+                with pytest.raises(P.ParseError) as ei:
+                    P.parse_edge_list(text, directed)
+                assert ei.value.line == want[1] and str(ei.value) == want[2], (i, text)
