@@ -10,6 +10,7 @@
 //   dijkstra_serial(g, s, c, &vo)    serial.hpp:26   sssp::cuda::dijkstra(g, s, &vo)
 //   dijkstra_partitioned(g, s, p)    partitioned:184 sssp::cuda::dijkstra_partitioned(g, s, devices)
 //   dijkstra_dataparallel(g, s)      dataparallel:302 sssp::cuda::dijkstra_dataparallel(g, s)
+//   parse_edge_list_text(in)         graph.hpp:126   sssp::cuda::parse_edge_list_text(text)
 //   (repeated solves on one graph)                   sssp::cuda::DeviceGraph
 //
 // Results are bit-identical to dijkstra_serial (dist AND pred), so
@@ -22,6 +23,7 @@
 #include <cstdint>
 #include <stdexcept>
 #include <string>
+#include <string_view>
 #include <utility>
 #include <vector>
 
@@ -29,6 +31,7 @@
 #include "sssp/result.hpp"
 #include "sssp/weight.hpp"
 #include "sssp_cuda.h"
+#include "sssp_graph_gen.h"
 
 namespace sssp::cuda {
 
@@ -154,6 +157,32 @@ class DeviceGraph {
   sssp_graph* h_ = nullptr;
   std::size_t n_ = 0;
 };
+
+// parse_edge_list_text (graph.hpp:126-170) on all host threads: same EdgeList,
+// same ParseError (line and message) for input the reference rejects.
+inline EdgeList parse_edge_list_text(std::string_view text) {
+  std::uint64_t n = 0, m = 0, line = 0;
+  char err[512] = {};
+  int rc = sssp_parse_edge_list(text.data(), text.size(), &n, &m, nullptr, 0, &line, err, sizeof(err));
+  std::vector<std::uint64_t> e;
+  if (rc == SSSP_OK) {
+    e.resize(3 * m);
+    rc = sssp_parse_edge_list(text.data(), text.size(), &n, &m, e.data(), m, &line, err, sizeof(err));
+  }
+  if (rc != SSSP_OK) {
+    if (line) {
+      const std::string msg(err);
+      const std::size_t k = msg.find(": ");
+      throw ParseError(line, k == std::string::npos ? msg : msg.substr(k + 2));
+    }
+    check(rc, "sssp_parse_edge_list");
+  }
+  EdgeList el;
+  el.n = n;
+  el.edges.resize(m);
+  for (std::uint64_t i = 0; i < m; ++i) el.edges[i] = {e[3 * i], e[3 * i + 1], e[3 * i + 2]};
+  return el;
+}
 
 // Drop-in for dijkstra_serial(g, source) (serial.hpp:65-68).
 inline ShortestPathResult dijkstra(const Graph& g, VertexId source,

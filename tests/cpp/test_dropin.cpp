@@ -81,6 +81,23 @@ int main() {
     }
     EXPECT(t2);
   }
+  // the multi-threaded parser: same EdgeList, same ParseError as graph.hpp:126-170
+  {
+    const char* texts[] = {"# c\n4 2\r\n0 1 5\r\n\n2 3 7 \n", "3 1\n0 1 1\n1 2 1\n", "3 2\n0 1 1\n",
+                           "3 1\n1 1 4\n", "3 1\n0 x 4\n", "5 6\n0 1 4\n1 2 1\n0 2 9\n2 3 2\n3 4 1\n0 1 3\n"};
+    for (const char* t : texts) {
+      std::istringstream in(t);
+      std::string want_err, got_err;
+      EdgeList want, got;
+      try { want = parse_edge_list_text(in); } catch (const ParseError& e) { want_err = e.what(); }
+      try { got = cuda::parse_edge_list_text(t); } catch (const ParseError& e) { got_err = e.what(); }
+      EXPECT(want_err == got_err);
+      EXPECT(want.n == got.n && want.edges.size() == got.edges.size());
+      for (std::size_t i = 0; i < want.edges.size() && i < got.edges.size(); ++i)
+        EXPECT(want.edges[i].u == got.edges[i].u && want.edges[i].v == got.edges[i].v &&
+               want.edges[i].w == got.edges[i].w);
+    }
+  }
   // device-side build from the reference's own parsed EdgeList (-w off and on)
   {
     std::istringstream in("5 6\n0 1 4\n1 2 1\n0 2 9\n2 3 2\n3 4 1\n0 1 3\n");
