@@ -293,6 +293,30 @@ int main() {
     }
   }
   {
+    // bare 35 MB stream, 256 CTAs, with the bucket kernel's 92 KB of dynamic
+    // smem per CTA (L1 left for in-flight loads) vs none; in-kernel span
+    CK(cudaFuncSetAttribute(stream_kernel<8, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    CK(cudaFuncSetAttribute(stream_kernel<8, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    const uint64_t bytes = 1073ull * 32768;
+    for (int cgv = 0; cgv < 2; ++cgv)
+      for (size_t smem : {(size_t)0, (size_t)92 * 1024}) {
+        uint64_t best = ~0ull;
+        for (int it = 0; it < 8; ++it) {
+          stream_kernel<8, false><<<296, 256, 0>>>((const uint4*)(buf + (512ull << 20)), (256ull << 20) / 16, (uint32_t*)out);
+          unsigned long long init[2] = {~0ull, 0ull};
+          CK(cudaMemcpyToSymbol(g_t, init, 16));
+          if (cgv) stream_kernel<8, true><<<256, 256, smem>>>((const uint4*)buf, bytes / 16, (uint32_t*)out);
+          else stream_kernel<8, false><<<256, 256, smem>>>((const uint4*)buf, bytes / 16, (uint32_t*)out);
+          CK(cudaDeviceSynchronize());
+          unsigned long long t[2];
+          CK(cudaMemcpyFromSymbol(t, g_t, 16));
+          if (t[1] - t[0] < best) best = t[1] - t[0];
+        }
+        printf("{\"bench\": \"stream_smem\", \"load\": \"%s\", \"smem_kb\": %zu, \"us\": %.2f, \"GBps\": %.0f}\n",
+               cgv ? "ld.cg" : "ld.nc", smem / 1024, best * 1e-3, bytes / (best * 1e-9) / 1e9);
+      }
+  }
+  {
     // 1073 rows of 32 KB: contiguous block vs random rows of a 1 GiB matrix
     const uint32_t nrows = 1073, rowbytes = 32768;
     uint32_t h[1073];
