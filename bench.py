@@ -425,6 +425,31 @@ def main():
                                     "sample": "one full dijkstra_serial solve of the same graph "
                                               "(oracle/_ref, reference headers)",
                                     "parity": "dist and pred bit-identical"}
+    else:
+        # ---- e2e at N GPUs: the collective dijkstra_distributed call -- every
+        # rank uploads its host column block (narrow + H2D + permute), the
+        # shards connect (IPC handles), solve, owned slices gathered to every
+        # rank; wall time per call, max over ranks
+        from paper_2504_03667_b200 import distributed as D
+        e2e = []
+        for i in range(args.e2e_steps + 1):
+            dist.barrier()
+            torch.cuda.synchronize()
+            t = time.perf_counter()
+            r = D.dijkstra_distributed(block, n, args.source, 100, local_rank)
+            torch.cuda.synchronize()
+            dt = torch.tensor([time.perf_counter() - t], dtype=torch.float64)
+            if dist.get_backend() == "nccl":
+                dt = dt.cuda()
+            dist.all_reduce(dt, op=dist.ReduceOp.MAX)
+            e2e.append(float(dt.item()))
+        e2e_ms = 1e3 * float(np.mean(e2e[1:])) if len(e2e) > 1 else 1e3 * e2e[0]
+        line["e2e"] = {"value": round(e2e_ms, 3), "unit": "ms",
+                       "h2d_bytes_per_step": int(n * loc_cols * wb * world),
+                       "d2h_bytes_per_step": int(16 * n),
+                       "note": "collective dijkstra_distributed: every rank narrows and uploads its "
+                               "uint64 column block, connects, solves, gathers the owned slices; "
+                               "max over ranks"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if dist is not None:
