@@ -179,6 +179,7 @@ def main():
     ap.add_argument("--warps", type=int, default=0)
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-batch", action="store_true", help="skip the config-5 batch object")
     ap.add_argument("--ref-skip-partitioned", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
@@ -347,6 +348,39 @@ def main():
                 "histogram": {f"{a}-{b}": int(c) for a, b, c in zip(edges[:-1], edges[1:], hist)},
                 "note": "%globaltimer deltas between consecutive round ends (CTA 0 of the cluster)"}
 
+    # ---- BASELINE config 5 beside it: 64 sources 256*k on the config-2 graph
+    # (n=16384 Bernoulli 0.5), sources split across ranks, one full replica
+    # per GPU, no cross-GPU traffic; device ms for all 64 (max over ranks)
+    batch = None
+    if not args.no_batch:
+        gb = P.generate_bernoulli(16384, 0.5, 16384)
+        srcs = [256 * k for k in range(64)][rank::world]
+        with P.DeviceGraph(gb, (local_rank,)) as bdg:
+            bstream = torch.cuda.ExternalStream(bdg.stream_ptr())
+            for _ in range(2):
+                bdg.enqueue(srcs)
+                bdg.finish()
+            if dist is not None:
+                dist.barrier()
+            torch.cuda.synchronize()
+            b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            b0.record(bstream)
+            bdg.enqueue(srcs)
+            b1.record(bstream)
+            bst = bdg.finish()
+            torch.cuda.synchronize()
+            bms = b0.elapsed_time(b1)
+        if dist is not None:
+            t = torch.tensor([bms], dtype=torch.float64, device="cuda")
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            bms = float(t[0])
+        batch = {"workload": "config 5: 64 sources 256*k, generate_bernoulli(16384, 0.5, 16384), "
+                             "sources split over the GPUs, one replica each",
+                 "ms_all_sources": round(bms, 4), "ms_per_source": round(bms / 64, 5),
+                 "sources_per_gpu": len(srcs), "engine": ENG[bst["engine"]],
+                 "scaling": "strong (64 sources in total)"}
+        del gb
+
     # context for the per-round exchange: a host-driven NCCL
     # 8-byte min-allreduce, the comparison path the device-initiated P2P
     # exchange replaces (N > 1 only)
@@ -390,6 +424,7 @@ def main():
                              "rows; scan: n rows)"},
         "scan_engine": scan,
         "dataparallel_engine": dp,
+        "batch": batch,
         "clocks": clocks,
         "build_s": round(t_build, 2), "transfer_in_s": round(transfer_in_s, 4),
     }
