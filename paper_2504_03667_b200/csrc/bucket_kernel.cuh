@@ -425,16 +425,21 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       K best[CPT];
 #pragma unroll
       for (int j = 0; j < CPT; ++j) best[j] = KT::kNone;
-      // enumerate B_d in ascending order: each pass takes 2 bitmap words per
-      // thread (<= kBucketChunk ids) with one block scan
-      constexpr uint32_t WPT = 2;
-      for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads * WPT) {
-        const uint32_t w0 = wbase + tid * WPT;
-        uint32_t bw[WPT];
+      // enumerate B_d in ascending order with one block scan per pass: a
+      // class that fits the id chunk takes a single pass over all words (up
+      // to 8 per thread), otherwise passes of 2 words per thread (<=
+      // kBucketChunk ids each)
+      constexpr uint32_t WMAX = 8;
+      const uint32_t wpt = (bcount <= (uint32_t)kBucketChunk && words <= WMAX * kBucketThreads)
+                               ? (words + kBucketThreads - 1) / kBucketThreads
+                               : 2u;
+      for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads * wpt) {
+        const uint32_t w0 = wbase + tid * wpt;
+        uint32_t bw[WMAX];
         uint32_t c = 0;
 #pragma unroll
-        for (uint32_t k2 = 0; k2 < WPT; ++k2) {
-          bw[k2] = w0 + k2 < words ? sbm[w0 + k2] : 0u;
+        for (uint32_t k2 = 0; k2 < WMAX; ++k2) {
+          bw[k2] = k2 < wpt && w0 + k2 < words ? sbm[w0 + k2] : 0u;
           c += __popc(bw[k2]);
         }
         if (!__syncthreads_or(c != 0)) continue;
@@ -453,7 +458,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         }
         uint32_t o = wofs + incl - c;
 #pragma unroll
-        for (uint32_t k2 = 0; k2 < WPT; ++k2)
+        for (uint32_t k2 = 0; k2 < WMAX; ++k2)
           for (uint32_t m = bw[k2]; m; m &= m - 1)
             schunk[o++] = gvid((w0 + k2) * 32 + (__ffs(m) - 1));
         __syncthreads();
