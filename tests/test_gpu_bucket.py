@@ -203,3 +203,22 @@ def test_bucket_multislot_batches(gpu, oracle_c, directed):
     for s, r in zip(srcs, res):
         d, p = oracle_c.serial(g.adj, n, s)
         assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p), s
+
+
+@pytest.mark.parametrize("engine", ["bucket", "auto"])
+def test_long_chain_thousands_of_classes(gpu, oracle_c, engine):
+    # a shuffled chain with sparse shortcuts: distance classes >> n/8, so AUTO
+    # leaves the bucket engine; forced, it must still be exact
+    n = 4099
+    rng = np.random.default_rng(41)
+    adj = np.full((n, n), INF, dtype=np.uint64)
+    order = rng.permutation(n)
+    adj[order[:-1], order[1:]] = rng.integers(1, 4, size=n - 1, dtype=np.uint64)
+    k = n // 8
+    u, v = rng.integers(0, n, size=k), rng.integers(0, n, size=k)
+    adj[u, v] = rng.integers(2, 50, size=k, dtype=np.uint64)
+    np.fill_diagonal(adj, 0)
+    g = gpu.Graph(n, True, adj.ravel())
+    info, _ = check(gpu, oracle_c, g, int(order[0]), engine=engine)
+    if engine == "bucket":
+        assert info["engine"] == 3

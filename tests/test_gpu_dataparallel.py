@@ -109,3 +109,29 @@ def test_config2_full_size(gpu, oracle_c):
     assert np.array_equal(r.dist, sd)
     with gpu.DeviceGraph(g) as dg:
         assert dg.validate(r) == 0
+
+
+@pytest.mark.parametrize("n,density,whi", [(8191, 0.3, 200), (8193, 0.3, 40000), (9001, 0.05, 400_000)])
+def test_ragged_sizes_across_frontier_chunks(gpu, oracle_c, n, density, whi):
+    # frontiers larger than one enumeration chunk (kDpChunk = 8192 vertices)
+    # and row strides that are not a multiple of the 16-byte load width
+    rng = np.random.default_rng(n)
+    g = rand_graph(gpu, rng, n, 1, whi, density, bool(n % 2))
+    check(gpu, oracle_c, g, int(rng.integers(0, n)))
+
+
+def test_long_path_many_rounds(gpu, oracle_c):
+    # a shuffled chain plus sparse shortcuts: over a hundred relaxation rounds with
+    # tiny frontiers, and ties on the shortcuts
+    n = 4099
+    rng = np.random.default_rng(41)
+    adj = np.full((n, n), INF, dtype=np.uint64)
+    order = rng.permutation(n)
+    adj[order[:-1], order[1:]] = rng.integers(1, 4, size=n - 1, dtype=np.uint64)
+    k = n // 8
+    u, v = rng.integers(0, n, size=k), rng.integers(0, n, size=k)
+    adj[u, v] = rng.integers(2, 50, size=k, dtype=np.uint64)
+    np.fill_diagonal(adj, 0)
+    g = gpu.Graph(n, True, adj.ravel())
+    r = check(gpu, oracle_c, g, int(order[0]))
+    assert r.stats["rounds"] > 100
