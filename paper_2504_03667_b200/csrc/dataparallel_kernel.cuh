@@ -144,6 +144,11 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpPar
     uint32_t best[CPT];
 #pragma unroll
     for (int j = 0; j < CPT; ++j) best[j] = kDpInf;
+    // u8 rows whose snapshot distance is below 0xFF00: candidates fit 16 bits,
+    // two columns per VIADDMNMX.U16x2 (lanes j = 2k, 2k + 1; 0xFFFF = none)
+    uint32_t best16[CPT / 2];
+#pragma unroll
+    for (int k = 0; k < CPT / 2; ++k) best16[k] = 0xFFFFFFFFu;
     constexpr uint32_t WPT = 1;
     for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads * WPT) {
       const uint32_t w0 = wbase + tid * WPT;
@@ -217,7 +222,28 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpPar
             for (int k2 = 0; k2 < 4; ++k2) z |= (~wd[k2] - 0x01010101u) & wd[k2] & 0x80808080u;
             inf_free = z == 0;  // no byte == 0xFF (haszero(~x))
           }
-          if (inf_free) {
+          if (sizeof(W) == 1 && inf_free && dum < 0xFF00u) {
+            const uint32_t d2 = dum * 0x10001u;  // du + w <= 0xFEFF + 0xFE < 0xFFFF
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              best16[2 * q] = __viaddmin_u16x2(d2, __byte_perm(wd[q], 0u, 0x4140u), best16[2 * q]);
+              best16[2 * q + 1] = __viaddmin_u16x2(d2, __byte_perm(wd[q], 0u, 0x4342u), best16[2 * q + 1]);
+            }
+          } else if (sizeof(W) == 1 && dum < 0xFF00u) {
+            // INF bytes (0xFF): that lane's addend becomes 0xFF00, so its
+            // candidate is exactly 0xFFFF ("none"); finite ones stay <= 0xFFFD
+            const uint32_t d2 = dum * 0x10001u;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+              const uint32_t y = ~wd[q];
+              const uint32_t ff = ~(((y & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | y) & 0x80808080u;  // byte == 0xFF
+              const uint32_t m0 = (__byte_perm(ff, 0u, 0x4140u) >> 7) * 0xFFFFu;  // lane -> 0xFFFF
+              const uint32_t m1 = (__byte_perm(ff, 0u, 0x4342u) >> 7) * 0xFFFFu;
+              const uint32_t a0 = (d2 & ~m0) | (0xFF00FF00u & m0), a1 = (d2 & ~m1) | (0xFF00FF00u & m1);
+              best16[2 * q] = __viaddmin_u16x2(a0, __byte_perm(wd[q], 0u, 0x4140u), best16[2 * q]);
+              best16[2 * q + 1] = __viaddmin_u16x2(a1, __byte_perm(wd[q], 0u, 0x4342u), best16[2 * q + 1]);
+            }
+          } else if (inf_free) {
 #pragma unroll
             for (int j = 0; j < CPT; ++j)
               best[j] = __viaddmin_u32(dum, dp_weight<W>(wd[(j * sizeof(W)) / 4], j), best[j]);
@@ -236,6 +262,14 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_relax_kernel(const DpPar
       }
       cp_async_wait<0>();
       __syncthreads();
+    }
+    if constexpr (sizeof(W) == 1) {
+#pragma unroll
+      for (int k = 0; k < CPT / 2; ++k) {
+        const uint32_t lo = best16[k] & 0xFFFFu, hi = best16[k] >> 16;
+        if (lo != 0xFFFFu) best[2 * k] = min(best[2 * k], lo);
+        if (hi != 0xFFFFu) best[2 * k + 1] = min(best[2 * k + 1], hi);
+      }
     }
 #pragma unroll
     for (int j = 0; j < CPT; ++j) scomb[tid * CPT + j] = best[j];
