@@ -366,6 +366,16 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpPara
 #pragma unroll
   for (int j = 0; j < CPT; ++j) cd[j] = sdv[ct * CPT + j];
   const uint32_t cv0 = vid(p0 + ct * CPT);
+  // u8 FAST: my columns' distances as 16-bit lanes (j = 2k, 2k + 1) for a
+  // per-row filter; a row passes it only if some lane has w == (dv - du) mod
+  // 2^16 (no false negatives), and only those rows run the exact test
+  uint32_t cd2[CPT / 2];
+  bool small16 = true;
+#pragma unroll
+  for (int k = 0; k < CPT / 2; ++k) {
+    cd2[k] = (cd[2 * k] & 0xFFFFu) | (cd[2 * k + 1] << 16);
+    small16 &= cd[2 * k] <= 0xFFFFu && cd[2 * k + 1] <= 0xFFFFu;
+  }
   bool zero_tight = false;
   for (uint32_t sweep = 0;; ++sweep) {
     uint32_t best[CPT];
@@ -405,6 +415,19 @@ __global__ void __launch_bounds__(kBucketThreads, 2) dp_tree_kernel(const DpPara
         const uint4 v4 = st[m * kBucketThreads + tid];
         const uint32_t wd[4] = {v4.x, v4.y, v4.z, v4.w};
         if constexpr (FAST) {
+          if constexpr (sizeof(W) == 1) {
+            if (small16 && dum <= 0xFFFFu) {
+              const uint32_t du2 = dum * 0x10001u;
+              uint32_t any = 0;
+#pragma unroll
+              for (int q = 0; q < 4; ++q) {
+                const uint32_t x0 = __vsub2(cd2[2 * q], du2) ^ __byte_perm(wd[q], 0u, 0x4140u);
+                const uint32_t x1 = __vsub2(cd2[2 * q + 1], du2) ^ __byte_perm(wd[q], 0u, 0x4342u);
+                any |= ((x0 - 0x00010001u) & ~x0) | ((x1 - 0x00010001u) & ~x1);  // a zero lane
+              }
+              if (!(any & 0x80008000u)) continue;
+            }
+          }
           const uint32_t dj = u - cv0;  // row u is my column j's own vertex iff dj == j*Q
           const uint32_t jd = ((dj & (p.Q - 1)) == 0 && (dj >> p.qbits) < (uint32_t)CPT)
                                   ? (dj >> p.qbits) : (uint32_t)CPT;
