@@ -106,6 +106,18 @@ def build_graph(n, seed, kind, cols=None):
     raise ValueError(kind)
 
 
+def self_launch(nproc: int) -> int:
+    """Re-runs this command under torch.distributed.run with nproc ranks on
+    127.0.0.1 (a free port); returns the launcher's exit code."""
+    import socket
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nproc}",
+           "--master-addr=127.0.0.1", f"--master-port={port}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
 def run_reference(args, rank, world):
     """The reference's own CPU implementation (oracle/_ref), rank 0 only."""
     if rank != 0:
@@ -180,10 +192,16 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-batch", action="store_true", help="skip the config-5 batch object")
+    ap.add_argument("--no-configs", action="store_true",
+                    help="skip the per-config objects (BASELINE configs 1, 2, 4, 5)")
     ap.add_argument("--ref-skip-partitioned", action="store_true")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` without a launcher: start the N ranks
+        # (one process per GPU) ourselves, exactly as the driver's torchrun does
+        raise SystemExit(self_launch(args.gpus))
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))

@@ -44,9 +44,26 @@ namespace sssp_b200 {
 // position order.
 constexpr int kBucketMaxSlots = 8;
 
-struct BucketParams {
+// One shard of the launch.  Every shard that lives on the launching device
+// runs in the SAME cooperative launch (CTA range [i*G, (i+1)*G) = local shard
+// i), so shards never wait on a kernel that CUDA is free not to co-schedule
+// (ncu replay, CUDA_LAUNCH_BLOCKING, MPS).  Only shards on other devices /
+// processes sit behind the cross-launch barrier.
+struct BucketLocal {
   const void* adj;      // [n rows][row_stride]: this shard's columns, positions
   const void* adjT;     // PULL source (nullptr: push only); row r, global positions
+  uint32_t* ubm;        // [2][row_stride/32]: published unsettled bitmap per tile
+  void* pkey;           // [row_stride] K: per-column pull minimum (balanced pull)
+  uint64_t* dist_out;   // [loc_n] (local vertex ids)
+  uint64_t* pred_out;   // [loc_n]
+  uint64_t* info;       // [4]: settled vertices, classes, rows pushed, rows pulled
+  uint64_t* info2;      // [2]: barriers used, error
+  uint32_t shard;       // global shard index
+};
+
+struct BucketParams {
+  BucketLocal loc[kMaxShards];  // the shards of this launch (nlocal)
+  uint32_t nlocal;
   uint64_t adjT_stride; // elements per adjT row (= nshards * row_stride)
   uint32_t adjT_by_pos; // 1: adjT row of column p is the local position p (sharded
                         //    transpose); 0: the vertex id vid(p) (one shard)
@@ -55,19 +72,18 @@ struct BucketParams {
   uint32_t Q, L;        // layout: position p = q*L + s  <->  local vertex s*Q + q
   uint32_t qbits, lbits;
   uint32_t T;           // positions per CTA
-  uint32_t nshards, shard, loc_n;
+  uint32_t nshards, loc_n;
   uint32_t* peer_bitmap[kMaxShards];  // every shard's [2][nshards*row_stride/32] (self incl.)
   uint32_t* peer_ctrl[kMaxShards];    // every shard's [2][3][nshards*G]: tile lmin, cand, uns
-  unsigned long long* peer_bar[kMaxShards];  // every shard's barrier counter (nshards > 1)
-  uint32_t* ubm;        // this shard's [2][row_stride/32]: published unsettled bitmap per tile
-  void* pkey;           // this shard's [row_stride] K: per-column pull minimum (balanced pull)
-  uint64_t* bar_epoch;  // this shard's count of cross-shard barriers completed by earlier
-                        // launches (read at start, advanced at exit; same on every shard)
+  // Cross-launch barrier (nlocal < nshards): launch counters, by global shard.
+  // The leader of every launch adds nlocal to EVERY shard's counter once per
+  // barrier; a launch waits on the counter of its first shard.
+  unsigned long long* peer_bar[kMaxShards];
+  unsigned long long* arrive;  // this launch's CTA arrival counter (monotonic)
+  unsigned long long* release; // this launch's release word (barrier count)
+  uint64_t* bar_epoch;  // cross-launch barriers completed by earlier launches (read at
+                        // start, advanced at exit; the same value on every launch)
   uint64_t timeout_ns;
-  uint64_t* dist_out;   // [loc_n] (local vertex ids)
-  uint64_t* pred_out;   // [loc_n]
-  uint64_t* info;       // [4]: settled vertices, classes, rows pushed, rows pulled
-  uint64_t* info2;      // [2]: barriers used, error
   uint64_t* trace;      // optional [64]: %globaltimer after every barrier (CTA 0 of shard 0)
   uint64_t seq;         // launch tag: a watchdog failure writes it to info2[1] (no reset needed)
   // Independent solves sharing one launch (one shard only): the grid is
@@ -183,15 +199,18 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   constexpr int CPT = 16 / (int)sizeof(W);  // columns per thread (one 16 B load)
 
   extern __shared__ __align__(16) uint32_t smem[];
-  // slot (independent solve) of this CTA and its tile within the slot
-  const uint32_t Gs = MULTI ? gridDim.x / p.nslots : gridDim.x;
-  const uint32_t slot = MULTI ? blockIdx.x / Gs : 0u, bx = blockIdx.x - slot * Gs;
+  // slot (independent solve; MULTI) or local shard of this CTA, and its tile
+  const uint32_t Gs = MULTI ? gridDim.x / p.nslots : gridDim.x / p.nlocal;
+  const uint32_t grp = blockIdx.x / Gs, bx = blockIdx.x - grp * Gs;
+  const uint32_t slot = MULTI ? grp : 0u;
+  const BucketLocal& S = p.loc[MULTI ? 0u : grp];
+  const uint32_t shard = S.shard;
   auto at = [&](auto* ptr) {  // this slot's copy of an exchange-region array
     return reinterpret_cast<decltype(ptr)>(reinterpret_cast<char*>(const_cast<void*>(
                                                static_cast<const void*>(ptr))) + slot * p.slot_bytes);
   };
   const uint32_t source = p.slot_src[slot];
-  uint32_t* const ubm = at(p.ubm);
+  uint32_t* const ubm = at(S.ubm);
   const uint32_t T = p.T, G = Gs * p.nshards;  // G = tiles of ALL shards
   const uint32_t TW = T / 32;  // bitmap words per tile
   const uint32_t lwords = (uint32_t)(p.row_stride / 32);
@@ -209,17 +228,17 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   __shared__ uint32_t s_cnt[2];
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t me = p.shard * Gs + bx;  // global tile id
+  const uint32_t me = shard * Gs + bx;    // global tile id
   const uint32_t p0 = bx * T;             // first LOCAL position of the tile
   const uint32_t tbits = 31u - __clz(T);  // T is a power of two
-  const W* adj = static_cast<const W*>(p.adj);
-  const W* adjT = static_cast<const W*>(p.adjT);
+  const W* adj = static_cast<const W*>(S.adj);
+  const W* adjT = static_cast<const W*>(S.adjT);
   const uint32_t TPR = T * sizeof(W) / 16;  // threads per row slice
   const uint32_t RG = kBucketThreads / TPR; // row groups
   // global per-step arrays: ctrl = [2][3][G] (lmin, candidates, unsettled)
-  uint32_t* const glob = at(p.peer_ctrl[p.shard]);
-  const uint32_t* const gbm = at(p.peer_bitmap[p.shard]);
-  K* const pkey = at(static_cast<K*>(p.pkey));
+  uint32_t* const glob = at(p.peer_ctrl[shard]);
+  const uint32_t* const gbm = at(p.peer_bitmap[shard]);
+  K* const pkey = at(static_cast<K*>(S.pkey));
   // global position -> global vertex id
   auto gvid = [&](uint32_t g) -> uint32_t {
     const uint32_t j = g >> (p.qbits + p.lbits);  // row_stride = Q*L = 2^(qbits+lbits)
@@ -230,38 +249,56 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   auto stamp = [&]() {
     if (p.trace && me == 0 && slot == 0 && tid == 0 && ntr < 64) p.trace[ntr++] = globaltimer();
   };
-  // One barrier over every CTA of every shard: the cooperative grid barrier
-  // with one shard (1.29 us at 256 CTAs, the fastest measured variant:
-  // profiles/r01_ubench_barrier.jsonl); with several, each CTA bumps every
-  // shard's counter by a system-scope atomic (an NVLink write for a remote
-  // shard) and waits until its own shard's counter shows all G tiles of this
-  // barrier.  The counter continues across launches (bar_epoch).
+  // One barrier over every CTA of every shard.  All shards in this launch:
+  // the cooperative grid barrier (1.29 us at 256 CTAs, the fastest measured
+  // variant: profiles/r01_ubench_barrier.jsonl).  Shards in other launches
+  // (other GPUs / processes): hierarchical -- CTAs arrive on this launch's
+  // counter, the launch leader adds nlocal to every shard's counter with one
+  // system-scope atomic each (an NVLink write for a remote shard), waits for
+  // all nshards arrivals on its own, then releases its CTAs: nshards NVLink
+  // atomics per launch per barrier, not one per CTA.  Every counter continues
+  // across launches (bar_epoch), so nothing is reset between solves.
   __shared__ uint32_t s_fail;
   if (tid == 0) s_fail = 0;
   uint64_t nbar = 0;
   bool failed = false;
   const uint64_t t_start = globaltimer();
-  const uint64_t bar_base = p.nshards > 1 ? *(volatile uint64_t*)p.bar_epoch : 0;
+  const bool cross = p.nlocal < p.nshards;
+  const uint64_t bar_base = cross ? *(volatile uint64_t*)p.bar_epoch : 0;
   stamp();  // trace[0]: kernel start
+  auto spin_until = [&](const unsigned long long* a, unsigned long long target, bool sys) -> bool {
+    unsigned long long v;
+    uint32_t polls = 0;
+    while (true) {
+      if (sys) asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+      else asm volatile("ld.acquire.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(a) : "memory");
+      if (v >= target) return (v >> 63) == 0;  // bit 63: the leader's watchdog fired
+      if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) return false;
+    }
+  };
   auto barrier = [&]() {
-    if (p.nshards == 1) {
+    if (!cross) {
       cg::this_grid().sync();
     } else {
       __syncthreads();
       if (tid == 0) {
-        __threadfence_system();
-        for (uint32_t j = 0; j < p.nshards; ++j) atomicAdd_system(p.peer_bar[j], 1ull);
-        const unsigned long long target = (bar_base + nbar + 1) * (unsigned long long)G;
-        unsigned long long v;
-        uint32_t polls = 0;
-        while (true) {
-          asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p.peer_bar[p.shard]) : "memory");
-          if (v >= target) break;
-          if ((++polls & 1023u) == 0 && globaltimer() - t_start > p.timeout_ns) {
-            s_fail = 1;
-            p.info2[slot * 2 + 1] = p.seq + slot;
-            break;
-          }
+        const unsigned long long b = bar_base + nbar + 1;  // global barrier number
+        bool ok = true;
+        __threadfence();
+        atomicAdd(p.arrive, 1ull);
+        if (blockIdx.x == 0) {
+          ok = spin_until(p.arrive, b * gridDim.x, false);
+          __threadfence_system();
+          for (uint32_t j = 0; j < p.nshards; ++j) atomicAdd_system(p.peer_bar[j], (unsigned long long)p.nlocal);
+          ok = ok && spin_until(p.peer_bar[p.loc[0].shard], b * p.nshards, true);
+          const unsigned long long rel = ok ? b : (b | (1ull << 63));
+          asm volatile("st.release.gpu.global.u64 [%0], %1;" ::"l"(p.release), "l"(rel) : "memory");
+        } else {
+          ok = spin_until(p.release, b, false);
+        }
+        if (!ok) {
+          s_fail = 1;
+          S.info2[slot * 2 + 1] = p.seq + slot;
         }
       }
       __syncthreads();
@@ -312,7 +349,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   // distance 0 -- settled and its row pushed by every CTA over its own tile
   // without a barrier (every CTA knows the source): dist = w(s,v), pred = s
   // for each finite w, exactly the serial engine's first round.
-  const uint32_t vbase = p.shard * p.loc_n;
+  const uint32_t vbase = shard * p.loc_n;
   for (uint32_t i = warp; i < TW; i += kBucketThreads / 32) {  // one ballot per bitmap word
     const uint32_t vl = pos_to_vid(p0 + i * 32 + lane, p.Q, p.lbits, p.qbits);
     const uint32_t m =
@@ -522,7 +559,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       // the cp.async stage [2][kPullDepth][threads] of 16 B slots
       K* sk = scomb;
       uint32_t* scol = reinterpret_cast<uint32_t*>(scomb + (T + 2));
-      const uint32_t* bml = sbm + p.shard * lwords;
+      const uint32_t* bml = sbm + shard * lwords;
       const uint32_t wpt = (lwords + kBucketThreads - 1) / kBucketThreads;
       const uint32_t w0 = tid * wpt;
       auto uword = [&](uint32_t k2) -> uint32_t {  // unsettled-after-B_d word w0 + k2
@@ -562,7 +599,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       for (uint32_t i = tid; i < ncols; i += kBucketThreads) sk[i] = KT::kNone;
       __syncthreads();
       stamp();
-      if (p.trace && tid == 0 && p.shard == 0 && slot == 0 && bx < 1024)  // per-CTA pull span (debug)
+      if (p.trace && tid == 0 && shard == 0 && slot == 0 && bx < 1024)  // per-CTA pull span (debug)
         p.trace[64 + 2 * bx] = globaltimer();
       // Two-stage cp.async pipeline: a thread's items are lo + tid + k*256;
       // batch b+1's 16 B chunks stream into the thread's stage slots while
@@ -671,7 +708,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       __syncthreads();
       for (uint32_t i = tid; i < ncols; i += kBucketThreads)
         if (sk[i] != KT::kNone) smem_min(&pkey[scol[i]], sk[i]);
-      if (p.trace && tid == 0 && p.shard == 0 && slot == 0 && bx < 1024)
+      if (p.trace && tid == 0 && shard == 0 && slot == 0 && bx < 1024)
         p.trace[64 + 2 * bx + 1] = globaltimer();
     }
     // the pull's extra barrier (every partial minimum is in pkey); with
@@ -715,19 +752,19 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   for (uint32_t i = tid; i < T; i += kBucketThreads) {
     const uint32_t v = pos_to_vid(p0 + i, p.Q, p.lbits, p.qbits);
     if (v < p.loc_n && vbase + v < p.n) {
-      p.dist_out[slot * p.out_stride + v] = sdist[i] == DINF ? ~0ull : (uint64_t)sdist[i];
-      p.pred_out[slot * p.out_stride + v] = spred[i] == 0xFFFFFFFFu ? ~0ull : (uint64_t)spred[i];
+      S.dist_out[slot * p.out_stride + v] = sdist[i] == DINF ? ~0ull : (uint64_t)sdist[i];
+      S.pred_out[slot * p.out_stride + v] = spred[i] == 0xFFFFFFFFu ? ~0ull : (uint64_t)spred[i];
     }
   }
   stamp();
   if (bx == 0 && tid == 0) {
-    uint64_t* const info = p.info + slot * 4;
+    uint64_t* const info = S.info + slot * 4;
     info[0] = settled;
     info[1] = step;
     info[2] = pushed;
     info[3] = pulled;
-    p.info2[slot * 2] = nbar;
-    if (p.nshards > 1) *p.bar_epoch = bar_base + nbar;  // every CTA read it before barrier 1
+    S.info2[slot * 2] = nbar;
+    if (cross && blockIdx.x == 0) *p.bar_epoch = bar_base + nbar;  // every CTA read it before barrier 1
   }
 }
 

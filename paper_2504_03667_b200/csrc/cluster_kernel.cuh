@@ -76,8 +76,9 @@ __device__ __forceinline__ uint64_t ld_smem_pair(uint32_t addr, uint64_t& hi) {
 // TRACE: record %globaltimer at every round end (record_round_times); a
 // separate instance because even an untaken trace branch in the round loop
 // cost ~4 % of the solve (18.6 vs 17.85 ms at n=32768)
-template <typename W, int EPL, int NW, bool PACKED, bool TRACE = false>
-__global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanParams p) {
+template <typename W, int EPL, int NW, bool PACKED, bool TRACE = false, bool MS = false>
+__global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const __grid_constant__ ScanLaunch LA) {
+  SSSP_LAUNCH_SHARD(MS, LA, p, bid);
   using Row = RowSlice<W, EPL>;
   constexpr int NP = NW / 4;  // key pairs per lane: Q <= 16*NW = 64*NP
   constexpr uint32_t WINF = WInf<W>::v;
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
   const uint32_t csize = cluster_nctarank();
   const uint32_t Q = p.G;             // = csize * NW, a power of two
   const uint32_t qbits = 31u - __clz(Q);
-  const uint32_t solve = blockIdx.x / csize;
+  const uint32_t solve = bid / csize;
   const uint32_t q = cr * NW + warp;
   const uint32_t tb = 32u - p.vbits;
   const uint64_t tagmask = (1ull << tb) - 1ull;
@@ -518,8 +519,9 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_scan_kernel(const ScanPara
 // cycles vs ~590 for 64).  Participant q = warp*C + cta_rank, so consecutive
 // vertex ids fall on consecutive CTAs and the runner-up CTA minimum is still
 // the likely next winner.  PACKED state only (the host falls back otherwise).
-template <typename W, int EPL, int NW>
-__global__ void __launch_bounds__(NW * 32, 1) cluster_hier_kernel(const ScanParams p) {
+template <typename W, int EPL, int NW, bool MS = false>
+__global__ void __launch_bounds__(NW * 32, 1) cluster_hier_kernel(const __grid_constant__ ScanLaunch LA) {
+  SSSP_LAUNCH_SHARD(MS, LA, p, bid);
   using Row = RowSlice<W, EPL>;
   constexpr uint32_t WINF = WInf<W>::v;
   constexpr uint32_t DINF = 0xFFFFFFFFu;
@@ -537,7 +539,7 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_hier_kernel(const ScanPara
   const uint32_t csize = cluster_nctarank();
   const uint32_t Q = p.G;  // = csize * NW, a power of two
   const uint32_t qbits = 31u - __clz(Q);
-  const uint32_t solve = blockIdx.x / csize;
+  const uint32_t solve = bid / csize;
   const uint32_t q = warp * csize + cr;
   const uint32_t tb = 32u - p.vbits;
   const uint64_t tagmask = (1ull << tb) - 1ull;
@@ -744,10 +746,11 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_hier_kernel(const ScanPara
 // t_sync microbenchmark for the cluster exchange (same code, no relax).
 // HIER = the hierarchical variant: named barrier, warp 0 publishes the CTA
 // key, every warp polls the C CTA keys.
-template <int NW, bool HIER = false>
-__global__ void __launch_bounds__(NW * 32, 1) cluster_probe_kernel(const ScanParams p,
+template <int NW, bool HIER = false, bool MS = false>
+__global__ void __launch_bounds__(NW * 32, 1) cluster_probe_kernel(const __grid_constant__ ScanLaunch LA,
                                                                   uint32_t rounds,
                                                                   uint64_t* out_ns) {
+  SSSP_LAUNCH_SHARD(MS, LA, p, bid);
   constexpr int NP = NW / 4;
   constexpr uint32_t QMAX = 16u * NW;
   __shared__ __align__(16) uint64_t s_keys[2][QMAX];
@@ -757,7 +760,7 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_probe_kernel(const ScanPar
   const uint32_t cr = cluster_ctarank();
   const uint32_t csize = cluster_nctarank();
   const uint32_t Q = HIER ? csize : p.G;  // participants of the DSMEM exchange
-  const uint32_t solve = blockIdx.x / csize;
+  const uint32_t solve = bid / csize;
   const uint32_t q = HIER ? cr : cr * NW + warp;
   const uint32_t tb = 32u - p.vbits;
   const uint64_t tagmask = (1ull << tb) - 1ull;
@@ -839,7 +842,7 @@ __global__ void __launch_bounds__(NW * 32, 1) cluster_probe_kernel(const ScanPar
     acc += best >> 32;
   }
   if (cr == 0 && warp == 0 && lane == 0) {
-    out_ns[solve] = failed ? ~0ull : globaltimer() - t0;
+    out_ns[lsh_ + solve] = failed ? ~0ull : globaltimer() - t0;
     p.info[solve * 4 + 1] = E;
     p.info[solve * 4 + 0] = acc;
   }

@@ -67,6 +67,28 @@ struct ScanParams {
   uint64_t timeout_ns;
 };
 
+// One launch carries every shard that lives on the launching device: blocks
+// [i*bps, (i+1)*bps) run local shard i.  Shards of one device therefore never
+// wait on a separate kernel that CUDA is free not to co-schedule (ncu replay,
+// CUDA_LAUNCH_BLOCKING, MPS); only shards on other devices / processes are
+// separate launches.
+struct ScanLaunch {
+  ScanParams sh[kMaxShards];
+  uint32_t nlocal;  // shards in this launch
+  uint32_t bps;     // blocks per shard (solves x CTAs per solve)
+};
+
+// Kernel preamble: this block's shard parameters and its block index within
+// the shard (`bid` replaces blockIdx.x in the kernels).  MS (a template
+// constant) = the launch may carry several shards; the single-shard instances
+// index sh[0] statically, so every parameter stays an immediate constant-bank
+// operand in the round loop (a runtime index costs an LDC per use: the n-round
+// kernel measured 18.8 vs 17.9 ms at n=32768).
+#define SSSP_LAUNCH_SHARD(MS, LA, p, bid)                       \
+  const uint32_t lsh_ = (MS) ? blockIdx.x / (LA).bps : 0u;     \
+  const ScanParams& p = (LA).sh[(MS) ? lsh_ : 0u];             \
+  const uint32_t bid = blockIdx.x - lsh_ * (LA).bps
+
 constexpr uint32_t kFlagPrefetchReg = 1u;  // runner-up row into registers
 constexpr uint32_t kFlagPrefetchL2 = 2u;   // owner L2 prefetch of local-best rows
 constexpr uint32_t kFlagSpeculate = 4u;    // cluster engine: speculative relax of the runner-up
@@ -255,13 +277,14 @@ __device__ __forceinline__ uint64_t min_key(const uint64_t (&ks)[2 * NP]) {
 // t_sync microbenchmark: the same launch shape and the same publish/gather
 // code as the solve, with the relaxation and local election removed.  Each
 // CTA publishes a synthetic key per round; out_ns[solve] = elapsed ns.
-template <int NP>
-__global__ void __launch_bounds__(32, 1) exchange_probe_kernel(const ScanParams p,
+template <int NP, bool MS = false>
+__global__ void __launch_bounds__(32, 1) exchange_probe_kernel(const __grid_constant__ ScanLaunch LA,
                                                                uint32_t rounds,
                                                                uint64_t* out_ns) {
+  SSSP_LAUNCH_SHARD(MS, LA, p, bid);
   const int lane = threadIdx.x;
-  const uint32_t solve = blockIdx.x / p.G;
-  const uint32_t c = blockIdx.x - solve * p.G;
+  const uint32_t solve = bid / p.G;
+  const uint32_t c = bid - solve * p.G;
   const uint32_t nslot = p.nshards * p.G;
   const uint32_t tb = 32u - p.vbits;
   const uint64_t tagmask = (1ull << tb) - 1ull;
@@ -287,15 +310,16 @@ __global__ void __launch_bounds__(32, 1) exchange_probe_kernel(const ScanParams 
     acc += min_key<NP>(ks) >> 32;
   }
   if (c == 0 && lane == 0) {
-    out_ns[solve] = failed ? ~0ull : globaltimer() - t0;
+    out_ns[lsh_ + solve] = failed ? ~0ull : globaltimer() - t0;
     p.info[solve * 4 + 1] = E;
     p.info[solve * 4 + 0] = acc;  // keeps the reduction live
   }
 }
 
 // NP = pairs of exchange slots each lane reads (P*G <= 64*NP).
-template <typename W, int EPL, int NP>
-__global__ void __launch_bounds__(32, 1) scan_dijkstra_kernel(const ScanParams p) {
+template <typename W, int EPL, int NP, bool MS = false>
+__global__ void __launch_bounds__(32, 1) scan_dijkstra_kernel(const __grid_constant__ ScanLaunch LA) {
+  SSSP_LAUNCH_SHARD(MS, LA, p, bid);
   using Row = RowSlice<W, EPL>;
   constexpr uint32_t WINF = WInf<W>::v;
   constexpr uint32_t DINF = 0xFFFFFFFFu;
@@ -306,8 +330,8 @@ __global__ void __launch_bounds__(32, 1) scan_dijkstra_kernel(const ScanParams p
 
   const int lane = threadIdx.x;
   const uint32_t G = p.G;
-  const uint32_t solve = blockIdx.x / G;
-  const uint32_t c = blockIdx.x - solve * G;
+  const uint32_t solve = bid / G;
+  const uint32_t c = bid - solve * G;
   const uint32_t nslot = p.nshards * G;
   const uint32_t tb = 32u - p.vbits;
   const uint64_t tagmask = (1ull << tb) - 1ull;

@@ -189,6 +189,7 @@ struct Shard {
   uint64_t* d_info2 = nullptr;   // bucket: [B][2] barriers used, watchdog
   uint64_t* d_trace = nullptr;   // debug (SSSP_BUCKET_TRACE)
   bool peer_ipc[kMaxShards] = {};
+  bool own_stream = true;        // false: shares the stream of the device's first shard
   KernelFn fn = nullptr;
 };
 
@@ -215,7 +216,7 @@ struct sssp_graph {
   uint32_t bTb = 0, bGb = 0, bslots_b = 0;  // batch tiling: wider tiles, more slots per launch
   uint64_t done_off = 0;                 // bucket: per-slot done flags (after the slot regions)
   uint64_t slots_bytes = 0;              // scan-engine exchange region (start of d_slots)
-  uint64_t bar_off = 0, epoch_off = 0, ctrl_off = 0, bm_off = 0, ubm_off = 0, pkey_off = 0,
+  uint64_t bar_off = 0, arrive_off = 0, epoch_off = 0, release_off = 0, ctrl_off = 0, bm_off = 0, ubm_off = 0, pkey_off = 0,
            region_bytes = 0;
   uint64_t exch_base = 0;
   double transfer_in_s = 0;
@@ -504,6 +505,13 @@ int alloc_state(sssp_graph* g, Shard& s) {
   return SSSP_OK;
 }
 
+// Shards of this process on `device` (they share one launch).
+uint32_t shards_on_device(const sssp_graph* g, int device) {
+  uint32_t c = 0;
+  for (const auto& t : g->sh) c += t.device == device ? 1u : 0u;
+  return c;
+}
+
 // Encoding-dependent constants shared by every shard; requires max_w.
 int finalize_encoding(sssp_graph* g) {
   const uint64_t n = g->n;
@@ -526,9 +534,10 @@ int finalize_encoding(sssp_graph* g) {
     for (auto& s : g->sh) {
       s.NP = s.NW / 4;
       s.hier = g->packed && (g->opt.flags & kFlagHier) && s.C <= 16;
-      s.fn = s.hier ? get_cluster_hier_kernel((int)g->wbytes, (int)s.EPL, (int)s.NW)
+      const bool ms = shards_on_device(g, s.device) > 1;
+      s.fn = s.hier ? get_cluster_hier_kernel((int)g->wbytes, (int)s.EPL, (int)s.NW, ms)
                     : get_cluster_kernel((int)g->wbytes, (int)s.EPL, (int)s.NW, g->packed != 0,
-                                         g->opt.record_round_times != 0);
+                                         g->opt.record_round_times != 0, ms);
       if (!s.fn) return fail(SSSP_ERR_UNSUPPORTED, "no cluster kernel instance for this layout");
     }
     return SSSP_OK;
@@ -544,7 +553,7 @@ int finalize_encoding(sssp_graph* g) {
   if (!np) return fail(SSSP_ERR_UNSUPPORTED, "too many exchange participants");
   for (auto& s : g->sh) {
     s.NP = np;
-    s.fn = get_grid_kernel((int)g->wbytes, (int)s.EPL, (int)np);
+    s.fn = get_grid_kernel((int)g->wbytes, (int)s.EPL, (int)np, shards_on_device(g, s.device) > 1);
     if (!s.fn) return fail(SSSP_ERR_UNSUPPORTED, "no kernel instance for this layout");
   }
   return SSSP_OK;
@@ -714,7 +723,9 @@ int plan_bucket(sssp_graph* g) {
   const uint64_t GT = (uint64_t)g->bG * g->P;
   const uint64_t words = s0.row_stride / 32 * g->P;
   g->bar_off = 0;
+  g->arrive_off = 64;
   g->epoch_off = 128;
+  g->release_off = 192;
   g->ctrl_off = 256;
   g->bm_off = (g->ctrl_off + 2 * 3 * GT * 4 + 255) & ~255ull;
   g->ubm_off = (g->bm_off + 2 * words * 4 + 255) & ~255ull;
@@ -830,7 +841,15 @@ int create_shard_objects(sssp_graph* g, uint32_t P, const int* devices, uint32_t
       rc = plan_layout(s, loc_n, gm);
     }
     if (rc) return rc;
-    CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
+    // shards on one device share one stream (and one cooperative launch)
+    s.own_stream = true;
+    for (uint32_t j = 0; j < i; ++j)
+      if (g->sh[j].device == s.device) {
+        s.stream = g->sh[j].stream;
+        s.own_stream = false;
+        break;
+      }
+    if (s.own_stream) CK(cudaStreamCreateWithFlags(&s.stream, cudaStreamNonBlocking));
     CK(cudaEventCreate(&s.ev0));
     CK(cudaEventCreate(&s.ev1));
   }
@@ -856,38 +875,79 @@ void destroy_graph(sssp_graph* g) {
     pinned_put(s.h_info, B * 4 * sizeof(uint64_t));
     if (s.ev0) cudaEventDestroy(s.ev0);
     if (s.ev1) cudaEventDestroy(s.ev1);
-    if (s.stream) cudaStreamDestroy(s.stream);
   }
+  for (auto& s : g->sh)  // after every shard's frees were queued (shared streams)
+    if (s.stream && s.own_stream) {
+      cudaSetDevice(s.device);
+      cudaStreamDestroy(s.stream);
+    }
   delete g;
 }
 
-// Launches k solves of `fn` (cluster engine: k clusters of C CTAs x NW warps;
-// grid engine: k*G single-warp CTAs).  Probe kernels pass rounds/out_ns.
-cudaError_t launch_kernel(sssp_graph* g, Shard& s, void* fn, uint32_t k, const ScanParams& p,
-                          const uint32_t* rounds, int is_probe, uint64_t* out_ns) {
+// Shards grouped by device, in order of first appearance: every group is ONE
+// launch (shards as block ranges), so shards on one device never depend on
+// CUDA co-scheduling two kernels.
+std::vector<std::vector<uint32_t>> device_groups(const sssp_graph* g) {
+  std::vector<std::vector<uint32_t>> groups;
+  for (uint32_t a = 0; a < g->sh.size(); ++a) {
+    bool placed = false;
+    for (auto& gr : groups)
+      if (!placed && g->sh[gr[0]].device == g->sh[a].device) {
+        gr.push_back(a);
+        placed = true;
+      }
+    if (!placed) groups.push_back({a});
+  }
+  return groups;
+}
+
+// Launches k solves of `fn` for every shard of a device group (cluster
+// engine: k clusters of C CTAs x NW warps per shard; grid engine: k*G
+// single-warp CTAs per shard).  Probe kernels pass rounds/out_ns.  Several
+// shards in one launch spin on each other's mailboxes, so that launch is
+// cooperative (co-residency guaranteed or the launch fails loudly).
+cudaError_t launch_kernel(sssp_graph* g, const std::vector<uint32_t>& grp, void* fn, uint32_t k,
+                          const std::vector<ScanParams>& ps, const uint32_t* rounds, int is_probe,
+                          uint64_t* out_ns) {
+  const Shard& s = g->sh[grp[0]];
+  ScanLaunch la{};
+  la.nlocal = (uint32_t)grp.size();
+  for (uint32_t i = 0; i < la.nlocal; ++i) la.sh[i] = ps[i];
   cudaLaunchConfig_t cfg{};
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
+  int na = 0;
   cfg.stream = s.stream;
   if (g->cluster) {
-    cfg.gridDim = dim3(k * s.C);
+    la.bps = k * s.C;
+    cfg.gridDim = dim3(la.bps * la.nlocal);
     cfg.blockDim = dim3(s.NW * 32);
     cfg.dynamicSmemBytes = is_probe ? 0 : (size_t)s.NW * s.L * 4;
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = s.C;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = s.C;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
   } else {
-    cfg.gridDim = dim3(k * s.G);
+    la.bps = k * s.G;
+    cfg.gridDim = dim3(la.bps * la.nlocal);
     cfg.blockDim = dim3(32);
   }
+  // independent single-shard clusters never wait on each other; everything
+  // else spins on other blocks of the launch
+  const bool coop = !g->cluster || la.nlocal > 1;
+  if (coop) {
+    at[na].id = cudaLaunchAttributeCooperative;
+    at[na].val.cooperative = 1;
+    ++na;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
   if (is_probe) {
     uint32_t r = *rounds;
-    void* args[] = {(void*)&p, (void*)&r, (void*)&out_ns};
+    void* args[] = {(void*)&la, (void*)&r, (void*)&out_ns};
     return cudaLaunchKernelExC(&cfg, fn, args);
   }
-  void* args[] = {(void*)&p};
+  void* args[] = {(void*)&la};
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
@@ -906,67 +966,72 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
       if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
     }
     const size_t smem_b = g->bslots_b ? bucket_smem(g, true) : 0;
+    // shards on one device share one cooperative launch (grid = nlocal x tiles)
+    const auto groups = device_groups(g);
     for (uint32_t i = 0; i < k;) {  // solves i .. i+ns-1 share a launch
       // more solves left than the single-solve grid can pair: batch tiling
       const bool wide = g->bslots_b > 0 && k - i > g->bslots;
       const uint32_t ns = std::min<uint32_t>(wide ? g->bslots_b : g->bslots, k - i);
       const uint32_t tiles = wide ? g->bGb : g->bG;
-      for (auto& s : g->sh) {
-        CK(cudaSetDevice(s.device));
+      for (const auto& gr : groups) {
+        Shard& s0 = g->sh[gr[0]];
+        CK(cudaSetDevice(s0.device));
         BucketParams bp{};
         bp.nslots = ns;
         for (uint32_t j = 0; j < ns; ++j) bp.slot_src[j] = (uint32_t)sources[i + j];
         bp.slot_bytes = g->region_bytes;
-        bp.out_stride = s.loc_n;
-        bp.adj = s.d_adj;
-        bp.adjT = s.pull_src;
-        bp.adjT_by_pos = s.pull_src == s.d_adj ? 0u : 1u;  // transpose rows: local positions
-        bp.adjT_stride = s.pull_src == s.d_adj ? s.row_stride : s.row_stride * g->P;
-        bp.row_stride = s.row_stride;
+        bp.out_stride = s0.loc_n;
+        bp.nlocal = (uint32_t)gr.size();
+        for (uint32_t li = 0; li < gr.size(); ++li) {
+          Shard& s = g->sh[gr[li]];
+          BucketLocal& L = bp.loc[li];
+          char* own = reinterpret_cast<char*>(s.d_slots) + g->slots_bytes;
+          L.adj = s.d_adj;
+          L.adjT = s.pull_src;
+          L.ubm = reinterpret_cast<uint32_t*>(own + g->ubm_off);
+          L.pkey = own + g->pkey_off;
+          L.dist_out = s.d_dist + (uint64_t)i * s.loc_n;
+          L.pred_out = s.d_pred + (uint64_t)i * s.loc_n;
+          L.info = s.d_info + (uint64_t)i * 4;
+          L.info2 = s.d_info2 + (uint64_t)i * 2;
+          L.shard = s.k;
+        }
+        bp.adjT_by_pos = s0.pull_src == s0.d_adj ? 0u : 1u;  // transpose rows: local positions
+        bp.adjT_stride = s0.pull_src == s0.d_adj ? s0.row_stride : s0.row_stride * g->P;
+        bp.row_stride = s0.row_stride;
         bp.n = (uint32_t)g->n;
-        bp.Q = s.G;
-        bp.L = s.L;
-        bp.qbits = bitlen(s.G) - 1;
-        bp.lbits = bitlen(s.L) - 1;
+        bp.Q = s0.G;
+        bp.L = s0.L;
+        bp.qbits = bitlen(s0.G) - 1;
+        bp.lbits = bitlen(s0.L) - 1;
         bp.T = wide ? g->bTb : g->bT;
         bp.nshards = g->P;
-        bp.shard = s.k;
-        bp.loc_n = (uint32_t)s.loc_n;
+        bp.loc_n = (uint32_t)s0.loc_n;
         for (uint32_t j = 0; j < g->P; ++j) {
-          char* base = reinterpret_cast<char*>(g->multiproc ? (void*)s.peer[j] : (void*)g->sh[j].d_slots) +
+          char* base = reinterpret_cast<char*>(g->multiproc ? (void*)s0.peer[j] : (void*)g->sh[j].d_slots) +
                        g->slots_bytes;
           bp.peer_ctrl[j] = reinterpret_cast<uint32_t*>(base + g->ctrl_off);
           bp.peer_bitmap[j] = reinterpret_cast<uint32_t*>(base + g->bm_off);
           bp.peer_bar[j] = reinterpret_cast<unsigned long long*>(base + g->bar_off);
         }
-        char* own = reinterpret_cast<char*>(s.d_slots) + g->slots_bytes;
-        bp.bar_epoch = reinterpret_cast<uint64_t*>(own + g->epoch_off);
-        bp.ubm = reinterpret_cast<uint32_t*>(own + g->ubm_off);
-        bp.pkey = own + g->pkey_off;
-        bp.done = reinterpret_cast<uint32_t*>(own + g->done_off);
+        char* own0 = reinterpret_cast<char*>(s0.d_slots) + g->slots_bytes;
+        bp.bar_epoch = reinterpret_cast<uint64_t*>(own0 + g->epoch_off);
+        bp.arrive = reinterpret_cast<unsigned long long*>(own0 + g->arrive_off);
+        bp.release = reinterpret_cast<unsigned long long*>(own0 + g->release_off);
+        bp.done = reinterpret_cast<uint32_t*>(own0 + g->done_off);
         bp.timeout_ns = g->opt.timeout_ms * 1000000ull;
-        bp.dist_out = s.d_dist + (uint64_t)i * s.loc_n;
-        bp.pred_out = s.d_pred + (uint64_t)i * s.loc_n;
-        bp.info = s.d_info + (uint64_t)i * 4;
-        bp.info2 = s.d_info2 + (uint64_t)i * 2;
-        if (getenv("SSSP_BUCKET_TRACE") && s.k == 0) {  // debug: per-barrier timestamps
-          if (!s.d_trace) CK(cudaMalloc(&s.d_trace, (64 + 2048) * 8));
-          CK(cudaMemsetAsync(s.d_trace, 0, (64 + 2048) * 8, s.stream));
-          bp.trace = s.d_trace;
+        if (getenv("SSSP_BUCKET_TRACE") && s0.k == 0) {  // debug: per-barrier timestamps
+          if (!s0.d_trace) CK(cudaMalloc(&s0.d_trace, (64 + 2048) * 8));
+          CK(cudaMemsetAsync(s0.d_trace, 0, (64 + 2048) * 8, s0.stream));
+          bp.trace = s0.d_trace;
         }
         bp.seq = g->bseq + 1 + i;
         void* args[] = {&bp};
-        if (g->P == 1) {
-          CK(cudaLaunchCooperativeKernel(ns > 1 ? bucket_fn(g->wbytes, true) : fn, dim3(tiles * ns),
-                                         dim3(kBucketThreads), args, wide ? smem_b : smem, s.stream));
-        } else {  // co-residency was checked in plan_bucket; cross-shard barrier in-kernel
-          cudaLaunchConfig_t cfg{};
-          cfg.gridDim = dim3(g->bG);
-          cfg.blockDim = dim3(kBucketThreads);
-          cfg.dynamicSmemBytes = smem;
-          cfg.stream = s.stream;
-          CK(cudaLaunchKernelExC(&cfg, fn, args));
-        }
+        const uint32_t grid = tiles * (ns > 1 ? ns : bp.nlocal);
+        // local shards other than the first wait for the launch on the
+        // group's stream (their own streams record the completion below)
+        CK(cudaLaunchCooperativeKernel(ns > 1 ? bucket_fn(g->wbytes, true) : fn, dim3(grid),
+                                       dim3(kBucketThreads), args, wide ? smem_b : smem, s0.stream));
       }
       i += ns;
     }
@@ -996,44 +1061,51 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
       }
     }
   }
-  for (auto& s : g->sh) {
-    CK(cudaSetDevice(s.device));
-    for (cudaEvent_t e : reset_ev) CK(cudaStreamWaitEvent(s.stream, e, 0));
-    for (uint32_t i = 0; i < k; ++i) s.h_sources[i] = (uint32_t)sources[i];
-    CK(cudaMemcpyAsync(s.d_sources, s.h_sources, k * sizeof(uint32_t), cudaMemcpyHostToDevice,
-                       s.stream));
-    CK(cudaMemsetAsync(s.d_info, 0, (uint64_t)k * 4 * sizeof(uint64_t), s.stream));
-    ScanParams p{};
-    p.adj = s.d_adj;
-    p.row_stride = s.row_stride;
-    p.n = (uint32_t)g->n;
-    p.G = s.G;
-    p.col_base = (uint32_t)s.col_base;
-    p.loc_n = (uint32_t)s.loc_n;
-    p.vbits = g->vbits;
-    p.shard = s.k;
-    p.nshards = g->P;
-    p.packed = g->packed;
-    p.sbits = g->sbits;
-    p.flags = g->opt.flags;
-    p.slots = s.d_slots;
-    for (uint32_t j = 0; j < g->P && j < (uint32_t)kMaxShards; ++j)
-      p.peer_slots[j] = g->multiproc ? s.peer[j] : g->sh[j].d_slots;
-    p.slot_stride = g->slot_stride;
-    p.bstride = (uint32_t)g->bstride;
-    p.nrep = g->nrep;
-    p.exch_base = g->exch_base;
-    p.sources = s.d_sources;
-    p.nsolve = k;
-    p.dist_out = s.d_dist;
-    p.pred_out = s.d_pred;
-    p.visit_order = s.d_visit;
-    p.round_ns = s.d_round_ns;
-    p.info = s.d_info;
-    p.timeout_ns = g->opt.timeout_ms * 1000000ull;
-    if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
-    CK(launch_kernel(g, s, (void*)s.fn, k, p, nullptr, 0, nullptr));
-    CK(cudaEventRecord(s.ev1, s.stream));
+  for (const auto& grp : device_groups(g)) {
+    std::vector<ScanParams> ps;
+    for (uint32_t li : grp) {
+      Shard& s = g->sh[li];
+      CK(cudaSetDevice(s.device));
+      for (cudaEvent_t e : reset_ev) CK(cudaStreamWaitEvent(s.stream, e, 0));
+      for (uint32_t i = 0; i < k; ++i) s.h_sources[i] = (uint32_t)sources[i];
+      CK(cudaMemcpyAsync(s.d_sources, s.h_sources, k * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                         s.stream));
+      CK(cudaMemsetAsync(s.d_info, 0, (uint64_t)k * 4 * sizeof(uint64_t), s.stream));
+      ScanParams p{};
+      p.adj = s.d_adj;
+      p.row_stride = s.row_stride;
+      p.n = (uint32_t)g->n;
+      p.G = s.G;
+      p.col_base = (uint32_t)s.col_base;
+      p.loc_n = (uint32_t)s.loc_n;
+      p.vbits = g->vbits;
+      p.shard = s.k;
+      p.nshards = g->P;
+      p.packed = g->packed;
+      p.sbits = g->sbits;
+      p.flags = g->opt.flags;
+      p.slots = s.d_slots;
+      for (uint32_t j = 0; j < g->P && j < (uint32_t)kMaxShards; ++j)
+        p.peer_slots[j] = g->multiproc ? s.peer[j] : g->sh[j].d_slots;
+      p.slot_stride = g->slot_stride;
+      p.bstride = (uint32_t)g->bstride;
+      p.nrep = g->nrep;
+      p.exch_base = g->exch_base;
+      p.sources = s.d_sources;
+      p.nsolve = k;
+      p.dist_out = s.d_dist;
+      p.pred_out = s.d_pred;
+      p.visit_order = s.d_visit;
+      p.round_ns = s.d_round_ns;
+      p.info = s.d_info;
+      p.timeout_ns = g->opt.timeout_ms * 1000000ull;
+      if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
+      ps.push_back(p);
+    }
+    Shard& s0 = g->sh[grp[0]];
+    CK(cudaSetDevice(s0.device));
+    CK(launch_kernel(g, grp, (void*)s0.fn, k, ps, nullptr, 0, nullptr));
+    for (uint32_t li : grp) CK(cudaEventRecord(g->sh[li].ev1, g->sh[li].stream));
   }
   for (cudaEvent_t e : reset_ev) cudaEventDestroy(e);
   g->pending = k;
@@ -1567,12 +1639,11 @@ int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round) {
   if (g->multiproc && !g->connected) return fail(SSSP_ERR_BAD_ARG, "shard not connected");
   if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
   const uint32_t np = g->sh[0].NP;
-  ProbeFn fn = g->cluster ? get_cluster_probe((int)g->sh[0].NW, g->sh[0].hier)
-                          : get_grid_probe((int)np);
-  if (!fn) return fail(SSSP_ERR_UNSUPPORTED, "no probe instance");
-  if (g->cluster && g->sh[0].C > 8)
-    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
-  std::vector<uint64_t*> d_ns(g->sh.size(), nullptr);
+  auto probe_fn = [&](int device) -> ProbeFn {  // a launch with several shards: the MS instance
+    const bool ms = shards_on_device(g, device) > 1;
+    return g->cluster ? get_cluster_probe((int)g->sh[0].NW, g->sh[0].hier, ms)
+                      : get_grid_probe((int)np, ms);
+  };
   std::vector<cudaEvent_t> reset_ev;
   if (!g->multiproc) {
     g->exch_base = 0;
@@ -1585,41 +1656,54 @@ int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round) {
       reset_ev.push_back(e);
     }
   }
-  for (size_t i = 0; i < g->sh.size(); ++i) {
-    Shard& s = g->sh[i];
-    CK(cudaSetDevice(s.device));
-    for (cudaEvent_t e : reset_ev) CK(cudaStreamWaitEvent(s.stream, e, 0));
-    CK(cudaMalloc(&d_ns[i], sizeof(uint64_t)));
-    CK(cudaMemsetAsync(s.d_info, 0, 4 * sizeof(uint64_t), s.stream));
-    ScanParams p{};
-    p.G = s.G;
-    p.vbits = g->vbits;
-    p.shard = s.k;
-    p.nshards = g->P;
-    p.slots = s.d_slots;
-    for (uint32_t j = 0; j < g->P && j < (uint32_t)kMaxShards; ++j)
-      p.peer_slots[j] = g->multiproc ? s.peer[j] : g->sh[j].d_slots;
-    p.slot_stride = g->slot_stride;
-    p.bstride = (uint32_t)g->bstride;
-    p.nrep = g->nrep;
-    p.exch_base = g->exch_base;
-    p.info = s.d_info;
-    p.timeout_ns = g->opt.timeout_ms * 1000000ull;
-    CK(launch_kernel(g, s, (void*)fn, 1, p, &rounds, 1, d_ns[i]));
+  const auto groups = device_groups(g);
+  std::vector<uint64_t*> d_ns(groups.size(), nullptr);
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    std::vector<ScanParams> ps;
+    for (uint32_t li : groups[gi]) {
+      Shard& s = g->sh[li];
+      CK(cudaSetDevice(s.device));
+      for (cudaEvent_t e : reset_ev) CK(cudaStreamWaitEvent(s.stream, e, 0));
+      CK(cudaMemsetAsync(s.d_info, 0, 4 * sizeof(uint64_t), s.stream));
+      ScanParams p{};
+      p.G = s.G;
+      p.vbits = g->vbits;
+      p.shard = s.k;
+      p.nshards = g->P;
+      p.slots = s.d_slots;
+      for (uint32_t j = 0; j < g->P && j < (uint32_t)kMaxShards; ++j)
+        p.peer_slots[j] = g->multiproc ? s.peer[j] : g->sh[j].d_slots;
+      p.slot_stride = g->slot_stride;
+      p.bstride = (uint32_t)g->bstride;
+      p.nrep = g->nrep;
+      p.exch_base = g->exch_base;
+      p.info = s.d_info;
+      p.timeout_ns = g->opt.timeout_ms * 1000000ull;
+      ps.push_back(p);
+    }
+    CK(cudaSetDevice(g->sh[groups[gi][0]].device));
+    ProbeFn fn = probe_fn(g->sh[groups[gi][0]].device);
+    if (!fn) return fail(SSSP_ERR_UNSUPPORTED, "no probe instance");
+    if (g->cluster && g->sh[0].C > 8)
+      CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(cudaMalloc(&d_ns[gi], groups[gi].size() * sizeof(uint64_t)));  // [local shard]
+    CK(launch_kernel(g, groups[gi], (void*)fn, 1, ps, &rounds, 1, d_ns[gi]));
   }
   double worst = 0;
   uint64_t last = 0;
-  for (size_t i = 0; i < g->sh.size(); ++i) {
-    Shard& s = g->sh[i];
-    CK(cudaSetDevice(s.device));
-    CK(cudaStreamSynchronize(s.stream));
-    uint64_t ns = 0, info[4];
-    CK(cudaMemcpy(&ns, d_ns[i], sizeof(ns), cudaMemcpyDeviceToHost));
-    CK(cudaMemcpy(info, s.d_info, sizeof(info), cudaMemcpyDeviceToHost));
-    cudaFree(d_ns[i]);
-    if (ns == ~0ull) return fail(SSSP_ERR_TIMEOUT, "probe watchdog fired");
-    worst = std::max(worst, ns * 1e-9 / rounds);
-    last = std::max(last, info[1]);
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    for (size_t li = 0; li < groups[gi].size(); ++li) {
+      Shard& s = g->sh[groups[gi][li]];
+      CK(cudaSetDevice(s.device));
+      CK(cudaStreamSynchronize(s.stream));
+      uint64_t ns = 0, info[4];
+      CK(cudaMemcpy(&ns, d_ns[gi] + li, sizeof(ns), cudaMemcpyDeviceToHost));
+      CK(cudaMemcpy(info, s.d_info, sizeof(info), cudaMemcpyDeviceToHost));
+      if (ns == ~0ull) return fail(SSSP_ERR_TIMEOUT, "probe watchdog fired");
+      worst = std::max(worst, ns * 1e-9 / rounds);
+      last = std::max(last, info[1]);
+    }
+    cudaFree(d_ns[gi]);
   }
   for (cudaEvent_t e : reset_ev) cudaEventDestroy(e);
   if (g->multiproc) g->exch_base = last + 1;
