@@ -33,6 +33,7 @@
 #include <cooperative_groups.h>
 
 #include <cstdint>
+#include <type_traits>
 
 #include "scan_kernel.cuh"
 
@@ -74,7 +75,13 @@ struct BucketParams {
   uint32_t T;           // positions per CTA
   uint32_t nshards, loc_n;
   uint32_t* peer_bitmap[kMaxShards];  // every shard's [2][nshards*row_stride/32] (self incl.)
-  uint32_t* peer_ctrl[kMaxShards];    // every shard's [2][3][nshards*G]: tile lmin, cand, uns
+  uint32_t* peer_ctrl[kMaxShards];    // every shard's [2][4][nshards*G]: tile lmin, cand, open, finite
+  uint32_t wmin;        // smallest finite off-diagonal weight of the whole graph (>= 1)
+  uint32_t push_ldg;    // 1: push rows through registers (LDG) instead of bulk copies (A/B)
+  uint32_t push_depth16;  // LDG push: one 16-deep batch for classes of <= 16 rows per row group
+  uint32_t owner_pieces; // pull steps whose largest per-tile pull is <= this many 32 KB
+                         // pieces (2 = all in flight at once) run on the column owners
+                         // (no combine barrier); 0 = never
   // Cross-launch barrier (nlocal < nshards): launch counters, by global shard.
   // The leader of every launch adds nlocal to EVERY shard's counter once per
   // barrier; a launch waits on the counter of its first shard.
@@ -147,6 +154,39 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// Bulk (TMA-engine) global -> shared copies completing on an mbarrier
+// (cp.async.bulk -> UBLKCP, expect_tx -> SYNCS.ARRIVE.TRANS64): a row slice
+// is one copy instruction, so every row of a class is in flight at once
+// instead of the 8 16 B loads a thread can keep outstanding.
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n .reg .pred P1;\n WAIT_%=:\n"
+      " mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      " @!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(bar)), "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+// generic-proxy accesses of a shared buffer before async-proxy (bulk) writes to it
+__device__ __forceinline__ void fence_proxy_async() {
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+}
+
 // shared- or global-memory atomic minimum of a packed key
 __device__ __forceinline__ void smem_min(uint32_t* a, uint32_t v) { atomicMin(a, v); }
 __device__ __forceinline__ void smem_min(uint64_t* a, uint64_t v) {
@@ -167,6 +207,8 @@ __device__ __forceinline__ K warp_min_key(K k) {
     return ((uint64_t)a << 32) | b;
   }
 }
+
+__device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 constexpr int kBucketThreads = 256;
 
@@ -224,8 +266,8 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   uint32_t* schunk = sub + bucket_round4(words);
   K* scomb = reinterpret_cast<K*>(schunk + kBucketChunk);
   __shared__ uint32_t s_red[kBucketThreads / 32];
-  __shared__ uint32_t s_red2[kBucketThreads / 32], s_red3[kBucketThreads / 32];
-  __shared__ uint32_t s_cnt[2];
+  __shared__ uint32_t s_red2[kBucketThreads / 32], s_red3[kBucketThreads / 32], s_red4[kBucketThreads / 32], s_red5[kBucketThreads / 32];
+  __shared__ uint32_t s_cnt[3];
 
   const uint32_t tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const uint32_t me = shard * Gs + bx;    // global tile id
@@ -235,7 +277,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   const W* adjT = static_cast<const W*>(S.adjT);
   const uint32_t TPR = T * sizeof(W) / 16;  // threads per row slice
   const uint32_t RG = kBucketThreads / TPR; // row groups
-  // global per-step arrays: ctrl = [2][3][G] (lmin, candidates, unsettled)
+  // global per-step arrays: ctrl = [2][4][G] (lmin, candidates, open, finite)
   uint32_t* const glob = at(p.peer_ctrl[shard]);
   const uint32_t* const gbm = at(p.peer_bitmap[shard]);
   K* const pkey = at(static_cast<K*>(S.pkey));
@@ -243,6 +285,43 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   auto gvid = [&](uint32_t g) -> uint32_t {
     const uint32_t j = g >> (p.qbits + p.lbits);  // row_stride = Q*L = 2^(qbits+lbits)
     return j * p.loc_n + pos_to_vid(g & ((1u << (p.qbits + p.lbits)) - 1u), p.Q, p.lbits, p.qbits);
+  };
+
+  // Minimum (w, u) key over the class members of one 16 B chunk of a
+  // transposed row: `bits` = the B_d bits of its CPT positions, vid0 = the
+  // vertex of its first position (consecutive positions of one participant:
+  // vertex ids step by Q).
+  auto chunk_min = [&](const uint4 v4m, uint32_t bits, uint32_t vid0) -> K {
+    const uint32_t wd[4] = {v4m.x, v4m.y, v4m.z, v4m.w};
+    if constexpr (sizeof(W) == 1) {
+      // u8, branch-free: the chunk's minimum (w, position) pair on the
+      // native 16x2 min.  Non-class bytes -> 0xFF (INF); one PRMT packs
+      // two bytes with their in-chunk index as (w << 8 | cc) lanes; the
+      // min lane gives the smallest w at the lowest cc = lowest vertex id
+      // (ids rise with cc).  (A data-dependent skip here measured slower.)
+      uint32_t lanes[8];
+#pragma unroll
+      for (int k2 = 0; k2 < 4; ++k2) {
+        const uint32_t b4 = (bits >> (4 * k2)) & 0xFu;
+        const uint32_t mw = wd[k2] | ~(((b4 * 0x00204081u) & 0x01010101u) * 0xFFu);
+        const uint32_t ccs = 0x03020100u + 0x04040404u * (uint32_t)k2;
+        lanes[2 * k2] = __byte_perm(mw, ccs, 0x1504u);
+        lanes[2 * k2 + 1] = __byte_perm(mw, ccs, 0x3726u);
+      }
+      uint32_t mv = __vminu2(__vminu2(__vminu2(lanes[0], lanes[1]), __vminu2(lanes[2], lanes[3])),
+                             __vminu2(__vminu2(lanes[4], lanes[5]), __vminu2(lanes[6], lanes[7])));
+      mv = min(mv & 0xFFFFu, mv >> 16);
+      return (K)(((mv >> 8) << 24) | (vid0 + (mv & 0xFFu) * p.Q));
+    } else {
+      K run = KT::kNone;
+#pragma unroll
+      for (int cc = 0; cc < CPT; ++cc) {
+        const K kk = ((bits >> cc) & 1u) ? chunk_key<W>(wd[(cc * sizeof(W)) / 4], cc, vid0 + cc * p.Q)
+                                          : KT::kNone;
+        run = kk < run ? kk : run;
+      }
+      return run;
+    }
   };
 
   uint32_t ntr = 0;
@@ -258,6 +337,13 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   // all nshards arrivals on its own, then releases its CTAs: nshards NVLink
   // atomics per launch per barrier, not one per CTA.  Every counter continues
   // across launches (bar_epoch), so nothing is reset between solves.
+  __shared__ __align__(8) uint64_t s_mbar[2];  // bulk-copy completion (stage buffers 0/1)
+  uint32_t mph = 0;                             // their phase parities (bit per buffer)
+  if (tid == 0) {
+    mbar_init(&s_mbar[0], 1);
+    mbar_init(&s_mbar[1], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   __shared__ uint32_t s_fail;
   if (tid == 0) s_fail = 0;
   uint64_t nbar = 0;
@@ -308,29 +394,42 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   };
 
   // Publishes this tile's minimum, candidate bitmap and counts for step `s`.
-  auto publish = [&](uint32_t par) {
-    uint32_t m = DINF, uns = 0;
+  // A column whose dist is <= fb = (lowest possible next class) + wmin is
+  // FINAL: every later class d' relaxes it with d' + w >= fb, which never
+  // beats it under the strict '<' (serial.hpp:56), so neither dist nor pred
+  // can change.  Only the other ("open") unsettled columns are published for
+  // pull steps and counted for the push/pull choice and the end test.
+  auto publish = [&](uint32_t par, uint32_t fb) {
+    uint32_t m = DINF, nopen = 0, nfin = 0;
     for (uint32_t col = tid; col < T; col += kBucketThreads)
       if (!((ssettled[col >> 5] >> (col & 31)) & 1u)) {
-        m = min(m, sdist[col]);
-        ++uns;
+        const uint32_t dv = sdist[col];
+        m = min(m, dv);
+        nopen += dv > fb ? 1u : 0u;
+        nfin += dv != DINF ? 1u : 0u;
       }
     m = __reduce_min_sync(0xFFFFFFFFu, m);
-    uns = __reduce_add_sync(0xFFFFFFFFu, uns);
+    nopen = __reduce_add_sync(0xFFFFFFFFu, nopen);
+    nfin = __reduce_add_sync(0xFFFFFFFFu, nfin);
     if (lane == 0) s_red[warp] = m;
-    if (tid < 2) s_cnt[tid] = 0;
+    if (tid < 3) s_cnt[tid] = 0;
     __syncthreads();
-    if (lane == 0) atomicAdd(&s_cnt[1], uns);
+    if (lane == 0) {
+      atomicAdd(&s_cnt[1], nopen);
+      atomicAdd(&s_cnt[2], nfin);
+    }
     for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) m = min(m, s_red[w2]);
     // candidate bitmap word i (columns 32i..32i+31) = one ballot of warp i % 8
     for (uint32_t i = warp; i < TW; i += kBucketThreads / 32) {
       const uint32_t sm = ssettled[i];
-      const uint32_t cm =
-          __ballot_sync(0xFFFFFFFFu, m != DINF && !((sm >> lane) & 1u) && sdist[i * 32 + lane] == m);
+      const bool live = !((sm >> lane) & 1u);
+      const uint32_t dv = sdist[i * 32 + lane];
+      const uint32_t cm = __ballot_sync(0xFFFFFFFFu, m != DINF && live && dv == m);
+      const uint32_t om = __ballot_sync(0xFFFFFFFFu, live && dv > fb);
       if (lane < p.nshards)  // remote shards: P2P stores
         at(p.peer_bitmap[lane])[par * words + me * TW + i] = cm;
       if (lane == 31) {
-        ubm[par * lwords + bx * TW + i] = ~sm;  // local only (pull work list)
+        ubm[par * lwords + bx * TW + i] = om;  // local only (pull work list)
         if (cm) atomicAdd(&s_cnt[0], __popc(cm));
       }
     }
@@ -338,10 +437,15 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
     __syncthreads();
     if (tid < p.nshards) {
       uint32_t* c = at(p.peer_ctrl[tid]);
-      c[(par * 3 + 0) * G + me] = m;
-      c[(par * 3 + 1) * G + me] = s_cnt[0];
-      c[(par * 3 + 2) * G + me] = s_cnt[1];
+      c[(par * 4 + 0) * G + me] = m;
+      c[(par * 4 + 1) * G + me] = s_cnt[0];
+      c[(par * 4 + 2) * G + me] = s_cnt[1];
+      c[(par * 4 + 3) * G + me] = s_cnt[2];
     }
+  };
+  // lowest possible next class + wmin (64-bit: no wrap), capped below INF
+  auto final_bound = [&](uint32_t dlast) -> uint32_t {
+    return (uint32_t)umin64((uint64_t)dlast + 1u + p.wmin, (uint64_t)DINF - 1u);
   };
 
   // ---- init: dist = INF, pred = NONE, padding settled (serial.hpp:32-36),
@@ -371,7 +475,8 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   // its final barrier, and a step's extra (pull) barrier never lets a publish
   // overwrite a buffer some CTA may still read.
   if (MULTI && bx == 0 && tid == 0) p.done[slot] = 0;  // read after the first barrier
-  publish((uint32_t)(bar_base & 1ull));
+  uint32_t fb = final_bound(0);  // class 0 = {source} at distance 0
+  publish((uint32_t)(bar_base & 1ull), fb);
   barrier();
   stamp();
 
@@ -380,7 +485,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   uint32_t step = 1;
   while (!failed) {
     const uint32_t par = (uint32_t)((bar_base + nbar - 1) & 1ull);
-    bool relax = false, pull = false;
+    bool relax = false, pull = false, owner = false;
     uint32_t dk = 0, bcount = 0, ucount = 0;
     if (!done) {
       // ---- the class: d = min over tiles, B_d = candidates of the tiles at d.
@@ -393,13 +498,14 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         const uint32_t* ub = ubm + par * lwords;
         for (uint32_t i = tid; i < lwords; i += kBucketThreads) sub[i] = __ldcg(&ub[i]);
       }
-      uint32_t lm_r[4], cc_r[4], uu_r[4];  // G <= 4 * kBucketThreads tiles (host-checked)
+      uint32_t lm_r[4], cc_r[4], uu_r[4], ff_r[4];  // G <= 4 * kBucketThreads tiles (host-checked)
 #pragma unroll
       for (int k2 = 0; k2 < 4; ++k2) {
         const uint32_t c = tid + k2 * kBucketThreads;
-        lm_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 0) * G + c]) : DINF;
-        cc_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 1) * G + c]) : 0u;
-        uu_r[k2] = c < G ? __ldcg(&glob[(par * 3 + 2) * G + c]) : 0u;
+        lm_r[k2] = c < G ? __ldcg(&glob[(par * 4 + 0) * G + c]) : DINF;
+        cc_r[k2] = c < G ? __ldcg(&glob[(par * 4 + 1) * G + c]) : 0u;
+        uu_r[k2] = c < G ? __ldcg(&glob[(par * 4 + 2) * G + c]) : 0u;
+        ff_r[k2] = c < G ? __ldcg(&glob[(par * 4 + 3) * G + c]) : 0u;
       }
       uint32_t d = DINF;
 #pragma unroll
@@ -415,17 +521,24 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       if (d == DINF) {  // uniform within the slot: every CTA reads the same values
         done = true;
       } else {
-        uint32_t uns = 0;
+        uint32_t uns = 0, fin = 0, mopen = 0;  // mopen: most open columns left in one tile
 #pragma unroll
         for (int k2 = 0; k2 < 4; ++k2) {
-          bcount += lm_r[k2] == d ? cc_r[k2] : 0u;
+          const uint32_t cls = lm_r[k2] == d ? cc_r[k2] : 0u;
+          bcount += cls;
           uns += uu_r[k2];
+          fin += ff_r[k2];
+          mopen = max(mopen, uu_r[k2] - (d > fb ? cls : 0u));
         }
         bcount = __reduce_add_sync(0xFFFFFFFFu, bcount);
         uns = __reduce_add_sync(0xFFFFFFFFu, uns);
+        fin = __reduce_add_sync(0xFFFFFFFFu, fin);
+        mopen = __reduce_max_sync(0xFFFFFFFFu, mopen);
         if (lane == 0) {
           s_red2[warp] = bcount;
           s_red3[warp] = uns;
+          s_red4[warp] = fin;
+          s_red5[warp] = mopen;
         }
         // mask the staged bitmap to the tiles at d
         for (uint32_t i = tid; i < words; i += kBucketThreads)
@@ -433,23 +546,48 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         __syncthreads();
         bcount = 0;
         uns = 0;
+        fin = 0;
+        mopen = 0;
         for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) {
           bcount += s_red2[w2];
           uns += s_red3[w2];
+          fin += s_red4[w2];
+          mopen = max(mopen, s_red5[w2]);
         }
-        ucount = uns - bcount;  // unsettled after settling B_d
+        // open columns left after settling B_d (B_d is open iff d > fb: all
+        // its members hold dist d)
+        ucount = uns - (d > fb ? bcount : 0u);
         // settle my candidates if my tile is in the class
         for (uint32_t i = tid; i < TW; i += kBucketThreads) ssettled[i] |= sbm[me * TW + i];
         __syncthreads();
         stamp();
         ++step;
-        settled += bcount;
         if (ucount == 0) {
-          done = true;  // nothing left to relax (the last class needs no rows)
+          // nothing left any class could lower: every remaining finite column
+          // is final (it would be elected later without relaxing anything)
+          settled += fin;
+          done = true;
         } else {
+          settled += bcount;
           relax = true;
           pull = adjT != nullptr && ucount < bcount;
+          // small pulls run on the column owners: no partial minima to
+          // combine, so no extra barrier (uniform: every CTA read the same counts)
+          {
+            const uint64_t rowB = p.adjT_stride * sizeof(W);
+            const uint64_t ppr = (rowB + kBucketChunk * 2 - 1) / (kBucketChunk * 2);  // 32 KB pieces
+            owner = pull && (uint64_t)mopen * ppr <= p.owner_pieces;
+          }
           dk = d;
+          fb = final_bound(d);
+          // push: a tile none of whose columns is open after B_d skips the rows
+          if (!pull) {
+            const uint32_t lim = (uint32_t)umin64((uint64_t)d + p.wmin, (uint64_t)DINF - 1u);
+            bool open = false;
+            for (uint32_t col = tid; col < T; col += kBucketThreads)
+              open |= !((ssettled[col >> 5] >> (col & 31)) & 1u) && sdist[col] > lim;
+            relax = __syncthreads_or(open);
+          }
         }
       }
     }
@@ -463,13 +601,14 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
 #pragma unroll
       for (int j = 0; j < CPT; ++j) best[j] = KT::kNone;
       // enumerate B_d in ascending order with one block scan per pass: a
-      // class that fits the id chunk takes a single pass over all words (up
-      // to 8 per thread), otherwise passes of 2 words per thread (<=
-      // kBucketChunk ids each)
+      // class of <= kIdCap ids takes a single pass over all words (up to 8
+      // per thread), otherwise passes of one word per thread (<= kIdCap ids
+      // each); the rest of the chunk region stages the row slices
       constexpr uint32_t WMAX = 8;
-      const uint32_t wpt = (bcount <= (uint32_t)kBucketChunk && words <= WMAX * kBucketThreads)
+      constexpr uint32_t kIdCap = kBucketChunk / 2;
+      const uint32_t wpt = (bcount <= kIdCap && words <= WMAX * kBucketThreads)
                                ? (words + kBucketThreads - 1) / kBucketThreads
-                               : 2u;
+                               : 1u;
       for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads * wpt) {
         const uint32_t w0 = wbase + tid * wpt;
         uint32_t bw[WMAX];
@@ -498,31 +637,88 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         for (uint32_t k2 = 0; k2 < WMAX; ++k2)
           for (uint32_t m = bw[k2]; m; m &= m - 1)
             schunk[o++] = gvid((w0 + k2) * 32 + (__ffs(m) - 1));
-        __syncthreads();
-        // batches of 8 rows: all 8 loads are issued before any is consumed
-        for (uint32_t r0 = rg; r0 < tot; r0 += 8 * RG) {
-          uint32_t ub[8];
-          uint4 vb[8];
+        if (!p.push_ldg) {
+          // Row slices staged by bulk copies: thread t issues the copies of
+          // rows t, t+256, ... of a batch (one UBLKCP per row slice); a batch
+          // is every row of the pass when it fits the stage, else the stage
+          // is split in two and batch b+2 is issued while b+1 is in flight.
+          const uint32_t TB = T * (uint32_t)sizeof(W);
+          uint8_t* const stage = reinterpret_cast<uint8_t*>(schunk + bucket_round4(tot));
+          const uint32_t SB = (kBucketChunk - bucket_round4(tot)) * 4u;
+          const uint32_t RB = tot * TB <= SB ? tot : (SB / 2u) / TB;  // rows per batch
+          const uint32_t nbt = (tot + RB - 1u) / RB;
+          auto buf = [&](uint32_t b) { return stage + (size_t)(b & 1u) * RB * TB; };
+          auto issue = [&](uint32_t b) {
+            const uint32_t r0 = b * RB, nr = min(RB, tot - r0);
+            if (tid == 0) mbar_arrive_expect_tx(&s_mbar[b & 1u], nr * TB);
+            for (uint32_t r = tid; r < nr; r += kBucketThreads)
+              bulk_g2s(buf(b) + r * TB,
+                       reinterpret_cast<const uint8_t*>(adj + (size_t)schunk[r0 + r] * p.row_stride + p0),
+                       TB, &s_mbar[b & 1u]);
+          };
+          fence_proxy_async();  // earlier generic accesses of the stage bytes
+          __syncthreads();
+          issue(0);
+          if (nbt > 1) issue(1);
+          for (uint32_t b = 0; b < nbt; ++b) {
+            mbar_wait(&s_mbar[b & 1u], (mph >> (b & 1u)) & 1u);
+            mph ^= 1u << (b & 1u);
+            const uint8_t* sb = buf(b);
+            const uint32_t r0 = b * RB, nr = min(RB, tot - r0);
+#pragma unroll 4
+            for (uint32_t r = rg; r < nr; r += RG) {
+              const uint4 v = *reinterpret_cast<const uint4*>(sb + r * TB + ct * 16);
+              const uint32_t u = schunk[r0 + r];
+              const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            const uint32_t r = r0 + m * RG;
-            ub[m] = r < tot ? schunk[r] : 0xFFFFFFFFu;
-            if (r < tot)
-              vb[m] = __ldg(reinterpret_cast<const uint4*>(
-                  reinterpret_cast<const uint8_t*>(adj + (size_t)ub[m] * p.row_stride + p0) + ct * 16));
-          }
-#pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            if (ub[m] == 0xFFFFFFFFu) break;
-            const uint32_t wd[4] = {vb[m].x, vb[m].y, vb[m].z, vb[m].w};
-#pragma unroll
-            for (int j = 0; j < CPT; ++j) {
-              // INF weights make keys above every finite one
-              const K k = chunk_key<W>(wd[(j * sizeof(W)) / 4], j, ub[m]);
-              best[j] = k < best[j] ? k : best[j];
+              for (int j = 0; j < CPT; ++j) {
+                const K k = chunk_key<W>(wd[(j * sizeof(W)) / 4], j, u);
+                best[j] = k < best[j] ? k : best[j];
+              }
+            }
+            if (b + 2 < nbt) {
+              fence_proxy_async();
+              __syncthreads();  // batch b's buffer is free
+              issue(b + 2);
             }
           }
+          __syncthreads();
+          continue;
         }
+        __syncthreads();
+        // batches of DEPTH rows per thread: all loads of a batch are issued
+        // before any is consumed; a class of <= 16 rows per row group takes
+        // one 16-deep batch (one memory round trip), larger ones 8-deep batches
+        auto batches = [&](auto depth_c) {
+          constexpr int DEPTH = decltype(depth_c)::value;
+          for (uint32_t r0 = rg; r0 < tot; r0 += DEPTH * RG) {
+            uint32_t ub[DEPTH];
+            uint4 vb[DEPTH];
+#pragma unroll
+            for (int m = 0; m < DEPTH; ++m) {
+              const uint32_t r = r0 + m * RG;
+              ub[m] = r < tot ? schunk[r] : 0xFFFFFFFFu;
+              if (r < tot)
+                vb[m] = __ldg(reinterpret_cast<const uint4*>(
+                    reinterpret_cast<const uint8_t*>(adj + (size_t)ub[m] * p.row_stride + p0) + ct * 16));
+            }
+#pragma unroll
+            for (int m = 0; m < DEPTH; ++m) {
+              if (ub[m] == 0xFFFFFFFFu) break;
+              const uint32_t wd[4] = {vb[m].x, vb[m].y, vb[m].z, vb[m].w};
+#pragma unroll
+              for (int j = 0; j < CPT; ++j) {
+                // INF weights make keys above every finite one
+                const K k = chunk_key<W>(wd[(j * sizeof(W)) / 4], j, ub[m]);
+                best[j] = k < best[j] ? k : best[j];
+              }
+            }
+          }
+        };
+        if (p.push_depth16 && tot > 8 * RG && tot <= 16 * RG)
+          batches(std::integral_constant<int, 16>{});
+        else
+          batches(std::integral_constant<int, 8>{});
         __syncthreads();
       }
 #pragma unroll
@@ -541,6 +737,85 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
             sdist[col] = cand;
             spred[col] = KT::u(k);
           }
+        }
+      }
+      __syncthreads();
+    } else if (relax && owner) {
+      // ---- PULL on the column owners (small pulls): a CTA streams the
+      // transposed rows of its own open columns through the stage by bulk
+      // copies (pieces of <= 32 KB, two in flight) and folds each column's
+      // (w, u) minimum itself -- nothing to combine, no extra barrier.
+      pulled += ucount;
+      const uint32_t lim = (uint32_t)umin64((uint64_t)dk + p.wmin, (uint64_t)DINF - 1u);
+      uint32_t* ocol = reinterpret_cast<uint32_t*>(scomb);        // open columns of the tile
+      K* skey = reinterpret_cast<K*>(ocol + ((T + 3u) & ~3u));    // [2][8] warp minima
+      if (tid == 0) s_cnt[0] = 0;
+      __syncthreads();
+      for (uint32_t col = tid; col < T; col += kBucketThreads)
+        if (!((ssettled[col >> 5] >> (col & 31)) & 1u) && sdist[col] > lim)
+          ocol[atomicAdd(&s_cnt[0], 1u)] = col;
+      fence_proxy_async();  // earlier generic accesses of the stage bytes
+      __syncthreads();
+      const uint32_t no = s_cnt[0];
+      const uint32_t rowB = (uint32_t)(p.adjT_stride * sizeof(W));
+      const uint32_t PB = min(rowB, (uint32_t)kBucketChunk * 2u);  // half the stage
+      const uint32_t ppr = (rowB + PB - 1u) / PB;                  // pieces per row
+      const uint32_t nit = no * ppr;
+      uint8_t* const stage = reinterpret_cast<uint8_t*>(schunk);
+      auto issue = [&](uint32_t it) {
+        const uint32_t c = ocol[it / ppr], pc = it % ppr;
+        const uint32_t pos = p0 + c;
+        const uint32_t v = p.adjT_by_pos ? pos : pos_to_vid(pos, p.Q, p.lbits, p.qbits);
+        const uint32_t bytes = min(PB, rowB - pc * PB);
+        const uint8_t* src = reinterpret_cast<const uint8_t*>(adjT + (size_t)v * p.adjT_stride) +
+                             (size_t)pc * PB;
+        uint8_t* dst = stage + (it & 1u) * PB;
+        if (tid == 0) mbar_arrive_expect_tx(&s_mbar[it & 1u], bytes);
+        for (uint32_t q = tid; q * 4096u < bytes; q += kBucketThreads)
+          bulk_g2s(dst + q * 4096u, src + q * 4096u, min(4096u, bytes - q * 4096u), &s_mbar[it & 1u]);
+      };
+      if (nit > 0) issue(0);
+      if (nit > 1) issue(1);
+      K run = KT::kNone;
+      for (uint32_t it = 0; it < nit; ++it) {
+        mbar_wait(&s_mbar[it & 1u], (mph >> (it & 1u)) & 1u);
+        mph ^= 1u << (it & 1u);
+        const uint32_t pc = it % ppr;
+        const uint32_t nch = min(PB, rowB - pc * PB) / 16u;
+        const uint4* sp = reinterpret_cast<const uint4*>(stage + (it & 1u) * PB);
+        const uint32_t pbase = pc * (PB / (uint32_t)sizeof(W));  // first position of the piece
+        for (uint32_t ch = tid; ch < nch; ch += kBucketThreads) {
+          const uint32_t pos0 = pbase + ch * CPT;
+          const uint32_t bits = (sbm[pos0 >> 5] >> (pos0 & 31)) & ((1u << CPT) - 1u);
+          if (!bits) continue;
+          const K kk = chunk_min(sp[ch], bits, gvid(pos0));
+          run = kk < run ? kk : run;
+        }
+        if (pc == ppr - 1u) {  // the column's last piece: block minimum, apply
+          const uint32_t cpar = (it / ppr) & 1u;
+          K k = warp_min_key(run);
+          if (lane == 0) skey[cpar * 8 + warp] = k;
+          __syncthreads();
+          if (tid == 0) {
+            for (uint32_t w2 = 1; w2 < kBucketThreads / 32; ++w2) {
+              const K x = skey[cpar * 8 + w2];
+              k = x < k ? x : k;
+            }
+            const uint32_t col = ocol[it / ppr];
+            if (k != KT::kNone && KT::w(k) != WINF) {
+              const uint32_t cand = dk + KT::w(k);
+              if (cand < sdist[col]) {
+                sdist[col] = cand;
+                spred[col] = KT::u(k);
+              }
+            }
+          }
+          run = KT::kNone;
+        }
+        if (it + 2 < nit) {
+          fence_proxy_async();
+          __syncthreads();  // piece it's buffer is free
+          issue(it + 2);
         }
       }
       __syncthreads();
@@ -670,37 +945,8 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
           const uint32_t bits = (sbm[pos0 >> 5] >> (pos0 & 31)) & ((1u << CPT) - 1u);
           if (!bits) continue;
           // consecutive positions of one participant: vertex ids step by Q
-          const uint32_t vid0 = gvid(pos0);
-          const uint4 v4m = st[m * kBucketThreads + tid];
-          const uint32_t wd[4] = {v4m.x, v4m.y, v4m.z, v4m.w};
-          if constexpr (sizeof(W) == 1) {
-            // u8, branch-free: the chunk's minimum (w, position) pair on the
-            // native 16x2 min.  Non-class bytes -> 0xFF (INF); one PRMT packs
-            // two bytes with their in-chunk index as (w << 8 | cc) lanes; the
-            // min lane gives the smallest w at the lowest cc = lowest vertex id
-            // (ids rise with cc).  (A data-dependent skip here measured slower.)
-            uint32_t lanes[8];
-#pragma unroll
-            for (int k2 = 0; k2 < 4; ++k2) {
-              const uint32_t b4 = (bits >> (4 * k2)) & 0xFu;
-              const uint32_t mw = wd[k2] | ~(((b4 * 0x00204081u) & 0x01010101u) * 0xFFu);
-              const uint32_t ccs = 0x03020100u + 0x04040404u * (uint32_t)k2;
-              lanes[2 * k2] = __byte_perm(mw, ccs, 0x1504u);
-              lanes[2 * k2 + 1] = __byte_perm(mw, ccs, 0x3726u);
-            }
-            uint32_t mv = __vminu2(__vminu2(__vminu2(lanes[0], lanes[1]), __vminu2(lanes[2], lanes[3])),
-                                   __vminu2(__vminu2(lanes[4], lanes[5]), __vminu2(lanes[6], lanes[7])));
-            mv = min(mv & 0xFFFFu, mv >> 16);
-            const K kk = ((mv >> 8) << 24) | (vid0 + (mv & 0xFFu) * p.Q);
-            run = kk < run ? kk : run;
-          } else {
-#pragma unroll
-            for (int cc = 0; cc < CPT; ++cc) {
-              const K kk = ((bits >> cc) & 1u) ? chunk_key<W>(wd[(cc * sizeof(W)) / 4], cc, vid0 + cc * p.Q)
-                                                : KT::kNone;
-              run = kk < run ? kk : run;
-            }
-          }
+          const K kk = chunk_min(st[m * kBucketThreads + tid], bits, gvid(pos0));
+          run = kk < run ? kk : run;
         }
       }
       cp_async_wait<0>();
@@ -713,12 +959,12 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
     }
     // the pull's extra barrier (every partial minimum is in pkey); with
     // several slots every step has it, so all CTAs count the same barriers
-    if (pull || MULTI) {
+    if ((pull && !owner) || MULTI) {
       stamp();
       barrier();
       stamp();
     }
-    if (relax && pull) {
+    if (relax && pull && !owner) {
       for (uint32_t col = tid; col < T; col += kBucketThreads) {
         if ((ssettled[col >> 5] >> (col & 31)) & 1u) continue;
         const K k = ld_cg(&pkey[p0 + col]);
@@ -735,7 +981,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
     // ---- publish the next class's candidates, one barrier per class
     if (!done) {
       stamp();
-      publish((uint32_t)((bar_base + nbar) & 1ull));
+      publish((uint32_t)((bar_base + nbar) & 1ull), fb);
     } else if (MULTI && bx == 0 && tid == 0) {
       p.done[slot] = 1;  // read by every slot after the barrier
     }

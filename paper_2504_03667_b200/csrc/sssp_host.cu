@@ -718,7 +718,7 @@ int plan_bucket(sssp_graph* g) {
     }
     T *= 2;
   }
-  // exchange region: [barrier counter | epoch | ctrl [2][3][P*G] | bitmap [2][P*row_stride/32]
+  // exchange region: [barrier counter | epoch | ctrl [2][4][P*G] | bitmap [2][P*row_stride/32]
   //                   | local: unsettled bitmap [2][row_stride/32] | pull keys [row_stride] u64]
   const uint64_t GT = (uint64_t)g->bG * g->P;
   const uint64_t words = s0.row_stride / 32 * g->P;
@@ -727,7 +727,7 @@ int plan_bucket(sssp_graph* g) {
   g->epoch_off = 128;
   g->release_off = 192;
   g->ctrl_off = 256;
-  g->bm_off = (g->ctrl_off + 2 * 3 * GT * 4 + 255) & ~255ull;
+  g->bm_off = (g->ctrl_off + 2 * 4 * GT * 4 + 255) & ~255ull;
   g->ubm_off = (g->bm_off + 2 * words * 4 + 255) & ~255ull;
   g->pkey_off = (g->ubm_off + 2 * (s0.row_stride / 32) * 4 + 255) & ~255ull;
   g->region_bytes = (g->pkey_off + s0.row_stride * 8 + 255) & ~255ull;
@@ -951,6 +951,11 @@ cudaError_t launch_kernel(sssp_graph* g, const std::vector<uint32_t>& grp, void*
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* e = getenv(name);
+  return e && *e ? strtoull(e, nullptr, 10) : dflt;
+}
+
 // Enqueues one launch of k solves on every local shard.
 int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
   if (g->multiproc && !g->connected)
@@ -1007,6 +1012,15 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.T = wide ? g->bTb : g->bT;
         bp.nshards = g->P;
         bp.loc_n = (uint32_t)s0.loc_n;
+        bp.wmin = (uint32_t)std::min<uint64_t>(g->min_w, 0xFFFFFFFFull);
+        // A/B switches (read once per process): bulk-copy push,
+        // 16-deep register push, owner-pull limit (0 = balanced pulls only)
+        static const uint32_t k_push_ldg = env_u64("SSSP_PUSH_BULK", 0) ? 0u : 1u;
+        static const uint32_t k_depth16 = env_u64("SSSP_PUSH_DEPTH16", 0) ? 1u : 0u;
+        static const uint32_t k_owner = (uint32_t)env_u64("SSSP_OWNER_PULL_PIECES", 2);
+        bp.push_ldg = k_push_ldg;
+        bp.push_depth16 = k_depth16;
+        bp.owner_pieces = k_owner;
         for (uint32_t j = 0; j < g->P; ++j) {
           char* base = reinterpret_cast<char*>(g->multiproc ? (void*)s0.peer[j] : (void*)g->sh[j].d_slots) +
                        g->slots_bytes;
