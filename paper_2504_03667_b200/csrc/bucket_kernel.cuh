@@ -212,6 +212,14 @@ __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < 
 
 constexpr int kBucketThreads = 256;
 
+// A/B variants measured and rejected: the bulk-copy push and
+// the 16-deep register push.  Compiled only with -DSSSP_BUCKET_AB=1 so the
+// default instance keeps its code (and instruction-cache footprint) small.
+#ifndef SSSP_BUCKET_AB
+#define SSSP_BUCKET_AB 0
+#endif
+constexpr bool kBucketAB = SSSP_BUCKET_AB != 0;
+
 __host__ __device__ constexpr uint32_t bucket_round4(uint32_t x) { return (x + 3u) & ~3u; }
 
 // dynamic shared memory of bucket_kernel (keeps every region 16 B aligned)
@@ -325,8 +333,10 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   };
 
   uint32_t ntr = 0;
-  auto stamp = [&]() {
-    if (p.trace && me == 0 && slot == 0 && tid == 0 && ntr < 64) p.trace[ntr++] = globaltimer();
+  // trace entry = phase code << 56 | %globaltimer (CTA 0 of shard 0, debug)
+  auto stamp = [&](uint32_t code) {
+    if (p.trace && me == 0 && slot == 0 && tid == 0 && ntr < 64)
+      p.trace[ntr++] = ((uint64_t)code << 56) | (globaltimer() & ((1ull << 56) - 1));
   };
   // One barrier over every CTA of every shard.  All shards in this launch:
   // the cooperative grid barrier (1.29 us at 256 CTAs, the fastest measured
@@ -351,7 +361,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   const uint64_t t_start = globaltimer();
   const bool cross = p.nlocal < p.nshards;
   const uint64_t bar_base = cross ? *(volatile uint64_t*)p.bar_epoch : 0;
-  stamp();  // trace[0]: kernel start
+  stamp(0);  // trace[0]: kernel start
   auto spin_until = [&](const unsigned long long* a, unsigned long long target, bool sys) -> bool {
     unsigned long long v;
     uint32_t polls = 0;
@@ -442,6 +452,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       c[(par * 4 + 2) * G + me] = s_cnt[1];
       c[(par * 4 + 3) * G + me] = s_cnt[2];
     }
+    stamp(10);
   };
   // lowest possible next class + wmin (64-bit: no wrap), capped below INF
   auto final_bound = [&](uint32_t dlast) -> uint32_t {
@@ -475,10 +486,11 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   // its final barrier, and a step's extra (pull) barrier never lets a publish
   // overwrite a buffer some CTA may still read.
   if (MULTI && bx == 0 && tid == 0) p.done[slot] = 0;  // read after the first barrier
+  stamp(12);  // class-0 row slice loaded
   uint32_t fb = final_bound(0);  // class 0 = {source} at distance 0
   publish((uint32_t)(bar_base & 1ull), fb);
   barrier();
-  stamp();
+  stamp(1);
 
   bool done = false;  // this slot's solve has settled every reachable vertex
   uint64_t pushed = 1, pulled = 0, settled = 1;
@@ -517,6 +529,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       d = __reduce_min_sync(0xFFFFFFFFu, d);
       if (lane == 0) s_red[warp] = d;
       __syncthreads();
+      stamp(2);
       for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) d = min(d, s_red[w2]);
       if (d == DINF) {  // uniform within the slot: every CTA reads the same values
         done = true;
@@ -560,7 +573,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         // settle my candidates if my tile is in the class
         for (uint32_t i = tid; i < TW; i += kBucketThreads) ssettled[i] |= sbm[me * TW + i];
         __syncthreads();
-        stamp();
+        stamp(3);
         ++step;
         if (ucount == 0) {
           // nothing left any class could lower: every remaining finite column
@@ -637,7 +650,8 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         for (uint32_t k2 = 0; k2 < WMAX; ++k2)
           for (uint32_t m = bw[k2]; m; m &= m - 1)
             schunk[o++] = gvid((w0 + k2) * 32 + (__ffs(m) - 1));
-        if (!p.push_ldg) {
+        stamp(4);
+        if (kBucketAB && !p.push_ldg) {
           // Row slices staged by bulk copies: thread t issues the copies of
           // rows t, t+256, ... of a batch (one UBLKCP per row slice); a batch
           // is every row of the pass when it fits the stage, else the stage
@@ -715,11 +729,12 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
             }
           }
         };
-        if (p.push_depth16 && tot > 8 * RG && tot <= 16 * RG)
+        if (kBucketAB && p.push_depth16 && tot > 8 * RG && tot <= 16 * RG)
           batches(std::integral_constant<int, 16>{});
         else
           batches(std::integral_constant<int, 8>{});
         __syncthreads();
+        stamp(5);
       }
 #pragma unroll
       for (int j = 0; j < CPT; ++j) scomb[tid * CPT + j] = best[j];
@@ -740,6 +755,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         }
       }
       __syncthreads();
+      stamp(6);
     } else if (relax && owner) {
       // ---- PULL on the column owners (small pulls): a CTA streams the
       // transposed rows of its own open columns through the stage by bulk
@@ -819,6 +835,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         }
       }
       __syncthreads();
+      stamp(13);
     } else if (relax && pull) {
       // ---- PULL, balanced over the whole shard: U = this shard's unsettled
       // columns after B_d (the published unsettled bitmaps minus the class).
@@ -873,7 +890,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       }
       for (uint32_t i = tid; i < ncols; i += kBucketThreads) sk[i] = KT::kNone;
       __syncthreads();
-      stamp();
+      stamp(7);
       if (p.trace && tid == 0 && shard == 0 && slot == 0 && bx < 1024)  // per-CTA pull span (debug)
         p.trace[64 + 2 * bx] = globaltimer();
       // Two-stage cp.async pipeline: a thread's items are lo + tid + k*256;
@@ -960,9 +977,9 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
     // the pull's extra barrier (every partial minimum is in pkey); with
     // several slots every step has it, so all CTAs count the same barriers
     if ((pull && !owner) || MULTI) {
-      stamp();
+      stamp(8);
       barrier();
-      stamp();
+      stamp(1);
     }
     if (relax && pull && !owner) {
       for (uint32_t col = tid; col < T; col += kBucketThreads) {
@@ -980,13 +997,13 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
     }
     // ---- publish the next class's candidates, one barrier per class
     if (!done) {
-      stamp();
+      stamp(9);
       publish((uint32_t)((bar_base + nbar) & 1ull), fb);
     } else if (MULTI && bx == 0 && tid == 0) {
       p.done[slot] = 1;  // read by every slot after the barrier
     }
     barrier();
-    stamp();
+    stamp(1);
     if (MULTI) {  // all slots done: leave together (uniform)
       bool all = true;
       for (uint32_t s2 = 0; s2 < p.nslots; ++s2) all &= __ldcg(&p.done[s2]) != 0;
@@ -1002,7 +1019,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       S.pred_out[slot * p.out_stride + v] = spred[i] == 0xFFFFFFFFu ? ~0ull : (uint64_t)spred[i];
     }
   }
-  stamp();
+  stamp(11);
   if (bx == 0 && tid == 0) {
     uint64_t* const info = S.info + slot * 4;
     info[0] = settled;

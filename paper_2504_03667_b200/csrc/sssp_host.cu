@@ -1179,8 +1179,15 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
   if (g->bucket && g->sh[0].d_trace) {
     std::vector<uint64_t> tr(64 + 2048);
     CK(cudaMemcpy(tr.data(), g->sh[0].d_trace, tr.size() * 8, cudaMemcpyDeviceToHost));
-    fprintf(stderr, "bucket trace (us since kernel start):");
-    for (int i = 1; i < 64 && tr[i]; ++i) fprintf(stderr, " %.2f", (tr[i] - tr[0]) * 1e-3);
+    // entries: phase code << 56 | %globaltimer (bucket_kernel.cuh stamp())
+    static const char* names[] = {"start", "bar", "detld", "det", "enum", "pushld", "push",
+                                  "pullset", "pull", "pub0", "pub1", "wb", "row0", "owner"};
+    const uint64_t tmask = (1ull << 56) - 1;
+    fprintf(stderr, "bucket trace (us since kernel start; phase:end):");
+    for (int i = 1; i < 64 && tr[i]; ++i) {
+      const uint32_t c = (uint32_t)(tr[i] >> 56);
+      fprintf(stderr, " %s:%.2f", c < 14 ? names[c] : "?", ((tr[i] & tmask) - (tr[0] & tmask)) * 1e-3);
+    }
     fprintf(stderr, "\n");
     // per-CTA span of the last pull step (start, end relative to kernel start)
     double smin = 1e30, smax = 0, emin = 1e30, emax = 0, dsum = 0;

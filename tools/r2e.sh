@@ -1,0 +1,4 @@
+nvidia-smi --query-gpu=clocks.sm,clocks.mem,clocks.max.sm,power.draw,temperature.gpu --format=csv
+SSSP_BUCKET_TRACE=1 python tools/trace_bucket.py 2>&1 | head -12
+python tools/bucket_time.py --configs 1d,2,3 --reps 30
+nvidia-smi --query-gpu=clocks.sm,clocks.mem,clocks.max.sm,power.draw,temperature.gpu --format=csv
