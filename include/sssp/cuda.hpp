@@ -7,8 +7,11 @@
 //
 //   reference                                        drop-in (B200)
 //   dijkstra_serial(g, s)            serial.hpp:65   sssp::cuda::dijkstra(g, s)
-//   dijkstra_serial(g, s, c, &vo)    serial.hpp:26   sssp::cuda::dijkstra(g, s, &vo)
-//   dijkstra_partitioned(g, s, p)    partitioned:184 sssp::cuda::dijkstra_partitioned(g, s, devices)
+//   dijkstra_serial(g, s, c, &vo)    serial.hpp:26   sssp::cuda::dijkstra(g, s, c, &vo)
+//   dijkstra_partitioned(g, s, p, m) partitioned:184 sssp::cuda::dijkstra_partitioned(g, s, p, m)
+//                                                    (the reference's PartitionedRun: result,
+//                                                    CollectiveStats, PartitionedPhases), or
+//                                                    sssp::cuda::dijkstra_partitioned(g, s, devices)
 //   dijkstra_dataparallel(g, s)      dataparallel:302 sssp::cuda::dijkstra_dataparallel(g, s)
 //   parse_edge_list_text(in)         graph.hpp:126   sssp::cuda::parse_edge_list_text(text)
 //   (repeated solves on one graph)                   sssp::cuda::DeviceGraph
@@ -20,6 +23,7 @@
 // failure throws std::runtime_error -- there is no CPU fallback.
 #pragma once
 
+#include <algorithm>
 #include <cstdint>
 #include <stdexcept>
 #include <string>
@@ -28,7 +32,9 @@
 #include <vector>
 
 #include "sssp/graph.hpp"
+#include "sssp/partitioned.hpp"
 #include "sssp/result.hpp"
+#include "sssp/serial.hpp"
 #include "sssp/weight.hpp"
 #include "sssp_cuda.h"
 #include "sssp_graph_gen.h"
@@ -109,7 +115,9 @@ class DeviceGraph {
           "sssp_solve");
     r.phases = {r.stats.transfer_in_s, r.stats.rounds_s, r.stats.transfer_out_s};
     r.iterations = r.stats.iterations;
-    if (visit_order) visit_order->assign(vo.begin(), vo.begin() + r.stats.iterations);
+    // all n rounds: the reachable vertices in election order, then the
+    // unreachable ones in ascending id (serial.hpp:41-48)
+    if (visit_order) visit_order->assign(vo.begin(), vo.end());
     return r;
   }
 
@@ -195,11 +203,75 @@ inline ShortestPathResult dijkstra(const Graph& g, VertexId source,
   return dg.run(source, visit_order).result;
 }
 
+// Drop-in for dijkstra_serial(g, source, counters, visit_order) (serial.hpp:26-28):
+// the counters are the reference's own definition of the work, n*n each
+// (serial.hpp:13-19); the device's actual work is in CudaRun::stats.
+inline ShortestPathResult dijkstra(const Graph& g, VertexId source, OpCounters& counters,
+                                   std::vector<VertexId>* visit_order = nullptr) {
+  if (source >= g.n) throw std::invalid_argument("dijkstra_serial: source out of range");
+  sssp_options opt{};
+  opt.flags = SSSP_FLAGS_DEFAULT;
+  opt.record_visit_order = visit_order ? 1 : 0;
+  DeviceGraph dg(g, {0}, &opt);
+  CudaRun r = dg.run(source, visit_order);
+  counters.extract_min_scans = r.stats.extract_min_scans;
+  counters.relax_checks = r.stats.ref_relax_checks;
+  return std::move(r.result);
+}
+
 // The same solve with the phase timings of the data-parallel scope.
 inline CudaRun dijkstra_run(const Graph& g, VertexId source) {
   if (source >= g.n) throw std::invalid_argument("dijkstra: source out of range");
   DeviceGraph dg(g);
   return dg.run(source);
+}
+
+// Drop-in for dijkstra_partitioned(g, source, p, mode) (partitioned.hpp:184-225),
+// returning the reference's own PartitionedRun.  The p column shards are dealt
+// round-robin over the visible GPUs, at most SSSP_MAX_SHARDS of them (dist and
+// pred do not depend on p: partitioned == serial, test_partitioned.cpp:135-165);
+// the shards of one GPU run as one launch, the analogue of WorkerMode::sequential
+// (partitioned.hpp:142-154), so `mode` changes nothing.  stats are the
+// reference's CollectiveStats for THIS p (allreduce_count = padded_n, scatter /
+// gather bytes of workers 1..p-1); phases = {upload, kernel, download}.  A graph
+// that needs 64-bit distances runs on one shard (same result).
+inline PartitionedRun dijkstra_partitioned(const Graph& g, VertexId source, std::size_t p,
+                                           WorkerMode mode = WorkerMode::threaded) {
+  (void)mode;
+  if (p < 1) throw std::invalid_argument("dijkstra_partitioned: p >= 1");
+  if (source >= g.n) throw std::invalid_argument("dijkstra_partitioned: source out of range");
+  int ndev = 0;
+  check(sssp_device_count(&ndev), "sssp_device_count");
+  const std::size_t shards = std::min<std::size_t>({p, (std::size_t)SSSP_MAX_SHARDS,
+                                                    std::max<std::size_t>(g.n, 1)});
+  std::vector<int> devices(shards);
+  for (std::size_t i = 0; i < shards; ++i) devices[i] = static_cast<int>(i % std::max(ndev, 1));
+  sssp_graph* h = nullptr;
+  int rc = sssp_graph_create(g.adj.data(), g.n, g.directed ? 1 : 0, devices.data(),
+                             static_cast<int>(devices.size()), nullptr, &h);
+  if (rc == SSSP_ERR_UNSUPPORTED && shards > 1)  // 64-bit distances: one shard
+    rc = sssp_graph_create(g.adj.data(), g.n, g.directed ? 1 : 0, devices.data(), 1, nullptr, &h);
+  check(rc, "sssp_graph_create");
+  PartitionedRun run;
+  run.result.source = source;
+  run.result.dist.resize(g.n);
+  run.result.pred.resize(g.n);
+  sssp_solve_stats st{};
+  rc = sssp_solve(h, source, run.result.dist.data(),
+                  reinterpret_cast<std::uint64_t*>(run.result.pred.data()), nullptr, &st);
+  sssp_graph_destroy(h);
+  check(rc, "sssp_solve");
+  const PartitionPlan plan = make_partition_plan(g.n, p);
+  run.stats.allreduce_count = plan.padded_n;
+  for (std::size_t k = 1; k < p; ++k) {
+    const std::size_t loc = plan.ranges[k].second - plan.ranges[k].first;
+    run.stats.scatter_bytes += plan.padded_n * loc * sizeof(Weight);
+    run.stats.gather_bytes += loc * (sizeof(Weight) + sizeof(VertexId));
+  }
+  run.phases.scatter_s = st.transfer_in_s;
+  run.phases.rounds_s = st.rounds_s;
+  run.phases.gather_s = st.transfer_out_s;
+  return run;
 }
 
 // Column-partitioned over one shard per device (partitioned.hpp:184-225);

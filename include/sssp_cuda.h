@@ -31,7 +31,9 @@
 extern "C" {
 #endif
 
-#define SSSP_ABI_VERSION 2 /* 2: sssp_options.record_round_times, sssp_solve_dataparallel, sssp_round_times */
+#define SSSP_ABI_VERSION 3 /* 2: sssp_options.record_round_times, sssp_solve_dataparallel, sssp_round_times
+                              3: SSSP_ENGINE_WIDE (64-bit distances), the reference's OpCounters /
+                                 CollectiveStats and device exchange counts in sssp_solve_stats */
 #define SSSP_IPC_HANDLE_BYTES 64 /* sizeof(cudaIpcMemHandle_t) */
 #define SSSP_MAX_SHARDS 8
 
@@ -39,7 +41,8 @@ typedef enum {
   SSSP_OK = 0,
   SSSP_ERR_BAD_SOURCE = 1,   /* source >= n: std::invalid_argument at serial.hpp:30 */
   SSSP_ERR_BAD_ARG = 2,      /* p < 1 (partitioned.hpp:187), n == 0, bad shard ids ... */
-  SSSP_ERR_WEIGHT_RANGE = 3, /* a weight/distance this device encoding cannot hold */
+  SSSP_ERR_WEIGHT_RANGE = 3, /* (ABI < 3) a weight/distance the 32-bit encoding cannot hold;
+                                since ABI 3 such graphs run on SSSP_ENGINE_WIDE */
   SSSP_ERR_OOM = 4,          /* device or pinned-host allocation failed */
   SSSP_ERR_CUDA = 5,         /* CUDA runtime error (no device, launch failure ...) */
   SSSP_ERR_NO_PEER = 6,      /* peer access / IPC import failed between shards */
@@ -58,7 +61,9 @@ typedef enum {
   SSSP_ENGINE_GRID = 1,    /* single-warp CTAs across the GPU, exchange through L2 */
   SSSP_ENGINE_CLUSTER = 2, /* one thread-block cluster per solve, exchange through DSMEM */
   SSSP_ENGINE_BUCKET = 3,  /* distance-class steps, push/pull over B200 HBM */
-  SSSP_ENGINE_DATAPARALLEL = 4 /* reported by sssp_solve_dataparallel only */
+  SSSP_ENGINE_DATAPARALLEL = 4, /* reported by sssp_solve_dataparallel only */
+  SSSP_ENGINE_WIDE = 5     /* 64-bit distances (a weight of 2^32-1, or n*max_weight >= 2^32-1):
+                              n-round cluster kernel, one shard; AUTO/CLUSTER select it */
 } sssp_engine;
 
 typedef struct {
@@ -99,6 +104,26 @@ typedef struct {
   uint32_t engine;        /* sssp_engine that ran */
   uint32_t classes;       /* BUCKET: distance classes (steps) */
   uint64_t rows_read;     /* matrix rows streamed (scan: = iterations) */
+  /* ABI 3.  The reference's own instrumentation, as it defines it for this
+   * input (so a caller of the drop-in reads the numbers the reference would):
+   *   OpCounters (serial.hpp:16-19): both counters are n*n for every solve;
+   *   CollectiveStats (partitioned.hpp:28-32) of dijkstra_partitioned with
+   *   p = shards: allreduce_count = padded_n (:205), scatter_bytes = uint64
+   *   bytes of the column blocks of workers 1..p-1 (:196-198), gather_bytes =
+   *   dist + pred bytes of workers 1..p-1 (:219-221); 0 for p = 1.
+   * And what the device actually executed: */
+  uint64_t extract_min_scans; /* OpCounters::extract_min_scans = n*n */
+  uint64_t ref_relax_checks;  /* OpCounters::relax_checks = n*n */
+  uint64_t allreduce_count;   /* CollectiveStats::allreduce_count = padded_n */
+  uint64_t scatter_bytes;     /* CollectiveStats::scatter_bytes */
+  uint64_t gather_bytes;      /* CollectiveStats::gather_bytes */
+  uint64_t exchanges;         /* device global-argmin exchanges executed per solve (mean over
+                                 a batch): scan / wide engines one per election (rounds until
+                                 the first INF election), bucket one per distance class */
+  uint64_t barriers;          /* device-wide barriers per solve (bucket: grid barriers incl.
+                                 pull-combine barriers; scan / wide: = exchanges) */
+  uint64_t upload_bytes;      /* host->device bytes of the graph upload (all local shards) */
+  uint64_t download_bytes;    /* device->host bytes of one solve's dist + pred */
 } sssp_solve_stats;
 
 typedef struct sssp_graph sssp_graph;
@@ -153,7 +178,10 @@ int sssp_graph_info(const sssp_graph* g, sssp_solve_stats* st);
 
 /* Synchronous solve.  dist_out/pred_out: n entries (single process), or the
  * shard's col_count entries in shard mode.  visit_order_out (optional, n
- * entries, filled up to stats.iterations; needs record_visit_order). */
+ * entries; needs record_visit_order): the vertex elected in every round of
+ * dijkstra_serial -- the stats.iterations reachable ones in election order,
+ * then the unreachable ones in ascending id, as the reference's later rounds
+ * elect them (serial.hpp:41-48). */
 int sssp_solve(sssp_graph* g, uint64_t source, uint64_t* dist_out, uint64_t* pred_out,
                uint64_t* visit_order_out, sssp_solve_stats* st);
 

@@ -175,6 +175,7 @@ def generate_bernoulli(n: int, p: float, seed: int, directed: bool = False,
 
 
 ENGINES = {"auto": 0, "grid": 1, "cluster": 2, "bucket": 3}
+ENGINE_NAMES = {1: "grid", 2: "cluster", 3: "bucket", 4: "dataparallel", 5: "wide"}
 
 
 def _options(flags: Optional[int], ctas: int, max_batch: int, timeout_ms: int,
@@ -273,7 +274,9 @@ class DeviceGraph:
               "sssp_solve")
         r = ShortestPathResult(source, dist, pred, st.as_dict())
         if order is not None:
-            r.stats["visit_order"] = order[: st.iterations].copy()
+            # all n rounds of dijkstra_serial: the reachable vertices in election
+            # order, then the unreachable ones in ascending id (serial.hpp:41-48)
+            r.stats["visit_order"] = order
         return r
 
     def solve_batch(self, sources: Sequence[int]) -> list:
@@ -404,14 +407,39 @@ def dijkstra_dataparallel(g: Graph, source: int, device: int = 0) -> ShortestPat
         return dg.solve_dataparallel(source)
 
 
+def collective_stats(n: int, p: int) -> dict:
+    """CollectiveStats of dijkstra_partitioned(g, s, p) as the reference defines
+    them (partitioned.hpp:196-221): allreduce_count = padded_n, scatter_bytes =
+    uint64 column blocks of workers 1..p-1, gather_bytes = their dist + pred."""
+    padded = pad_vertex_count(n, p)
+    loc = padded // p
+    return {"allreduce_count": padded, "scatter_bytes": (p - 1) * padded * loc * 8,
+            "gather_bytes": (p - 1) * loc * 16}
+
+
 def dijkstra_partitioned(g: Graph, source: int, p: int,
                          devices: Optional[Sequence[int]] = None) -> ShortestPathResult:
-    """Column-partitioned solve over p shards (partitioned.hpp:184-225); the
-    shards go to ``devices`` (default: all on GPU 0)."""
+    """Column-partitioned solve over p shards (partitioned.hpp:184-225), the
+    PartitionedRun mirror: ``result.stats`` carries the reference's
+    CollectiveStats for this p and ``phases`` = {scatter_s, rounds_s, gather_s}
+    (upload, kernel, download).  The shards go to ``devices`` (default: all on
+    GPU 0); at most SSSP_MAX_SHARDS = 8 shards are used for any p -- dist and
+    pred do not depend on p (test_partitioned.cpp:135-165) -- and a graph that
+    needs 64-bit distances runs on one shard."""
     if p < 1:
         raise ValueError("dijkstra_partitioned: p >= 1")
     if not 0 <= source < g.n:
         raise ValueError("dijkstra_partitioned: source out of range")
-    devs = list(devices) if devices is not None else [0] * p
-    with DeviceGraph(g, devs) as dg:
-        return dg.solve(source)
+    devs = list(devices) if devices is not None else [0] * min(p, 8)
+    try:
+        dg = DeviceGraph(g, devs)
+    except SsspError as e:
+        if len(devs) == 1 or "64-bit" not in str(e):
+            raise
+        dg = DeviceGraph(g, devs[:1])
+    with dg:
+        r = dg.solve(source)
+    r.stats.update(collective_stats(g.n, p))
+    r.stats["phases"] = {"scatter_s": r.stats["transfer_in_s"], "rounds_s": r.stats["rounds_s"],
+                         "gather_s": r.stats["transfer_out_s"]}
+    return r

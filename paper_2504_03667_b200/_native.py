@@ -65,6 +65,16 @@ class Stats(ctypes.Structure):
         ("engine", ctypes.c_uint32),
         ("classes", ctypes.c_uint32),
         ("rows_read", ctypes.c_uint64),
+        # ABI 3: the reference's OpCounters / CollectiveStats, device exchange counts
+        ("extract_min_scans", ctypes.c_uint64),
+        ("ref_relax_checks", ctypes.c_uint64),
+        ("allreduce_count", ctypes.c_uint64),
+        ("scatter_bytes", ctypes.c_uint64),
+        ("gather_bytes", ctypes.c_uint64),
+        ("exchanges", ctypes.c_uint64),
+        ("barriers", ctypes.c_uint64),
+        ("upload_bytes", ctypes.c_uint64),
+        ("download_bytes", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:

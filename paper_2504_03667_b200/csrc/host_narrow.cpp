@@ -125,8 +125,10 @@ __attribute__((target("avx512f,avx512vl,avx512bw"))) void narrow_seg_avx512(
       _mm_storel_epi64(reinterpret_cast<__m128i*>(o + j), _mm512_cvtepi64_epi8(nv));
     } else if constexpr (sizeof(W) == 2) {
       _mm_storeu_si128(reinterpret_cast<__m128i*>(o + j), _mm512_cvtepi64_epi16(nv));
-    } else {
+    } else if constexpr (sizeof(W) == 4) {
       _mm256_storeu_si256(reinterpret_cast<__m256i*>(o + j), _mm512_cvtepi64_epi32(nv));
+    } else {  // uint64 (wide encoding): a copy with the folds
+      _mm512_storeu_si512(reinterpret_cast<void*>(o + j), nv);
     }
     vmx = _mm512_mask_max_epu64(vmx, (__mmask8)~inf, vmx, v);
     vmn = _mm512_min_epu64(vmn, v);  // INF is the maximum: never lowers mn
@@ -204,6 +206,8 @@ template NarrowStats narrow_rows<uint8_t>(const uint64_t*, uint64_t, uint64_t, u
                                           uint64_t, uint8_t*);
 template NarrowStats narrow_rows<uint16_t>(const uint64_t*, uint64_t, uint64_t, uint64_t, uint64_t,
                                            uint64_t, uint16_t*);
+template NarrowStats narrow_rows<uint64_t>(const uint64_t*, uint64_t, uint64_t, uint64_t, uint64_t,
+                                           uint64_t, uint64_t*);
 template NarrowStats narrow_rows<uint32_t>(const uint64_t*, uint64_t, uint64_t, uint64_t, uint64_t,
                                            uint64_t, uint32_t*);
 

@@ -23,6 +23,7 @@
 #include "bucket_kernel.cuh"
 #include "dataparallel_kernel.cuh"
 #include "validate_kernel.cuh"
+#include "wide_kernel.cuh"
 #include "dispatch.h"
 #include "host_narrow.h"
 
@@ -108,7 +109,9 @@ __device__ __forceinline__ void min_cell(W* a, uint64_t row_stride, uint64_t u, 
                                          uint32_t G, uint32_t L, uint32_t w) {
   const uint64_t pos = (vl % G) * L + vl / G;
   W* cell = a + u * row_stride + pos;
-  if constexpr (sizeof(W) == 4) {
+  if constexpr (sizeof(W) == 8) {
+    atomicMin(reinterpret_cast<unsigned long long*>(cell), (unsigned long long)w);
+  } else if constexpr (sizeof(W) == 4) {
     atomicMin(reinterpret_cast<unsigned int*>(cell), w);
   } else {
     unsigned int* word = reinterpret_cast<unsigned int*>(reinterpret_cast<uintptr_t>(cell) & ~(uintptr_t)3);
@@ -209,6 +212,8 @@ struct sssp_graph {
   uint32_t nrep = 1;
   bool cluster = true;  // scan engine: cluster (DSMEM exchange) or grid (L2 exchange)
   bool bucket = false;  // distance-class engine available and selected (min weight >= 1)
+  bool wide = false;    // 64-bit distances (wide_kernel.cuh): a weight of 2^32-1 or n*max_w >= 2^32-1
+  uint32_t wPC = 0;     // wide engine: positions per CTA
   // bucket engine layout (identical on every shard)
   uint32_t bT = 0, bG = 0;               // positions per CTA, CTAs per shard
   uint64_t bseq = 0;                     // bucket launch tags (watchdog reports)
@@ -223,6 +228,7 @@ struct sssp_graph {
   uint32_t pending = 0;  // solves of the last enqueued launch (0: nothing pending)
   uint32_t queued = 0;   // launches enqueued since the last finish
   uint64_t matrix_bytes = 0;
+  uint64_t upload_bytes = 0;  // host->device bytes of the graph upload (stats)
 };
 
 namespace {
@@ -425,16 +431,16 @@ int alloc_matrix(Shard& s, uint64_t n, uint32_t wbytes) {
 int upload_shard(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, uint64_t hint_max_w,
                  uint32_t* wbytes_out, uint64_t* max_w, uint64_t* min_w) {
   CK(cudaSetDevice(s.device));
-  uint32_t wb = hint_max_w == 0 ? 1 : hint_max_w <= 0xFEull ? 1 : hint_max_w <= 0xFFFEull ? 2 : 4;
+  uint32_t wb = hint_max_w == 0 ? 1 : hint_max_w <= 0xFEull ? 1 : hint_max_w <= 0xFFFEull ? 2
+               : hint_max_w <= 0xFFFFFFFEull ? 4 : 8;
   while (true) {
-    if (hint_max_w > 0xFFFFFFFEull)
-      return fail(SSSP_ERR_WEIGHT_RANGE, "finite weight 0xFFFFFFFF needs the wide encoding");
     int rc = alloc_matrix(s, n, wb);
     if (rc) return rc;
     ScanResult res;
     rc = wb == 1 ? upload_block<uint8_t>(s, src, ld, n, res)
          : wb == 2 ? upload_block<uint16_t>(s, src, ld, n, res)
-                   : upload_block<uint32_t>(s, src, ld, n, res);
+         : wb == 4 ? upload_block<uint32_t>(s, src, ld, n, res)
+                   : upload_block<uint64_t>(s, src, ld, n, res);  // a weight of 2^32-1: wide
     if (rc) return rc;
     if (!res.overflow) {
       *wbytes_out = wb;
@@ -442,8 +448,7 @@ int upload_shard(Shard& s, const uint64_t* src, uint64_t ld, uint64_t n, uint64_
       *min_w = res.min_w;
       return SSSP_OK;
     }
-    if (wb == 4)
-      return fail(SSSP_ERR_WEIGHT_RANGE, "finite weight 0xFFFFFFFF needs the wide encoding");
+    if (wb == 8) return fail(SSSP_ERR_WEIGHT_RANGE, "weight outside uint64");  // unreachable
     wb *= 2;
   }
 }
@@ -515,10 +520,21 @@ uint32_t shards_on_device(const sssp_graph* g, int device) {
 // Encoding-dependent constants shared by every shard; requires max_w.
 int finalize_encoding(sssp_graph* g) {
   const uint64_t n = g->n;
-  // u32 distances: every candidate du + w <= n*max_w must stay below INF.
-  if (g->max_w != 0 && n > 0xFFFFFFFEull / g->max_w)
-    return fail(SSSP_ERR_WEIGHT_RANGE, "n * max_weight exceeds the 32-bit distance encoding");
   const Shard& s0 = g->sh[0];
+  // u32 distances need every candidate du + w <= n*max_w below INF; otherwise
+  // (or with a weight of exactly 2^32-1, which only uint64 storage keeps apart
+  // from INF) the solve runs on 64-bit distances (wide_kernel.cuh).
+  g->wide = g->wbytes == 8 || (g->max_w != 0 && n > 0xFFFFFFFEull / g->max_w);
+  if (g->wide) {
+    if (g->P > 1 || g->multiproc)
+      return fail(SSSP_ERR_UNSUPPORTED, "64-bit distances run on one shard (the result does not depend on p)");
+    if (!g->cluster || g->opt.engine == SSSP_ENGINE_BUCKET)
+      return fail(SSSP_ERR_UNSUPPORTED, "64-bit distances run on the wide n-round engine (engine AUTO or CLUSTER)");
+    g->wPC = (uint32_t)(s0.row_stride / s0.C);
+    if (wide_smem_bytes(g->wPC) > 200 * 1024)
+      return fail(SSSP_ERR_UNSUPPORTED, "graph too large for the 64-bit distance engine");
+    return SSSP_OK;
+  }
   g->sbits = bitlen(s0.L) - 1;
   const uint64_t dmax = n * g->max_w;
   g->packed = (dmax + 1) < (1ull << (32 - g->sbits)) ? 1u : 0u;
@@ -579,7 +595,22 @@ cudaError_t raise_smem(const void* fn, size_t bytes) {
   return e;
 }
 
+void* wide_fn(uint32_t wbytes) {
+  return wbytes == 1 ? (void*)wide_kernel<uint8_t>
+         : wbytes == 2 ? (void*)wide_kernel<uint16_t>
+         : wbytes == 4 ? (void*)wide_kernel<uint32_t> : (void*)wide_kernel<uint64_t>;
+}
+
 int compute_max_batch(sssp_graph* g) {
+  if (g->wide) {  // independent clusters: no co-residency needed
+    const Shard& s = g->sh[0];
+    CK(cudaSetDevice(s.device));
+    void* fn = wide_fn(g->wbytes);
+    if (s.C > 8) CK(cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1));
+    CK(raise_smem(fn, wide_smem_bytes(g->wPC)));
+    g->max_batch = g->opt.max_batch ? g->opt.max_batch : 64;
+    return SSSP_OK;
+  }
   uint32_t cap = ~0u;
   for (auto& s : g->sh) {
     CK(cudaSetDevice(s.device));
@@ -647,7 +678,7 @@ int plan_bucket(sssp_graph* g) {
   g->bucket = false;
   const int want = g->opt.engine;
   if (want == SSSP_ENGINE_GRID || want == SSSP_ENGINE_CLUSTER) return SSSP_OK;
-  const bool exact = g->min_w >= 1;
+  const bool exact = g->min_w >= 1 && !g->wide;
   const Shard& s0 = g->sh[0];
   const bool shape = g->cluster && g->n > 1 && !g->opt.record_visit_order &&
                      !g->opt.record_round_times &&
@@ -963,6 +994,46 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
   if (k == 0 || k > g->max_batch) return fail(SSSP_ERR_BAD_ARG, "bad batch size");
   for (uint32_t i = 0; i < k; ++i)
     if (sources[i] >= g->n) return fail(SSSP_ERR_BAD_SOURCE, "dijkstra: source out of range");
+  if (g->wide) {  // k independent clusters, 64-bit distances (wide_kernel.cuh)
+    Shard& s = g->sh[0];
+    CK(cudaSetDevice(s.device));
+    for (uint32_t i = 0; i < k; ++i) s.h_sources[i] = (uint32_t)sources[i];
+    CK(cudaMemcpyAsync(s.d_sources, s.h_sources, k * sizeof(uint32_t), cudaMemcpyHostToDevice, s.stream));
+    CK(cudaMemsetAsync(s.d_info, 0, (uint64_t)k * 4 * sizeof(uint64_t), s.stream));
+    WideParams wp{};
+    wp.adj = s.d_adj;
+    wp.row_stride = s.row_stride;
+    wp.n = (uint32_t)g->n;
+    wp.Q = s.G;
+    wp.qbits = bitlen(s.G) - 1;
+    wp.lbits = bitlen(s.L) - 1;
+    wp.C = s.C;
+    wp.PC = g->wPC;
+    wp.sources = s.d_sources;
+    wp.dist_out = s.d_dist;
+    wp.pred_out = s.d_pred;
+    wp.visit_order = s.d_visit;
+    wp.info = s.d_info;
+    if (!g->pending) CK(cudaEventRecord(s.ev0, s.stream));
+    cudaLaunchConfig_t cfg{};
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = s.C;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.gridDim = dim3(k * s.C);
+    cfg.blockDim = dim3(kWideThreads);
+    cfg.dynamicSmemBytes = wide_smem_bytes(g->wPC);
+    cfg.stream = s.stream;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    void* args[] = {(void*)&wp};
+    CK(cudaLaunchKernelExC(&cfg, wide_fn(g->wbytes), args));
+    CK(cudaEventRecord(s.ev1, s.stream));
+    g->pending = k;
+    g->queued += 1;
+    return SSSP_OK;
+  }
   if (g->bucket) {
     void* fn = bucket_fn(g->wbytes);
     const size_t smem = bucket_smem(g);
@@ -1128,11 +1199,28 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
 }
 
 // Waits for the pending launch, checks the watchdog, fills stats.
+// The reference's OpCounters (serial.hpp:16-19) and the CollectiveStats of
+// dijkstra_partitioned with p = shards (partitioned.hpp:196-221), as the
+// reference defines them for this input, plus the upload / output bytes.
+void fill_reference_stats(const sssp_graph* g, sssp_solve_stats* st) {
+  const uint64_t n = g->n, p = g->P;
+  const uint64_t padded = pad_vertex_count(n, p), loc_n = padded / p;
+  st->extract_min_scans = n * n;
+  st->ref_relax_checks = n * n;
+  st->allreduce_count = padded;
+  st->scatter_bytes = (p - 1) * padded * loc_n * sizeof(uint64_t);
+  st->gather_bytes = (p - 1) * loc_n * (sizeof(uint64_t) + sizeof(uint64_t));
+  st->upload_bytes = g->upload_bytes;
+  uint64_t cols = 0;
+  for (const auto& s : g->sh) cols += s.cols;
+  st->download_bytes = cols * 16;
+}
+
 int finish(sssp_graph* g, sssp_solve_stats* st) {
   const uint32_t k = g->pending;
   if (k == 0) return fail(SSSP_ERR_BAD_ARG, "nothing enqueued");
   double rounds = 0;
-  uint64_t iters = 0, last = 0, mis = 0, classes = 0, rows = 0;
+  uint64_t iters = 0, last = 0, mis = 0, classes = 0, rows = 0, nbars = 0;
   bool timeout = false;
   for (auto& s : g->sh) {
     CK(cudaSetDevice(s.device));
@@ -1144,8 +1232,10 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
                          cudaMemcpyDeviceToHost, s.stream));
       CK(cudaStreamSynchronize(s.stream));
       // launch i of the last enqueue carried tag bseq - k + 1 + i
-      for (uint32_t i = 0; i < std::min<uint32_t>(k, 64); ++i)
+      for (uint32_t i = 0; i < std::min<uint32_t>(k, 64); ++i) {
         timeout |= i2[2 * i + 1] == g->bseq - k + 1 + i;
+        if (s.k == g->sh[0].k) nbars += i2[2 * i];
+      }
     }
     CK(cudaStreamSynchronize(s.stream));
     float ms = 0;
@@ -1207,9 +1297,13 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     st->iterations = iters;
     st->relax_checks = (g->bucket ? rows : iters) * g->sh[0].row_stride * g->P;
     st->mispredicts = mis;
-    st->engine = g->bucket ? SSSP_ENGINE_BUCKET : g->cluster ? SSSP_ENGINE_CLUSTER : SSSP_ENGINE_GRID;
+    st->engine = g->wide ? SSSP_ENGINE_WIDE : g->bucket ? SSSP_ENGINE_BUCKET
+                 : g->cluster ? SSSP_ENGINE_CLUSTER : SSSP_ENGINE_GRID;
     st->classes = (uint32_t)classes;
     st->rows_read = g->bucket ? rows : iters;
+    fill_reference_stats(g, st);
+    st->exchanges = (g->bucket ? classes : iters) / k;
+    st->barriers = g->bucket ? nbars / std::min<uint32_t>(k, 64) : st->exchanges;
     st->matrix_bytes = g->matrix_bytes;
     st->weight_bytes = g->wbytes;
     st->ctas = g->cluster ? g->sh[0].C : g->sh[0].G;
@@ -1376,8 +1470,6 @@ int sssp_graph_create_from_edges(uint64_t n, const uint64_t* edges, uint64_t m, 
     if (bad[t]) return fail(SSSP_ERR_BAD_ARG, "edge endpoint out of range, self-loop or weight > 2^32-1");
   const uint64_t max_w = *std::max_element(tmx.begin(), tmx.end());
   const uint64_t min_w = *std::min_element(tmn.begin(), tmn.end());
-  if (max_w > 0xFFFFFFFEull)
-    return fail(SSSP_ERR_WEIGHT_RANGE, "finite weight 0xFFFFFFFF needs the wide encoding");
   sssp_graph* g = new sssp_graph();
   g->n = n;
   g->directed = directed;
@@ -1385,18 +1477,20 @@ int sssp_graph_create_from_edges(uint64_t n, const uint64_t* edges, uint64_t m, 
   g->opt = default_options(opt);
   g->max_w = max_w;
   g->min_w = min_w;
-  g->wbytes = max_w <= 0xFE ? 1 : max_w <= 0xFFFE ? 2 : 4;
+  g->wbytes = max_w <= 0xFE ? 1 : max_w <= 0xFFFE ? 2 : max_w <= 0xFFFFFFFEull ? 4 : 8;
   int rc = create_shard_objects(g, g->P, devices, g->P, 0);
   if (rc == SSSP_OK) rc = enable_peers(devices, ndev);
   for (uint32_t i = 0; rc == SSSP_OK && i < g->P; ++i)
     rc = g->wbytes == 1 ? build_from_edges<uint8_t>(g, g->sh[i], edges, m)
          : g->wbytes == 2 ? build_from_edges<uint16_t>(g, g->sh[i], edges, m)
-                          : build_from_edges<uint32_t>(g, g->sh[i], edges, m);
+         : g->wbytes == 4 ? build_from_edges<uint32_t>(g, g->sh[i], edges, m)
+                          : build_from_edges<uint64_t>(g, g->sh[i], edges, m);
   if (rc == SSSP_OK) rc = setup_common(g);
   if (rc) {
     destroy_graph(g);
     return rc;
   }
+  g->upload_bytes = m * 24 * g->P;  // the (u, v, w) triples, to every shard
   g->transfer_in_s = now_s() - t0;
   *out = g;
   return SSSP_OK;
@@ -1456,6 +1550,7 @@ int sssp_graph_create(const uint64_t* adj, uint64_t n, int directed, const int* 
     destroy_graph(g);
     return rc;
   }
+  for (const auto& sh : g->sh) g->upload_bytes += g->n * sh.cols * g->wbytes;  // narrowed H2D
   g->transfer_in_s = now_s() - t0;
   *out = g;
   return SSSP_OK;
@@ -1498,6 +1593,7 @@ int sssp_shard_create(const uint64_t* block, uint64_t ld, uint64_t n, uint32_t w
     destroy_graph(g);
     return rc;
   }
+  for (const auto& sh : g->sh) g->upload_bytes += g->n * sh.cols * g->wbytes;  // narrowed H2D
   g->transfer_in_s = now_s() - t0;
   *out = g;
   return SSSP_OK;
@@ -1581,7 +1677,9 @@ int sssp_graph_info(const sssp_graph* g, sssp_solve_stats* st) {
   st->ctas = g->cluster ? g->sh[0].C : g->sh[0].G;
   st->shards = g->P;
   st->packed_key = g->packed;
-  st->engine = g->bucket ? SSSP_ENGINE_BUCKET : g->cluster ? SSSP_ENGINE_CLUSTER : SSSP_ENGINE_GRID;
+  st->engine = g->wide ? SSSP_ENGINE_WIDE : g->bucket ? SSSP_ENGINE_BUCKET
+               : g->cluster ? SSSP_ENGINE_CLUSTER : SSSP_ENGINE_GRID;
+  fill_reference_stats(g, st);
   st->iterations = g->max_batch;  // reused: concurrent solve capacity
   st->relax_checks = g->min_w;    // reused: min finite off-diagonal weight
   st->mispredicts = g->max_w;     // reused: max finite weight
@@ -1605,6 +1703,16 @@ int sssp_solve(sssp_graph* g, uint64_t source, uint64_t* dist_out, uint64_t* pre
     CK(cudaSetDevice(g->sh[0].device));
     CK(cudaMemcpy(tmp.data(), g->sh[0].d_visit, local.iterations * 4, cudaMemcpyDeviceToHost));
     for (uint64_t i = 0; i < local.iterations; ++i) visit_order_out[i] = tmp[i];
+    // the reference keeps electing after the last reachable vertex: the
+    // unreachable ones, lowest id first (serial.hpp:41-48, INF ties), relaxing
+    // nothing -- the order is completed here (n entries, as visit_order gets)
+    if (!g->multiproc) {
+      std::vector<char> seen(g->n, 0);
+      for (uint64_t i = 0; i < local.iterations; ++i) seen[tmp[i]] = 1;
+      uint64_t k = local.iterations;
+      for (uint64_t v = 0; v < g->n; ++v)
+        if (!seen[v]) visit_order_out[k++] = v;
+    }
   }
   local.transfer_out_s = now_s() - t0;
   if (st) *st = local;
@@ -1660,6 +1768,7 @@ int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round) {
   if (g->multiproc && !g->connected) return fail(SSSP_ERR_BAD_ARG, "shard not connected");
   if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
   const uint32_t np = g->sh[0].NP;
+  if (g->wide) return fail(SSSP_ERR_UNSUPPORTED, "not available with 64-bit distances (wide engine)");
   auto probe_fn = [&](int device) -> ProbeFn {  // a launch with several shards: the MS instance
     const bool ms = shards_on_device(g, device) > 1;
     return g->cluster ? get_cluster_probe((int)g->sh[0].NW, g->sh[0].hier, ms)
@@ -1737,6 +1846,7 @@ int sssp_validate(sssp_graph* g, uint64_t source, const uint64_t* dist, const ui
   if (!g || !dist || !pred || !violations) return fail(SSSP_ERR_BAD_ARG, "null argument");
   if (source >= g->n) return fail(SSSP_ERR_BAD_SOURCE, "validate: source out of range");
   if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
+  if (g->wide) return fail(SSSP_ERR_UNSUPPORTED, "not available with 64-bit distances (wide engine)");
   uint64_t total = 0;
   const uint64_t n = g->n;
   for (auto& s : g->sh) {
@@ -1795,6 +1905,7 @@ int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, 
   if (!g) return fail(SSSP_ERR_BAD_ARG, "null handle");
   if (source >= g->n) return fail(SSSP_ERR_BAD_SOURCE, "dijkstra_dataparallel: source out of range");
   if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
+  if (g->wide) return fail(SSSP_ERR_UNSUPPORTED, "not available with 64-bit distances (wide engine)");
   if (g->P != 1 || g->multiproc) return fail(SSSP_ERR_UNSUPPORTED, "dataparallel engine: one shard");
   Shard& s = g->sh[0];
   if (!g->cluster || (s.G & (s.G - 1)) || (s.L & (s.L - 1)))
@@ -1926,6 +2037,7 @@ int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, 
     st->ctas = G;
     st->shards = 1;
     st->engine = SSSP_ENGINE_DATAPARALLEL;
+    fill_reference_stats(g, st);
     st->classes = (uint32_t)(flag ? info[2] : 0);  // pass-number sweeps (0: none needed)
   }
   return SSSP_OK;
@@ -1934,6 +2046,7 @@ int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, 
 int sssp_round_times(sssp_graph* g, uint64_t* ns_out, uint64_t cap, uint64_t* count) {
   if (!g || !count) return fail(SSSP_ERR_BAD_ARG, "null argument");
   if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
+  if (g->wide) return fail(SSSP_ERR_UNSUPPORTED, "not available with 64-bit distances (wide engine)");
   Shard* s0 = nullptr;
   for (auto& s : g->sh)
     if (s.d_round_ns) s0 = &s;

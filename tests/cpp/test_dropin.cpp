@@ -41,6 +41,71 @@ int main() {
     threw = true;
   }
   EXPECT(threw);
+  // test_serial.cpp:11-19: OpCounters land on n*n; the counters overload
+  {
+    OpCounters c, cr;
+    std::vector<VertexId> vo, vr;
+    EXPECT(cuda::dijkstra(four, 0, c, &vo) == dijkstra_serial(four, 0, cr, &vr));
+    EXPECT(c.extract_min_scans == 16 && c.relax_checks == 16);
+    EXPECT(c.extract_min_scans == cr.extract_min_scans && c.relax_checks == cr.relax_checks);
+    EXPECT(vo == vr);
+    // test_serial.cpp:21-26: directed, source 3 reaches nothing -- the visit
+    // order still lists all n rounds (unreachable ones lowest id first)
+    const Graph dg4 = graph_from_edges(el, true);
+    EXPECT(cuda::dijkstra(dg4, 3, c, &vo) == dijkstra_serial(dg4, 3, cr, &vr));
+    EXPECT(vo == vr && vo.size() == 4);
+  }
+  // partitioned.hpp:184-225: the reference's PartitionedRun, any p (also p > 8)
+  {
+    const Graph g = graph_from_edges(generate_sparse(61, 7), false);
+    for (std::size_t p : {1, 2, 3, 8, 12}) {
+      const PartitionedRun want = dijkstra_partitioned(g, 5, p);
+      const PartitionedRun got = cuda::dijkstra_partitioned(g, 5, p, WorkerMode::sequential);
+      EXPECT(got.result == want.result);
+      EXPECT(got.stats.allreduce_count == want.stats.allreduce_count);
+      EXPECT(got.stats.scatter_bytes == want.stats.scatter_bytes);
+      EXPECT(got.stats.gather_bytes == want.stats.gather_bytes);
+      EXPECT(got.phases.rounds_s > 0);
+    }
+    bool t3 = false;
+    try {
+      cuda::dijkstra_partitioned(g, 0, std::size_t{0});
+    } catch (const std::invalid_argument&) {
+      t3 = true;
+    }
+    EXPECT(t3);
+  }
+  // the reference's full value domain (weight.hpp:18, graph.hpp:79): a weight of
+  // kMaxWeight = 2^32-1, and n * max_weight >= 2^32 -- 64-bit distances
+  {
+    EdgeList w;
+    w.n = 6;
+    w.edges = {{0, 1, kMaxWeight}, {1, 2, kMaxWeight}, {0, 2, 7}, {2, 3, kMaxWeight - 1},
+               {3, 4, 1}, {1, 4, 0}};
+    for (bool directed : {false, true}) {
+      const Graph wg = graph_from_edges(w, directed);
+      for (VertexId s = 0; s < 6; ++s) {
+        EXPECT(cuda::dijkstra(wg, s) == dijkstra_serial(wg, s));
+        EXPECT(cuda::dijkstra_partitioned(wg, s, 2).result == dijkstra_serial(wg, s));
+      }
+      cuda::DeviceGraph edg(w, directed);
+      EXPECT(edg.solve(0) == dijkstra_serial(wg, 0));
+    }
+    std::mt19937_64 wr(4242);
+    for (int i = 0; i < 6; ++i) {
+      const std::size_t n = 20 + wr() % 300;
+      EdgeList big;
+      big.n = n;
+      for (std::size_t u = 0; u + 1 < n; ++u) big.edges.push_back({u, u + 1, 3000000000ull + wr() % 1000});
+      for (int k = 0; k < 3 * (int)n; ++k) {
+        const std::size_t a = wr() % n, b = wr() % n;
+        if (a != b) big.edges.push_back({a, b, 4000000000ull + wr() % 294967295ull});
+      }
+      const Graph bg = graph_from_edges(big, i % 2 == 1);
+      const VertexId s = wr() % n;
+      EXPECT(cuda::dijkstra(bg, s) == dijkstra_serial(bg, s));
+    }
+  }
   // acceptance.cpp:42-80 style sweep, full-result equality
   std::mt19937_64 rng(20240601);
   int graphs = 0;

@@ -39,11 +39,11 @@ def test_library_exports_every_declared_symbol():
 
 def test_abi_constants_and_strings():
     from paper_2504_03667_b200 import _native
-    assert _native.lib.sssp_abi_version() == 2
+    assert _native.lib.sssp_abi_version() == 3
     for code in range(9):
         assert _native.lib.sssp_status_string(code)
     assert ctypes.sizeof(_native.Options) == 56
-    assert ctypes.sizeof(_native.Stats) == 88
+    assert ctypes.sizeof(_native.Stats) == 160
 
 
 def test_struct_layout_matches_header():

@@ -230,11 +230,131 @@ def test_unpacked_key_path(gpu, oracle_c):
         assert_same(dg.solve(0), d, p, "unpacked")
 
 
-def test_weight_range_errors_are_loud(gpu):
-    g = gpu.Graph.no_edges(3, True)
-    g.adj[1] = 0xFFFFFFFF  # kMaxWeight is a legal finite weight (weight.hpp:18)
-    with pytest.raises(gpu.SsspError):
-        gpu.DeviceGraph(g)
+KMAX = 0xFFFFFFFF  # kMaxWeight (weight.hpp:18): a legal finite weight
+
+
+def wide_graph(rng, n, directed, wlo, whi, density, zero_frac=0.0):
+    adj = np.full((n, n), INF, dtype=np.uint64)
+    mask = rng.random((n, n)) < density
+    w = rng.integers(wlo, whi, size=(n, n), dtype=np.uint64, endpoint=True)
+    if zero_frac:
+        w = np.where(rng.random((n, n)) < zero_frac, np.uint64(0), w)
+    adj[mask] = w[mask]
+    for u in range(n - 1):  # a spanning path keeps most vertices reachable
+        adj[u, u + 1] = min(int(adj[u, u + 1]), int(rng.integers(wlo, whi, endpoint=True)))
+    if not directed:
+        adj = np.minimum(adj, adj.T)
+    np.fill_diagonal(adj, 0)
+    return adj.reshape(-1)
+
+
+def test_kmaxweight_fixture_is_exact(gpu, oracle_c):
+    """A weight of exactly kMaxWeight = 2^32-1 (weight.hpp:18, graph.hpp:79) is a
+    legal finite weight: the solve runs on 64-bit distances (engine WIDE) and
+    equals dijkstra_serial -- no SSSP_ERR_WEIGHT_RANGE."""
+    for directed in (False, True):
+        g = gpu.graph_from_edges(6, [(0, 1, KMAX), (1, 2, KMAX), (0, 2, 7), (2, 3, KMAX - 1),
+                                     (3, 4, 1), (1, 4, 0)], directed)
+        for s in range(6):
+            d, p = serial(oracle_c, g, s)
+            with gpu.DeviceGraph(g) as dg:
+                assert dg.info()["engine"] == 5 and dg.info()["weight_bytes"] == 8
+                r = dg.solve(s)
+            assert_same(r, d, p, f"kmax directed={directed} s={s}")
+
+
+@pytest.mark.parametrize("directed", [False, True])
+@pytest.mark.parametrize("wlo,whi", [(1 << 31, KMAX - 1), (3_000_000_000, KMAX), (1, KMAX)])
+def test_distances_beyond_32_bits(gpu, oracle_c, directed, wlo, whi):
+    """n * max_weight >= 2^32: distances past the 32-bit encoding (u32 weights,
+    u64 distances; or u64 weights when kMaxWeight occurs) -- bit-exact."""
+    rng = np.random.default_rng(wlo % 1000 + directed)
+    for n, dens in [(257, 0.02), (1000, 0.005), (1500, 0.3)]:
+        g = gpu.Graph(n, directed, wide_graph(rng, n, directed, wlo, whi, dens))
+        for s in (0, n // 2):
+            d, p = serial(oracle_c, g, s)
+            with gpu.DeviceGraph(g) as dg:
+                assert dg.info()["engine"] == 5
+                r = dg.solve(s)
+            assert_same(r, d, p, f"n={n} s={s}")
+            if wlo >= 1 << 31:  # every path of >= 3 edges passes 2^32
+                assert int(d[d != INF].max()) > 0xFFFFFFFF
+
+
+def test_wide_zero_weights_ties_unreachable(gpu, oracle_c):
+    """Tie-heavy wide graphs with zero weights and unreachable vertices (the
+    strict '<' and lowest-id rules of serial.hpp:42-56 at 64 bits)."""
+    rng = np.random.default_rng(77)
+    for trial in range(6):
+        n = int(rng.integers(50, 700))
+        adj = wide_graph(rng, n, bool(trial % 2), KMAX - 2, KMAX, 0.05, zero_frac=0.3)
+        adj = adj.reshape(n, n)
+        adj[:, n - 3:] = INF  # the last 3 vertices unreachable
+        np.fill_diagonal(adj, 0)
+        g = gpu.Graph(n, bool(trial % 2), adj.reshape(-1))
+        s = int(rng.integers(0, n - 3))
+        d, p, vo = oracle_c.serial(g.adj, n, s, visit_order=True)
+        with gpu.DeviceGraph(g, visit_order=True) as dg:
+            r = dg.solve(s, visit_order=True)
+            batch = dg.solve_batch([s, 0, n - 1])
+        assert_same(r, d, p, f"trial {trial}")
+        assert np.array_equal(r.stats["visit_order"], vo)
+        for src, rb in zip([s, 0, n - 1], batch):
+            d2, p2 = serial(oracle_c, g, src)
+            assert_same(rb, d2, p2, f"batch s={src}")
+
+
+def test_wide_edge_list_and_partitioned(gpu, oracle_c):
+    """The device edge-list build and dijkstra_partitioned take kMaxWeight too
+    (a wide graph runs on one shard: the result does not depend on p)."""
+    edges = [(0, 1, KMAX), (1, 2, 5), (2, 3, KMAX), (0, 3, KMAX), (3, 4, KMAX), (4, 5, 0)]
+    for directed in (False, True):
+        g = gpu.graph_from_edges(6, edges, directed)
+        d, p = serial(oracle_c, g, 0)
+        with gpu.DeviceGraph.from_edges(6, edges, directed) as dg:
+            assert_same(dg.solve(0), d, p, "edges")
+        r = gpu.dijkstra_partitioned(g, 0, 3)
+        assert_same(r, d, p, "partitioned")
+        assert r.stats["allreduce_count"] == 6
+
+
+def test_reference_counters_and_collective_stats(gpu, oracle_c):
+    """OpCounters (serial.hpp:16-19, pinned by test_serial.cpp:40-51: n*n each)
+    and CollectiveStats (partitioned.hpp:196-221: padded_n, scatter / gather
+    bytes, zero for one worker -- test_partitioned.cpp:132, 162, 230-237)."""
+    g = gpu.generate_sparse(1001, 3)
+    d, p, ct = oracle_c.serial(g.adj, g.n, 0, counters=True)
+    with gpu.DeviceGraph(g) as dg:
+        r = dg.solve(0)
+    st = r.stats
+    assert st["extract_min_scans"] == ct[0] == 1001 * 1001
+    assert st["ref_relax_checks"] == ct[1] == 1001 * 1001
+    assert st["allreduce_count"] == 1001 and st["scatter_bytes"] == 0 and st["gather_bytes"] == 0
+    assert st["download_bytes"] == 1001 * 16 and st["upload_bytes"] == 1001 * 1001 * st["weight_bytes"]
+    assert st["exchanges"] >= 1 and st["barriers"] >= st["exchanges"] - 1
+    for P in (2, 3, 8, 12):
+        rp = gpu.dijkstra_partitioned(g, 0, P)
+        assert_same(rp, d, p, f"P={P}")
+        padded = gpu.pad_vertex_count(1001, P)
+        loc = padded // P
+        assert rp.stats["allreduce_count"] == padded
+        assert rp.stats["scatter_bytes"] == (P - 1) * padded * loc * 8
+        assert rp.stats["gather_bytes"] == (P - 1) * loc * 16
+        assert rp.stats["phases"]["rounds_s"] > 0
+    # the device's own exchange counts: n-round engines one per election
+    with gpu.DeviceGraph(g, engine="cluster") as dg:
+        rc = dg.solve(0)
+    assert rc.stats["exchanges"] == rc.stats["iterations"] == int(np.count_nonzero(d != INF))
+    # bucket: one exchange per distance class, barriers counted by the kernel
+    gd = gpu.generate_dense(2048, 5)
+    with gpu.DeviceGraph(gd, engine="bucket") as dg:
+        rb = dg.solve(0)
+    assert rb.stats["exchanges"] == rb.stats["classes"] and rb.stats["barriers"] >= 2
+    # the C ABI struct carries the shard count's CollectiveStats too
+    with gpu.DeviceGraph(g, [0, 0, 0]) as dg:
+        r3 = dg.solve(0)
+    assert r3.stats["allreduce_count"] == gpu.pad_vertex_count(1001, 3)
+    assert r3.stats["scatter_bytes"] == 2 * 1002 * 334 * 8
 
 
 @pytest.mark.parametrize("engine", ENGINES)
@@ -286,7 +406,8 @@ def test_visit_order_matches_serial(gpu, oracle_c):
     with gpu.DeviceGraph(g, visit_order=True) as dg:
         r = dg.solve(0, visit_order=True)
     assert r.stats["iterations"] == finite
-    assert np.array_equal(r.stats["visit_order"], vo[:finite])
+    # all n rounds, unreachable vertices included (serial.hpp:41-48)
+    assert np.array_equal(r.stats["visit_order"], vo)
 
 
 def test_config2_n16384_bernoulli(gpu, oracle_c):
