@@ -54,8 +54,11 @@ typedef enum {
  * GRID / CLUSTER run the reference's n rounds in one persistent kernel and
  * differ in how a round's election is exchanged.  BUCKET settles a whole
  * distance class per step and is exact only when every finite off-diagonal
- * weight is >= 1; AUTO picks BUCKET when that holds (single shard), else
- * CLUSTER. */
+ * weight is >= 1.  AUTO: WIDE when distances need 64 bits; else BUCKET when
+ * it is exact (any number of shards), else CLUSTER.  In one process an AUTO
+ * bucket solve that needs more than n/12 distance classes stops and reruns on
+ * CLUSTER inside the same call (classes cost ~12 scan rounds each), and the
+ * handle keeps CLUSTER for its later solves. */
 typedef enum {
   SSSP_ENGINE_AUTO = 0,
   SSSP_ENGINE_GRID = 1,    /* single-warp CTAs across the GPU, exchange through L2 */

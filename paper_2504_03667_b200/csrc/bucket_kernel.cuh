@@ -77,6 +77,7 @@ struct BucketParams {
   uint32_t* peer_bitmap[kMaxShards];  // every shard's [2][nshards*row_stride/32] (self incl.)
   uint32_t* peer_ctrl[kMaxShards];    // every shard's [2][4][nshards*G]: tile lmin, cand, open, finite
   uint32_t wmin;        // smallest finite off-diagonal weight of the whole graph (>= 1)
+  uint32_t max_classes; // AUTO: stop after this many classes (0 = no limit; single solves)
   uint32_t push_ldg;    // 1: push rows through registers (LDG) instead of bulk copies (A/B)
   uint32_t push_depth16;  // LDG push: one 16-deep batch for classes of <= 16 rows per row group
   uint32_t owner_pieces; // pull steps whose largest per-tile pull is <= this many 32 KB
@@ -493,6 +494,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   stamp(1);
 
   bool done = false;  // this slot's solve has settled every reachable vertex
+  bool bailed = false;  // class budget exceeded (results invalid; host reruns)
   uint64_t pushed = 1, pulled = 0, settled = 1;
   uint32_t step = 1;
   while (!failed) {
@@ -575,7 +577,13 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         __syncthreads();
         stamp(3);
         ++step;
-        if (ucount == 0) {
+        if (!MULTI && p.max_classes && step > p.max_classes) {
+          // AUTO's class budget is spent: this graph has too many distance
+          // classes for class steps to beat n scan rounds -- stop; the host
+          // reruns the solve on the n-round engine (uniform: step is)
+          bailed = true;
+          done = true;
+        } else if (ucount == 0) {
           // nothing left any class could lower: every remaining finite column
           // is final (it would be elected later without relaxing anything)
           settled += fin;
@@ -1023,7 +1031,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   if (bx == 0 && tid == 0) {
     uint64_t* const info = S.info + slot * 4;
     info[0] = settled;
-    info[1] = step;
+    info[1] = step | (bailed ? 1ull << 63 : 0ull);
     info[2] = pushed;
     info[3] = pulled;
     S.info2[slot * 2] = nbar;

@@ -157,8 +157,7 @@ int parse_edge_list_text(const char* text, uint64_t len, uint64_t* n_out, uint64
   }
   *n_out = n;
   *m_out = m;
-  if (!edges) return 0;
-  if (cap < m) return 2;
+  if (edges && cap < m) return 2;
   // ---- body, in newline-aligned chunks on every host thread
   const unsigned T = narrow_threads();
   const uint64_t blen = (uint64_t)(end - body);
@@ -187,6 +186,24 @@ int parse_edge_list_text(const char* text, uint64_t len, uint64_t* n_out, uint64
   for (unsigned t = 0; t < T; ++t) {
     first[t] = header_line + 1 + acc;
     acc += lines[t];
+  }
+  if (!edges) {
+    // Header-only call: the caller sizes its buffer from m next, so a header
+    // the body does not back (e.g. '1 1000000000' over three lines) must fail
+    // HERE with the reference's ParseError instead of a 24 GB allocation.  When
+    // the body has exactly m candidate lines the second call validates them.
+    std::vector<uint64_t> cand(T, 0);
+    parallel_run([&](unsigned t) {
+      for_lines(cb[t], cb[t + 1], first[t], [&](std::string_view raw, uint64_t) {
+        const std::string_view line = trim(raw);
+        if (!line.empty() && line.front() != '#') ++cand[t];
+        return true;
+      });
+    });
+    uint64_t c = 0;
+    for (uint64_t x : cand) c += x;
+    if (c == m) return 0;
+    // otherwise the full pass below reports the reference's exact error
   }
   std::vector<std::vector<uint64_t>> local(T);
   std::vector<Err> errs(T);
@@ -237,6 +254,7 @@ int parse_edge_list_text(const char* text, uint64_t len, uint64_t* n_out, uint64
     *err = "expected " + std::to_string(m) + " edges, found " + std::to_string(total);
     return 1;
   }
+  if (!edges) return 0;  // (unreachable: a candidate count != m always errs above)
   std::vector<uint64_t> off(T + 1, 0);
   for (unsigned t = 0; t < T; ++t) off[t + 1] = off[t] + local[t].size();
   parallel_run([&](unsigned t) {

@@ -226,6 +226,7 @@ struct sssp_graph {
   uint64_t exch_base = 0;
   double transfer_in_s = 0;
   uint32_t pending = 0;  // solves of the last enqueued launch (0: nothing pending)
+  std::vector<uint64_t> last_sources;  // of the last enqueue (AUTO reruns a bailed bucket solve)
   uint32_t queued = 0;   // launches enqueued since the last finish
   uint64_t matrix_bytes = 0;
   uint64_t upload_bytes = 0;  // host->device bytes of the graph upload (stats)
@@ -994,6 +995,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
   if (k == 0 || k > g->max_batch) return fail(SSSP_ERR_BAD_ARG, "bad batch size");
   for (uint32_t i = 0; i < k; ++i)
     if (sources[i] >= g->n) return fail(SSSP_ERR_BAD_SOURCE, "dijkstra: source out of range");
+  g->last_sources.assign(sources, sources + k);
   if (g->wide) {  // k independent clusters, 64-bit distances (wide_kernel.cuh)
     Shard& s = g->sh[0];
     CK(cudaSetDevice(s.device));
@@ -1084,6 +1086,12 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.nshards = g->P;
         bp.loc_n = (uint32_t)s0.loc_n;
         bp.wmin = (uint32_t)std::min<uint64_t>(g->min_w, 0xFFFFFFFFull);
+        // AUTO picks the engine per call: a class step costs ~12 scan rounds
+        // (profiles/r01_configs_1gpu.jsonl: ~5.7 us vs ~0.45 us), so a solve
+        // that needs more than n/12 classes stops and reruns on the n-round
+        // engine (finish()).  One process only: every shard stops together.
+        bp.max_classes = g->opt.engine == SSSP_ENGINE_AUTO && !g->multiproc
+                             ? (uint32_t)std::max<uint64_t>(16, g->n / 12) : 0u;
         // A/B switches (read once per process): bulk-copy push,
         // 16-deep register push, owner-pull limit (0 = balanced pulls only)
         static const uint32_t k_push_ldg = env_u64("SSSP_PUSH_BULK", 0) ? 0u : 1u;
@@ -1221,7 +1229,7 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
   if (k == 0) return fail(SSSP_ERR_BAD_ARG, "nothing enqueued");
   double rounds = 0;
   uint64_t iters = 0, last = 0, mis = 0, classes = 0, rows = 0, nbars = 0;
-  bool timeout = false;
+  bool timeout = false, bailed = false;
   for (auto& s : g->sh) {
     CK(cudaSetDevice(s.device));
     CK(cudaMemcpyAsync(s.h_info, s.d_info, (uint64_t)k * 4 * sizeof(uint64_t),
@@ -1245,7 +1253,8 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
       if (g->bucket) {
         if (s.k == g->sh[0].k) {
           iters += s.h_info[4 * i];
-          classes += s.h_info[4 * i + 1];
+          bailed |= (s.h_info[4 * i + 1] >> 63) != 0;
+          classes += s.h_info[4 * i + 1] & ~(1ull << 63);
           rows += s.h_info[4 * i + 2] + s.h_info[4 * i + 3];
         }
         continue;
@@ -1258,6 +1267,23 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
   }
   g->pending = 0;
   g->queued = 0;
+  if (bailed && !timeout) {
+    // AUTO's class budget ran out (bucket_kernel.cuh): this graph is one for
+    // the n-round engine -- rerun these solves there, and keep it for the
+    // handle's later solves
+    g->bucket = false;
+    const std::vector<uint64_t> src = g->last_sources;
+    const float spent_ms = [&] {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, g->sh[0].ev0, g->sh[0].ev1);
+      return ms;
+    }();
+    int rc = launch(g, src.data(), (uint32_t)src.size());
+    if (rc) return rc;
+    rc = finish(g, st);
+    if (rc == SSSP_OK && st) st->rounds_s += spent_ms * 1e-3;  // both launches count
+    return rc;
+  }
   // AUTO re-plan: a distance class costs ~10x a scan round (measured: ~5 us vs
   // ~0.5 us), so a graph whose solves need more than n/8 classes (long sparse
   // paths: config 1 sparse has 154 classes at n=1000) runs faster on the

@@ -222,3 +222,25 @@ def test_long_chain_thousands_of_classes(gpu, oracle_c, engine):
     info, _ = check(gpu, oracle_c, g, int(order[0]), engine=engine)
     if engine == "bucket":
         assert info["engine"] == 3
+
+
+def test_auto_picks_scan_engine_on_the_first_call(gpu, oracle_c):
+    """The drop-in creates a handle per call, so AUTO must choose per call: a
+    graph with more than n/12 distance classes (config 1 sparse: 154 at
+    n=1000) stops the bucket solve on its class budget and reruns on the
+    n-round cluster engine inside the same dijkstra(G, s) -- exact either way."""
+    g = gpu.generate_sparse(1000, 42)
+    d, p = oracle_c.serial(g.adj, g.n, 0)
+    r = gpu.dijkstra(g, 0)
+    assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p)
+    assert r.stats["engine"] == 2
+    with gpu.DeviceGraph(g) as dg:
+        r1 = dg.solve(0)
+        assert r1.stats["engine"] == 2 and dg.info()["engine"] == 2  # kept for later solves
+        r2 = dg.solve(999)
+    d2, p2 = oracle_c.serial(g.adj, g.n, 999)
+    assert np.array_equal(r2.dist, d2) and np.array_equal(r2.pred, p2)
+    # few classes: AUTO stays on the bucket engine
+    gd = gpu.generate_dense(1000, 42)
+    rd = gpu.dijkstra(gd, 0)
+    assert rd.stats["engine"] == 3

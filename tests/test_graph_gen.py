@@ -1,6 +1,7 @@
 """Host-side graph builders of the product (include/sssp_graph_gen.h and the
 Python parse_edge_list mirror) against the reference: generate.hpp:15-83,
 graph.hpp:73-88 and :126-174 (test_generate.cpp, test_graph.cpp)."""
+import ctypes
 import hashlib
 import json
 import os
@@ -134,3 +135,27 @@ def test_native_parser_matches_reference(ref, seed):
                 with pytest.raises(P.ParseError) as ei:
                     P.parse_edge_list(text, directed)
                 assert ei.value.line == want[1] and str(ei.value) == want[2], (i, text)
+
+
+def test_header_m_not_backed_by_body_fails_before_allocation(ref):
+    # A header whose m the body does not back must give the reference's
+    # ParseError from the header-only call (graph.hpp:166-168), before the
+    # caller sizes a 3*m buffer (here 24 GB).
+    text = "3 1000000000\n0 1 5\n1 2 6\n"
+    want = ref.parse(text, False)
+    assert want[0] != "ok"
+    n, m, line = ctypes.c_uint64(), ctypes.c_uint64(), ctypes.c_uint64()
+    err = ctypes.create_string_buffer(256)
+    data = text.encode()
+    rc = P.lib.sssp_parse_edge_list(data, len(data), ctypes.byref(n), ctypes.byref(m), None, 0,
+                                    ctypes.byref(line), err, len(err))
+    assert rc != 0 and line.value == want[1]
+    with pytest.raises(P.ParseError) as ei:
+        P.parse_edge_list(text, False)
+    assert ei.value.line == want[1] and str(ei.value) == want[2]
+    # a body line error after a short body: the first error wins, as in the reference
+    text2 = "3 5\n0 1 5\n1 1 6\n"
+    want2 = ref.parse(text2, True)
+    with pytest.raises(P.ParseError) as ei:
+        P.parse_edge_list(text2, True)
+    assert ei.value.line == want2[1] and str(ei.value) == want2[2]
