@@ -106,6 +106,33 @@ def build_graph(n, seed, kind, cols=None):
     raise ValueError(kind)
 
 
+def host_info() -> dict:
+    """The host the CPU baseline ran on (lscpu model, nproc, free -g)."""
+    info = {"nproc": os.cpu_count()}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        for line in out.splitlines():
+            if line.startswith("Model name:"):
+                info["cpu_model"] = line.split(":", 1)[1].strip()
+            elif line.startswith("Socket(s):"):
+                info["sockets"] = int(line.split(":", 1)[1])
+    except Exception:
+        pass
+    try:
+        with open("/proc/meminfo") as f:
+            kb = int(f.readline().split()[1])
+        info["mem_total_gb"] = round(kb / 2**20, 1)
+    except Exception:
+        pass
+    return info
+
+
+def rotating_sources(n: int, first: int, k: int) -> list:
+    """k distinct-ish sources, `first` first: consecutive timed solves read
+    different rows of a matrix larger than L2 (the L2 rule of the timing contract)."""
+    return [(first + 7919 * i) % n for i in range(k)]
+
+
 def self_launch(nproc: int) -> int:
     """Re-runs this command under torch.distributed.run with nproc ranks on
     127.0.0.1 (a free port); returns the launcher's exit code."""
@@ -168,11 +195,82 @@ def run_reference(args, rank, world):
         "cpu_baseline": {"value": round(ms, 3), "unit": "ms", "cores": cores, "kind": "reference",
                          "sample": f"full {best} solve per step (reference dijkstra_* from "
                                    f"/root/reference/proj/include compiled into oracle/_ref)",
-                         "engine_probe_ms": {k: round(v * 1e3, 1) for k, v in probe.items()}},
+                         "engine_probe_ms": {k: round(v * 1e3, 1) for k, v in probe.items()},
+                         "host": host_info()},
         "e2e": {"value": round(ms, 3), "unit": "ms", "h2d_bytes_per_step": 0,
                 "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
+
+
+def run_configs(P, torch, peak, args) -> dict:
+    """BASELINE configs 1 (sparse + dense), 2 and 4 on one GPU: device ms per
+    solve (back to back, rotating sources, CUDA events), rows streamed, HBM
+    fraction, the reference's serial CPU solve of source 0 on this host as the
+    baseline AND the parity gate (bit-exact dist + pred, serial.hpp:26-68)."""
+    import oracle
+    R = oracle.REF()
+    ENG = P.ENGINE_NAMES
+    specs = [("1-sparse", "generate_sparse(1000,42) undirected",
+              lambda: P.generate_sparse(1000, 42)),
+             ("1-dense", "generate_dense(1000,42) undirected", lambda: P.generate_dense(1000, 42)),
+             ("2", "Bernoulli(16384, p=0.5, seed 16384) undirected",
+              lambda: P.generate_bernoulli(16384, 0.5, 16384)),
+             ("4", "Bernoulli(65536, p=0.001, seed 65536) DIRECTED (-w), 1 GPU here (8 in BASELINE)",
+              lambda: P.generate_bernoulli(65536, 0.001, 65536, directed=True))]
+    out = {}
+    for name, wl, build in specs:
+        t0 = time.perf_counter()
+        g = build()
+        t_build = time.perf_counter() - t0
+        hg = R.graph(g.adj, g.n, int(g.directed))
+        d, p, cpu_s = R.graph_serial(hg, g.n, 0)
+        R.graph_free(hg)
+        k = 10 if g.n > 20000 else 20
+        srcs = rotating_sources(g.n, 0, k)
+        with P.DeviceGraph(g) as dg:
+            r0 = dg.solve(0)
+            same = bool(np.array_equal(r0.dist, d) and np.array_equal(r0.pred, p))
+            if not same:
+                raise SystemExit(f"PARITY FAILURE: config {name} != reference dijkstra_serial")
+            invalid = sum(int(dg.validate(dg.solve(s)) != 0) for s in srcs)
+            if invalid:
+                raise SystemExit(f"VALIDATION FAILURE: config {name}: {invalid} sources")
+            stream = torch.cuda.ExternalStream(dg.stream_ptr())
+            for s in srcs[:3]:
+                dg.enqueue([s])
+                dg.finish()
+            torch.cuda.synchronize()
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            for s in srcs:
+                dg.enqueue([s])
+            e1.record(stream)
+            st = dg.finish()
+            torch.cuda.synchronize()
+            ms = e0.elapsed_time(e1) / k
+            rows = 0
+            for s in srcs:
+                dg.enqueue([s])
+                rows += dg.finish()["rows_read"]
+            rows /= k
+            info = dg.info()
+        nb = rows * g.n * info["weight_bytes"]
+        out[name] = {"workload": wl, "n": g.n, "engine": ENG[st["engine"]],
+                     "ms_per_solve": round(ms, 4), "kernel_ms": round(st["rounds_s"] * 1e3, 4),
+                     "sources": f"{k} rotating (0, 7919, ...)", "classes": st["classes"],
+                     "rows_read_mean": round(rows, 1), "weight_bytes": info["weight_bytes"],
+                     "roofline": {"bound": "hbm", "achieved_gbs": round(nb / (ms * 1e-3) / 1e9, 1),
+                                  "frac": round(nb / (ms * 1e-3) / 1e9 / peak, 4)},
+                     "parity": "source 0 dist and pred bit-identical to dijkstra_serial; all %d "
+                               "timed sources validate_result-valid" % k,
+                     "cpu_baseline": {"value": round(cpu_s * 1e3, 2), "unit": "ms", "cores": 1,
+                                      "kind": "reference",
+                                      "sample": "dijkstra_serial (oracle/_ref) from source 0"},
+                     "speedup_vs_cpu": round(cpu_s * 1e3 / ms, 1), "build_s": round(t_build, 1)}
+        print(f"config {name}: {json.dumps(out[name])}", file=sys.stderr, flush=True)
+        del g
+    return out
 
 
 def main():
@@ -249,13 +347,14 @@ def main():
         return D.open_shard(block, n, max_weight=100, device=local_rank, flags=args.flags,
                             ctas=args.ctas, engine=engine)
 
-    def time_engine(dg, steps, warmup, sample_clocks=False):
-        """W untimed + K timed solves, CUDA events on the library's launch
-        stream, barrier + synchronize on both sides, max over ranks."""
+    def time_engine(dg, steps, warmup, sample_clocks=False, sources=None):
+        """W untimed + K timed solves queued back to back, CUDA events on the
+        library's launch stream, barrier + synchronize on both sides, max over
+        ranks.  `sources` rotate (default: args.source only)."""
         stream = torch.cuda.ExternalStream(dg.stream_ptr())
-        src = [args.source]
-        for _ in range(warmup):
-            dg.enqueue(src)
+        srcs = sources or [args.source]
+        for i in range(warmup):
+            dg.enqueue([srcs[(i + 1) % len(srcs)]])
             dg.finish()
         sampler = ClockSampler(local_rank) if sample_clocks else None
         if sampler:
@@ -266,8 +365,8 @@ def main():
         ev_s = torch.cuda.Event(enable_timing=True)
         ev_e = torch.cuda.Event(enable_timing=True)
         ev_s.record(stream)
-        for _ in range(steps):  # queued back to back in stream order
-            dg.enqueue(src)
+        for i in range(steps):  # queued back to back in stream order
+            dg.enqueue([srcs[i % len(srcs)]])
         ev_e.record(stream)
         st = dg.finish()
         kern = [st["rounds_s"]]
@@ -283,20 +382,77 @@ def main():
             ms, kms = float(t[0]), float(t[1])
         return ms, kms, st, clocks
 
+    def time_cold(dg, sources, reps):
+        """Per-solve CUDA events with a 256 MiB write (> 126 MB L2) before every
+        solve: each solve starts with a cold L2 (and pays its own launch)."""
+        stream = torch.cuda.ExternalStream(dg.stream_ptr())
+        flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+        ts = []
+        for i in range(reps + 2):
+            with torch.cuda.stream(stream):
+                flush.fill_(i & 0xFF)
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            dg.enqueue([sources[i % len(sources)]])
+            e1.record(stream)
+            dg.finish()
+            torch.cuda.synchronize()
+            if i >= 2:
+                ts.append(e0.elapsed_time(e1))
+        del flush
+        return float(np.mean(ts)), float(np.min(ts))
+
     peak, peak_src = measured_peaks()
     loc_cols = n if world == 1 else P.pad_vertex_count(n, world) // world
     ENG = {1: "grid", 2: "cluster", 3: "bucket"}
 
-    # ---- the default engine (what dijkstra(G, s) runs) -> `value`
+    # ---- the default engine (what dijkstra(G, s) runs) -> `value`: K solves
+    # from K different sources back to back (each reads different rows of the
+    # 1 GiB matrix, > 126 MB L2), then every timed source's result validated
     dg = open_graph(args.engine)
     info = dg.info()
     wb = info["weight_bytes"]
-    ms, kern_ms, st, clocks = time_engine(dg, args.steps, args.warmup, sample_clocks=True)
+    srcs = rotating_sources(n, args.source, args.steps) if world == 1 else [args.source]
+    ms, kern_ms, st, clocks = time_engine(dg, args.steps, args.warmup, sample_clocks=True,
+                                          sources=srcs)
     engine = ENG[st["engine"]]
     res0 = dg.solve(args.source) if world == 1 else None
-    rows = st["rows_read"]
+    validated = None
+    if world == 1:
+        bad = 0
+        for s in sorted(set(srcs)):
+            bad += dg.validate(dg.solve(s)) != 0
+        validated = {"sources": len(set(srcs)), "invalid": int(bad),
+                     "check": "validate_result (oracle.hpp:51-120) on the device for every timed "
+                              "source; source %d also bit-exact vs the reference's dijkstra_serial "
+                              "(cpu_baseline.parity)" % args.source}
+        if bad:
+            raise SystemExit(f"VALIDATION FAILURE: {bad} timed sources invalid")
+    rows = st["rows_read"]  # of the last timed solve
+    # rows streamed per solve, averaged over the timed sources (each solve reads
+    # only the rows its distance classes need)
+    if world == 1 and engine == "bucket":
+        rsum = 0
+        for s in srcs:
+            dg.enqueue([s])
+            rsum += dg.finish()["rows_read"]
+        rows = rsum / len(srcs)
     alg_bytes = rows * loc_cols * wb  # every streamed row slice once
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
+    cold = time_cold(dg, srcs, 10) if world == 1 else None
+    skel = None
+    if world == 1 and engine == "bucket":
+        nbar = int(st["barriers"])
+        t_skel = dg.probe_skeleton(nbar, 100) * 1e3  # ms per launch, same shape, no data
+        t_hbm = alg_bytes / (peak * 1e9) * 1e3
+        skel = {"bound": "sync+hbm", "barriers": nbar, "t_skeleton_ms": round(t_skel, 5),
+                "t_hbm_ms": round(t_hbm, 5), "t_roof_ms": round(t_skel + t_hbm, 5),
+                "frac": round((t_skel + t_hbm) / ms, 4),
+                "note": "floor of a solve with this many grid barriers: the same cooperative "
+                        "launch doing only the barriers, back to back (sssp_probe_skeleton, "
+                        "this run), plus its algorithmic bytes at the measured HBM peak; "
+                        "frac = t_roof / ms_per_step"}
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(tpath):
@@ -372,22 +528,42 @@ def main():
     batch = None
     if not args.no_batch:
         gb = P.generate_bernoulli(16384, 0.5, 16384)
-        srcs = [256 * k for k in range(64)][rank::world]
+        bsrcs = [256 * k for k in range(64)][rank::world]
         with P.DeviceGraph(gb, (local_rank,)) as bdg:
             bstream = torch.cuda.ExternalStream(bdg.stream_ptr())
             for _ in range(2):
-                bdg.enqueue(srcs)
+                bdg.enqueue(bsrcs)
                 bdg.finish()
             if dist is not None:
                 dist.barrier()
             torch.cuda.synchronize()
             b0, b1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
             b0.record(bstream)
-            bdg.enqueue(srcs)
+            bdg.enqueue(bsrcs)
             b1.record(bstream)
             bst = bdg.finish()
             torch.cuda.synchronize()
             bms = b0.elapsed_time(b1)
+            # parity: every source validated on the device (validate_result),
+            # the first two bit-exact against the reference's dijkstra_serial
+            bres = bdg.solve_batch(bsrcs)
+            binvalid = sum(int(bdg.validate(r) != 0) for r in bres)
+        bpar = None
+        if rank == 0 and not args.no_cpu_baseline:
+            import oracle
+            R = oracle.REF()
+            hg = R.graph(gb.adj, gb.n)
+            cpu_s, same = [], True
+            for r in bres[:2]:
+                d, p, t = R.graph_serial(hg, gb.n, r.source)
+                cpu_s.append(t)
+                same &= bool(np.array_equal(d, r.dist) and np.array_equal(p, r.pred))
+            R.graph_free(hg)
+            if not same or binvalid:
+                raise SystemExit("PARITY FAILURE: config-5 batch != reference dijkstra_serial")
+            bpar = {"value": round(1e3 * float(np.mean(cpu_s)), 1), "unit": "ms per source",
+                    "cores": 1, "kind": "reference",
+                    "sample": f"dijkstra_serial (oracle/_ref) from sources {bsrcs[0]}, {bsrcs[1]}"}
         if dist is not None:
             t = torch.tensor([bms], dtype=torch.float64, device="cuda")
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -395,7 +571,13 @@ def main():
         batch = {"workload": "config 5: 64 sources 256*k, generate_bernoulli(16384, 0.5, 16384), "
                              "sources split over the GPUs, one replica each",
                  "ms_all_sources": round(bms, 4), "ms_per_source": round(bms / 64, 5),
-                 "sources_per_gpu": len(srcs), "engine": ENG[bst["engine"]],
+                 "sources_per_gpu": len(bsrcs), "engine": ENG[bst["engine"]],
+                 "rows_read": bst["rows_read"],
+                 "achieved_gbs": round(bst["rows_read"] * 16384 * 1 / (bms * 1e-3) / 1e9, 1),
+                 "parity": ("all %d sources validate_result-valid on the device; sources %d, %d "
+                            "bit-identical to dijkstra_serial" % (len(bres), bsrcs[0], bsrcs[1]))
+                           if bpar else "device validate_result only",
+                 "cpu_baseline": bpar,
                  "scaling": "strong (64 sources in total)"}
         del gb
 
@@ -428,18 +610,27 @@ def main():
                                f"single source {args.source}",
                    "n": n, "parallelism": f"column-partitioned x{world}" if world > 1 else "1 GPU",
                    "engine": engine, "weight_bytes": wb,
-                   "l2": f"matrix {info['matrix_bytes'] / 2**20:.0f} MiB per GPU > 126 MB L2; "
-                         "rows are streamed at most once per solve (no flush needed)"},
+                   "l2": (f"matrix {info['matrix_bytes'] / 2**20:.0f} MiB per GPU > 126 MB L2; the "
+                          f"{len(set(srcs))} timed solves start from different sources "
+                          f"({srcs[0]}, {srcs[1 % len(srcs)]}, ...: 7919-strided), so each reads "
+                          f"different rows; ms_cold = the same solves each after a 256 MiB "
+                          f"L2 flush, per-solve events (launch included)"),
+                   "sources": "rotating" if world == 1 else "single"},
         "kernel_ms": round(kern_ms, 4),
+        "ms_cold": round(cold[0], 4) if cold else None,
         "solve": {"vertices_settled": st["iterations"], "classes": st["classes"],
-                  "rows_read": rows, "mispredicts": st["mispredicts"]},
+                  "rows_read_mean": round(float(rows), 1), "barriers": st["barriers"],
+                  "mispredicts": st["mispredicts"], "validated": validated},
         "gpu_launches": args.steps,
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
-                     "peak_source": peak_src, "bytes_per_launch": alg_bytes,
-                     "note": "algorithmic bytes = rows the engine must stream x n_local x "
-                             "weight_bytes (bucket: sum over classes of min(|class|, |unsettled|) "
-                             "rows; scan: n rows)"},
+                     "peak_source": peak_src, "bytes_per_launch": int(alg_bytes),
+                     "note": "algorithmic bytes = matrix rows the solve must stream x n_local x "
+                             "weight_bytes (bucket: per class the rows of the class (push) or "
+                             "of its still-improvable columns (pull), columns whose dist <= next "
+                             "class + min weight are final and not read; scan: n rows), mean over "
+                             "the timed sources, / kernel_ms"},
+        "latency_roofline": skel,
         "scan_engine": scan,
         "dataparallel_engine": dp,
         "batch": batch,
@@ -476,8 +667,16 @@ def main():
             line["cpu_baseline"] = {"value": round(cpu_s * 1e3, 1), "unit": "ms", "cores": 1,
                                     "kind": "reference",
                                     "sample": "one full dijkstra_serial solve of the same graph "
-                                              "(oracle/_ref, reference headers)",
-                                    "parity": "dist and pred bit-identical"}
+                                              "(oracle/_ref, reference headers), source %d; timing "
+                                              "scope {algorithm} as timed_run (bench.hpp:114-180), "
+                                              "graph build excluded (PAPER.md:35)" % args.source,
+                                    "parity": "dist and pred bit-identical",
+                                    "host": host_info()}
+        # ---- BASELINE configs 1, 2 and 4 beside the headline (config 5 is
+        # `batch`), each parity-gated against the reference's dijkstra_serial
+        if not args.no_configs:
+            del g
+            line["configs"] = run_configs(P, torch, peak, args)
     else:
         # ---- e2e at N GPUs: the collective dijkstra_distributed call -- every
         # rank uploads its host column block (narrow + H2D + permute), the

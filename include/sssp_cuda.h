@@ -231,6 +231,14 @@ int sssp_round_times(sssp_graph* g, uint64_t* ns_out, uint64_t cap, uint64_t* co
  * (device %globaltimer).  Collective in shard mode: every rank must call. */
 int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round);
 
+/* The bucket engine's synchronisation floor (SURVEY.md §8d roofline, sync
+ * term): `launches` back-to-back cooperative launches of an empty kernel with
+ * the solve's grid, block and shared memory doing `barriers` grid barriers;
+ * *seconds_per_launch = CUDA-event time / launches.  Single-shard bucket
+ * graphs only (SSSP_ERR_UNSUPPORTED otherwise). */
+int sssp_probe_skeleton(sssp_graph* g, uint32_t barriers, uint32_t launches,
+                        double* seconds_per_launch);
+
 #ifdef __cplusplus
 }
 #endif

@@ -339,6 +339,15 @@ class DeviceGraph:
         check(lib.sssp_probe_sync(self._h, rounds, ctypes.byref(out)), "sssp_probe_sync")
         return out.value
 
+    def probe_skeleton(self, barriers: int, launches: int = 50) -> float:
+        """Seconds per launch of the bucket engine's synchronisation skeleton:
+        the solve's cooperative launch shape doing `barriers` grid barriers and
+        nothing else (the floor under a solve with that many barriers)."""
+        out = ctypes.c_double()
+        check(lib.sssp_probe_skeleton(self._h, barriers, launches, ctypes.byref(out)),
+              "sssp_probe_skeleton")
+        return out.value
+
     def stream_ptr(self, local: int = 0) -> int:
         return lib.sssp_stream(self._h, local) or 0
 

@@ -1039,6 +1039,17 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   }
 }
 
+// The bucket engine's synchronisation skeleton (bench roofline): the same
+// cooperative launch shape and shared memory, `nbar` grid barriers, no data.
+// Its time per launch is the floor under a solve with that many barriers.
+__global__ void __launch_bounds__(kBucketThreads, 2) bucket_skeleton_kernel(uint32_t nbar,
+                                                                             uint32_t* sink) {
+  extern __shared__ __align__(16) uint32_t smem[];
+  if (threadIdx.x == 0) smem[0] = blockIdx.x;
+  for (uint32_t i = 0; i < nbar; ++i) cooperative_groups::this_grid().sync();
+  if (threadIdx.x == 0 && smem[0] == 0xFFFFFFFFu) sink[0] = 1;
+}
+
 __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t T, uint32_t G, uint32_t words,
                                                        uint32_t wbytes) {
   return 4ull * (2ull * T + bucket_round4(T / 32) + bucket_round4(G) + 2ull * bucket_round4(words) +

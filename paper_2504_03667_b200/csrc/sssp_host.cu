@@ -1867,6 +1867,36 @@ int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round) {
   return SSSP_OK;
 }
 
+int sssp_probe_skeleton(sssp_graph* g, uint32_t barriers, uint32_t launches,
+                        double* seconds_per_launch) {
+  if (!g || !seconds_per_launch || launches == 0) return fail(SSSP_ERR_BAD_ARG, "bad probe arguments");
+  if (!g->bucket || g->P != 1 || g->multiproc)
+    return fail(SSSP_ERR_UNSUPPORTED, "skeleton probe: single-shard bucket engine only");
+  if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
+  Shard& s = g->sh[0];
+  CK(cudaSetDevice(s.device));
+  const size_t smem = bucket_smem(g);
+  CK(raise_smem((const void*)bucket_skeleton_kernel, smem));
+  uint32_t* sink = nullptr;
+  CK(pool_alloc(s, (void**)&sink, 64) == SSSP_OK ? cudaSuccess : cudaErrorMemoryAllocation);
+  void* args[] = {(void*)&barriers, (void*)&sink};
+  for (int w = 0; w < 3; ++w)
+    CK(cudaLaunchCooperativeKernel((void*)bucket_skeleton_kernel, dim3(g->bG), dim3(kBucketThreads),
+                                   args, smem, s.stream));
+  CK(cudaEventRecord(s.ev0, s.stream));
+  for (uint32_t i = 0; i < launches; ++i)
+    CK(cudaLaunchCooperativeKernel((void*)bucket_skeleton_kernel, dim3(g->bG), dim3(kBucketThreads),
+                                   args, smem, s.stream));
+  CK(cudaEventRecord(s.ev1, s.stream));
+  CK(cudaEventSynchronize(s.ev1));
+  float ms = 0;
+  CK(cudaEventElapsedTime(&ms, s.ev0, s.ev1));
+  pool_free(s, sink);
+  CK(cudaStreamSynchronize(s.stream));
+  *seconds_per_launch = ms * 1e-3 / launches;
+  return SSSP_OK;
+}
+
 int sssp_validate(sssp_graph* g, uint64_t source, const uint64_t* dist, const uint64_t* pred,
                   uint64_t* violations) {
   if (!g || !dist || !pred || !violations) return fail(SSSP_ERR_BAD_ARG, "null argument");
