@@ -249,17 +249,20 @@ def run_configs(P, torch, peak, args) -> dict:
             st = dg.finish()
             torch.cuda.synchronize()
             ms = e0.elapsed_time(e1) / k
-            rows = 0
+            rows = nb = 0
             for s in srcs:
                 dg.enqueue([s])
-                rows += dg.finish()["rows_read"]
+                x = dg.finish()
+                rows += x["rows_read"]
+                nb += x["bytes_read"]
             rows /= k
+            nb /= k
             info = dg.info()
-        nb = rows * g.n * info["weight_bytes"]
         out[name] = {"workload": wl, "n": g.n, "engine": ENG[st["engine"]],
                      "ms_per_solve": round(ms, 4), "kernel_ms": round(st["rounds_s"] * 1e3, 4),
                      "sources": f"{k} rotating (0, 7919, ...)", "classes": st["classes"],
-                     "rows_read_mean": round(rows, 1), "weight_bytes": info["weight_bytes"],
+                     "rows_read_mean": round(rows, 1), "bytes_read_mean": int(nb),
+                     "weight_bytes": info["weight_bytes"],
                      "roofline": {"bound": "hbm", "achieved_gbs": round(nb / (ms * 1e-3) / 1e9, 1),
                                   "frac": round(nb / (ms * 1e-3) / 1e9 / peak, 4)},
                      "parity": "source 0 dist and pred bit-identical to dijkstra_serial; all %d "
@@ -429,16 +432,17 @@ def main():
                               "(cpu_baseline.parity)" % args.source}
         if bad:
             raise SystemExit(f"VALIDATION FAILURE: {bad} timed sources invalid")
-    rows = st["rows_read"]  # of the last timed solve
-    # rows streamed per solve, averaged over the timed sources (each solve reads
-    # only the rows its distance classes need)
-    if world == 1 and engine == "bucket":
-        rsum = 0
+    rows, alg_bytes = st["rows_read"], st["bytes_read"]  # of the last timed solve
+    # matrix bytes per solve, averaged over the timed sources (each solve reads
+    # only what its distance classes need; the kernel counts every load)
+    if world == 1:
+        rsum = bsum = 0
         for s in srcs:
             dg.enqueue([s])
-            rsum += dg.finish()["rows_read"]
-        rows = rsum / len(srcs)
-    alg_bytes = rows * loc_cols * wb  # every streamed row slice once
+            x = dg.finish()
+            rsum += x["rows_read"]
+            bsum += x["bytes_read"]
+        rows, alg_bytes = rsum / len(srcs), bsum / len(srcs)
     achieved = alg_bytes / (kern_ms * 1e-3) / 1e9
     cold = time_cold(dg, srcs, 10) if world == 1 else None
     skel = None
@@ -572,8 +576,8 @@ def main():
                              "sources split over the GPUs, one replica each",
                  "ms_all_sources": round(bms, 4), "ms_per_source": round(bms / 64, 5),
                  "sources_per_gpu": len(bsrcs), "engine": ENG[bst["engine"]],
-                 "rows_read": bst["rows_read"],
-                 "achieved_gbs": round(bst["rows_read"] * 16384 * 1 / (bms * 1e-3) / 1e9, 1),
+                 "rows_read": bst["rows_read"], "bytes_read": bst["bytes_read"] * len(bsrcs),
+                 "achieved_gbs": round(bst["bytes_read"] * len(bsrcs) / (bms * 1e-3) / 1e9, 1),
                  "parity": ("all %d sources validate_result-valid on the device; sources %d, %d "
                             "bit-identical to dijkstra_serial" % (len(bres), bsrcs[0], bsrcs[1]))
                            if bpar else "device validate_result only",
@@ -625,11 +629,13 @@ def main():
         "roofline": {"bound": "hbm", "achieved": round(achieved, 2), "peak": peak,
                      "unit": "GB/s", "frac": round(achieved / peak, 5), "traffic": traffic,
                      "peak_source": peak_src, "bytes_per_launch": int(alg_bytes),
-                     "note": "algorithmic bytes = matrix rows the solve must stream x n_local x "
-                             "weight_bytes (bucket: per class the rows of the class (push) or "
-                             "of its still-improvable columns (pull), columns whose dist <= next "
-                             "class + min weight are final and not read; scan: n rows), mean over "
-                             "the timed sources, / kernel_ms"},
+                     "note": "algorithmic bytes = matrix bytes the solve kernel loads, counted "
+                             "by the kernel (stats.bytes_read; bucket: per class the tile slices "
+                             "of the class rows (push), or the still-improvable columns' "
+                             "transposed rows read in vertex-id order up to the first "
+                             "min-weight hit (pull); columns whose dist <= next class + min "
+                             "weight are final and never read; scan: n rows), mean over the "
+                             "timed sources, / kernel_ms; ncu DRAM bytes in `traffic`"},
         "latency_roofline": skel,
         "scan_engine": scan,
         "dataparallel_engine": dp,

@@ -127,6 +127,8 @@ typedef struct {
                                  pull-combine barriers; scan / wide: = exchanges) */
   uint64_t upload_bytes;      /* host->device bytes of the graph upload (all local shards) */
   uint64_t download_bytes;    /* device->host bytes of one solve's dist + pred */
+  uint64_t bytes_read;        /* matrix bytes the solve kernel loaded per solve, all local shards
+                                 (bucket: counted by every CTA; scan / wide: rows x row bytes) */
 } sssp_solve_stats;
 
 typedef struct sssp_graph sssp_graph;

@@ -75,6 +75,7 @@ class Stats(ctypes.Structure):
         ("barriers", ctypes.c_uint64),
         ("upload_bytes", ctypes.c_uint64),
         ("download_bytes", ctypes.c_uint64),
+        ("bytes_read", ctypes.c_uint64),
     ]
 
     def as_dict(self) -> dict:

@@ -59,6 +59,7 @@ struct BucketLocal {
   uint64_t* pred_out;   // [loc_n]
   uint64_t* info;       // [4]: settled vertices, classes, rows pushed, rows pulled
   uint64_t* info2;      // [2]: barriers used, error
+  uint64_t* cta_bytes;  // [slots][ctab_stride]: matrix bytes each CTA of the solve loaded
   uint32_t shard;       // global shard index
 };
 
@@ -80,9 +81,8 @@ struct BucketParams {
   uint32_t max_classes; // AUTO: stop after this many classes (0 = no limit; single solves)
   uint32_t push_ldg;    // 1: push rows through registers (LDG) instead of bulk copies (A/B)
   uint32_t push_depth16;  // LDG push: one 16-deep batch for classes of <= 16 rows per row group
-  uint32_t owner_pieces; // pull steps whose largest per-tile pull is <= this many 32 KB
-                         // pieces (2 = all in flight at once) run on the column owners
-                         // (no combine barrier); 0 = never
+  uint32_t owner_cols;   // pull steps with <= this many open columns in every tile run
+                         // on the column owners (no combine barrier); 0 = never
   // Cross-launch barrier (nlocal < nshards): launch counters, by global shard.
   // The leader of every launch adds nlocal to EVERY shard's counter once per
   // barrier; a launch waits on the counter of its first shard.
@@ -102,6 +102,7 @@ struct BucketParams {
   uint64_t slot_bytes;
   uint64_t out_stride;
   uint32_t* done;       // [kBucketMaxSlots] per-slot done flags (nslots > 1)
+  uint32_t ctab_stride; // CTAs per slot in cta_bytes
 };
 
 __device__ __forceinline__ uint32_t pos_to_vid(uint32_t pos, uint32_t Q, uint32_t lbits,
@@ -496,6 +497,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   bool done = false;  // this slot's solve has settled every reachable vertex
   bool bailed = false;  // class budget exceeded (results invalid; host reruns)
   uint64_t pushed = 1, pulled = 0, settled = 1;
+  uint64_t my_bytes = (uint64_t)T * sizeof(W);  // matrix bytes this CTA loaded (class 0: one slice)
   uint32_t step = 1;
   while (!failed) {
     const uint32_t par = (uint32_t)((bar_base + nbar - 1) & 1ull);
@@ -508,9 +510,6 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       {
         const uint32_t* bm = gbm + par * words;
         for (uint32_t i = tid; i < words; i += kBucketThreads) sbm[i] = __ldcg(&bm[i]);
-        // this shard's published unsettled bitmap, staged for a pull step
-        const uint32_t* ub = ubm + par * lwords;
-        for (uint32_t i = tid; i < lwords; i += kBucketThreads) sub[i] = __ldcg(&ub[i]);
       }
       uint32_t lm_r[4], cc_r[4], uu_r[4], ff_r[4];  // G <= 4 * kBucketThreads tiles (host-checked)
 #pragma unroll
@@ -594,11 +593,9 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
           pull = adjT != nullptr && ucount < bcount;
           // small pulls run on the column owners: no partial minima to
           // combine, so no extra barrier (uniform: every CTA read the same counts)
-          {
-            const uint64_t rowB = p.adjT_stride * sizeof(W);
-            const uint64_t ppr = (rowB + kBucketChunk * 2 - 1) / (kBucketChunk * 2);  // 32 KB pieces
-            owner = pull && (uint64_t)mopen * ppr <= p.owner_pieces;
-          }
+          // (a column read in id order stops at its first w == wmin hit; a
+          // row of <= 32 KB bounds the no-hit case at 32 rounds of 4 KB)
+          owner = pull && mopen <= p.owner_cols && p.adjT_stride * sizeof(W) <= 32768;
           dk = d;
           fb = final_bound(d);
           // push: a tile none of whose columns is open after B_d skips the rows
@@ -617,6 +614,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
     if (relax && !pull) {
       // ---- PUSH: stream the rows of B_d (ascending ids), per-column min key
       pushed += bcount;
+      my_bytes += (uint64_t)bcount * T * sizeof(W);  // every class row's slice of this tile
       const uint32_t rg = tid / TPR, ct = tid - rg * TPR;  // row group, column thread
       K best[CPT];
 #pragma unroll
@@ -765,83 +763,105 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       __syncthreads();
       stamp(6);
     } else if (relax && owner) {
-      // ---- PULL on the column owners (small pulls): a CTA streams the
-      // transposed rows of its own open columns through the stage by bulk
-      // copies (pieces of <= 32 KB, two in flight) and folds each column's
-      // (w, u) minimum itself -- nothing to combine, no extra barrier.
+      // ---- PULL on the column owners (small pulls), in ascending vertex id.
+      // An open column's transposed row is read id-block by id-block: a round
+      // is 256 16 B chunks = chunk b of every participant run (ids
+      // [b*CPT*Q, (b+1)*CPT*Q) of a shard, since position q*L + s holds vertex
+      // s*Q + q), and the column is final as soon as its minimum so far has
+      // w == wmin -- no later (larger) id can beat it: a smaller w does not
+      // exist and an equal w loses the lowest-id tie (serial.hpp:46, 56).
+      // Dense classes hit in the first round (~4 KB instead of the row).  Up
+      // to 4 columns share a round; nothing is combined across CTAs, so the
+      // step needs no extra barrier.
       pulled += ucount;
       const uint32_t lim = (uint32_t)umin64((uint64_t)dk + p.wmin, (uint64_t)DINF - 1u);
-      uint32_t* ocol = reinterpret_cast<uint32_t*>(scomb);        // open columns of the tile
-      K* skey = reinterpret_cast<K*>(ocol + ((T + 3u) & ~3u));    // [2][8] warp minima
+      uint32_t* ocol = reinterpret_cast<uint32_t*>(scomb);      // open columns of the tile
+      K* skey = reinterpret_cast<K*>(ocol + ((T + 3u) & ~3u));  // [4][8] warp minima + [4] result
+      __shared__ uint32_t s_odone[4];
       if (tid == 0) s_cnt[0] = 0;
       __syncthreads();
       for (uint32_t col = tid; col < T; col += kBucketThreads)
         if (!((ssettled[col >> 5] >> (col & 31)) & 1u) && sdist[col] > lim)
           ocol[atomicAdd(&s_cnt[0], 1u)] = col;
-      fence_proxy_async();  // earlier generic accesses of the stage bytes
       __syncthreads();
       const uint32_t no = s_cnt[0];
-      const uint32_t rowB = (uint32_t)(p.adjT_stride * sizeof(W));
-      const uint32_t PB = min(rowB, (uint32_t)kBucketChunk * 2u);  // half the stage
-      const uint32_t ppr = (rowB + PB - 1u) / PB;                  // pieces per row
-      const uint32_t nit = no * ppr;
-      uint8_t* const stage = reinterpret_cast<uint8_t*>(schunk);
-      auto issue = [&](uint32_t it) {
-        const uint32_t c = ocol[it / ppr], pc = it % ppr;
-        const uint32_t pos = p0 + c;
-        const uint32_t v = p.adjT_by_pos ? pos : pos_to_vid(pos, p.Q, p.lbits, p.qbits);
-        const uint32_t bytes = min(PB, rowB - pc * PB);
-        const uint8_t* src = reinterpret_cast<const uint8_t*>(adjT + (size_t)v * p.adjT_stride) +
-                             (size_t)pc * PB;
-        uint8_t* dst = stage + (it & 1u) * PB;
-        if (tid == 0) mbar_arrive_expect_tx(&s_mbar[it & 1u], bytes);
-        for (uint32_t q = tid; q * 4096u < bytes; q += kBucketThreads)
-          bulk_g2s(dst + q * 4096u, src + q * 4096u, min(4096u, bytes - q * 4096u), &s_mbar[it & 1u]);
-      };
-      if (nit > 0) issue(0);
-      if (nit > 1) issue(1);
-      K run = KT::kNone;
-      for (uint32_t it = 0; it < nit; ++it) {
-        mbar_wait(&s_mbar[it & 1u], (mph >> (it & 1u)) & 1u);
-        mph ^= 1u << (it & 1u);
-        const uint32_t pc = it % ppr;
-        const uint32_t nch = min(PB, rowB - pc * PB) / 16u;
-        const uint4* sp = reinterpret_cast<const uint4*>(stage + (it & 1u) * PB);
-        const uint32_t pbase = pc * (PB / (uint32_t)sizeof(W));  // first position of the piece
-        for (uint32_t ch = tid; ch < nch; ch += kBucketThreads) {
-          const uint32_t pos0 = pbase + ch * CPT;
-          const uint32_t bits = (sbm[pos0 >> 5] >> (pos0 & 31)) & ((1u << CPT) - 1u);
-          if (!bits) continue;
-          const K kk = chunk_min(sp[ch], bits, gvid(pos0));
-          run = kk < run ? kk : run;
+      uint32_t nld = 0;  // 16 B chunks this thread loaded
+      const uint32_t nbits = p.lbits - (31u - __clz((uint32_t)CPT));  // log2(L / CPT)
+      const uint32_t total = p.nshards << (nbits + p.qbits);           // chunks per row
+      for (uint32_t c0 = 0; c0 < no; c0 += 4) {
+        const uint32_t nc = min(4u, no - c0);
+        const uint8_t* rows[4];
+#pragma unroll
+        for (uint32_t k = 0; k < 4; ++k) {
+          const uint32_t pos = p0 + ocol[c0 + min(k, nc - 1)];
+          const uint32_t v = p.adjT_by_pos ? pos : pos_to_vid(pos, p.Q, p.lbits, p.qbits);
+          rows[k] = reinterpret_cast<const uint8_t*>(adjT + (size_t)v * p.adjT_stride);
         }
-        if (pc == ppr - 1u) {  // the column's last piece: block minimum, apply
-          const uint32_t cpar = (it / ppr) & 1u;
-          K k = warp_min_key(run);
-          if (lane == 0) skey[cpar * 8 + warp] = k;
-          __syncthreads();
-          if (tid == 0) {
-            for (uint32_t w2 = 1; w2 < kBucketThreads / 32; ++w2) {
-              const K x = skey[cpar * 8 + w2];
-              k = x < k ? x : k;
-            }
-            const uint32_t col = ocol[it / ppr];
-            if (k != KT::kNone && KT::w(k) != WINF) {
-              const uint32_t cand = dk + KT::w(k);
-              if (cand < sdist[col]) {
-                sdist[col] = cand;
-                spred[col] = KT::u(k);
-              }
+        K best[4] = {KT::kNone, KT::kNone, KT::kNone, KT::kNone};
+        if (tid < 4) s_odone[tid] = tid >= nc ? 1u : 0u;
+        __syncthreads();
+        for (uint32_t base = 0; base < total; base += kBucketThreads) {
+          const uint32_t it = base + tid;
+          uint32_t bits = 0, g = 0;
+          uint4 v4[4];
+          if (it < total) {
+            const uint32_t q = it & (p.Q - 1u), t2 = it >> p.qbits;
+            const uint32_t b = t2 & ((1u << nbits) - 1u), j = t2 >> nbits;
+            g = j * (uint32_t)p.row_stride + (q << p.lbits) + b * CPT;
+            bits = (sbm[g >> 5] >> (g & 31)) & ((1u << CPT) - 1u);
+            if (bits) {
+#pragma unroll
+              for (uint32_t k = 0; k < 4; ++k)
+                if (!s_odone[k]) {
+                  v4[k] = __ldg(reinterpret_cast<const uint4*>(rows[k] + (size_t)g * sizeof(W)));
+                  ++nld;
+                }
             }
           }
-          run = KT::kNone;
+          if (bits) {
+            const uint32_t vid0 = gvid(g);
+#pragma unroll
+            for (uint32_t k = 0; k < 4; ++k)
+              if (!s_odone[k]) {
+                const K kk = chunk_min(v4[k], bits, vid0);
+                best[k] = kk < best[k] ? kk : best[k];
+              }
+          }
+#pragma unroll
+          for (uint32_t k = 0; k < 4; ++k) {
+            const K kk = warp_min_key(best[k]);
+            if (lane == 0) skey[k * 8 + warp] = kk;
+          }
+          __syncthreads();
+          if (tid < nc && !s_odone[tid]) {
+            K m = skey[tid * 8];
+            for (uint32_t w2 = 1; w2 < kBucketThreads / 32; ++w2) {
+              const K x = skey[tid * 8 + w2];
+              m = x < m ? x : m;
+            }
+            skey[32 + tid] = m;
+            if (m != KT::kNone && KT::w(m) == p.wmin) s_odone[tid] = 1u;  // final
+          }
+          __syncthreads();
+          if (s_odone[0] & s_odone[1] & s_odone[2] & s_odone[3]) break;  // uniform
         }
-        if (it + 2 < nit) {
-          fence_proxy_async();
-          __syncthreads();  // piece it's buffer is free
-          issue(it + 2);
+        if (tid < nc) {  // apply (strict '<': serial.hpp:56)
+          const K m = skey[32 + tid];
+          const uint32_t col = ocol[c0 + tid];
+          if (m != KT::kNone && KT::w(m) != WINF) {
+            const uint32_t cand = dk + KT::w(m);
+            if (cand < sdist[col]) {
+              sdist[col] = cand;
+              spred[col] = KT::u(m);
+            }
+          }
         }
+        __syncthreads();
       }
+      nld = __reduce_add_sync(0xFFFFFFFFu, nld);
+      if (lane == 0) s_red[warp] = nld;
+      __syncthreads();
+      for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) my_bytes += 16ull * s_red[w2];
       __syncthreads();
       stamp(13);
     } else if (relax && pull) {
@@ -854,6 +874,11 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       // atomicMin per column it touched, and after an extra barrier every
       // owner applies its columns' minima.
       pulled += ucount;
+      {  // this shard's published open-column bitmap (the pull work list)
+        const uint32_t* ub = ubm + par * lwords;
+        for (uint32_t i = tid; i < lwords; i += kBucketThreads) sub[i] = __ldcg(&ub[i]);
+        __syncthreads();
+      }
       // the combine region holds the touched columns' running keys and local
       // positions (ncols <= T + 2, host-checked); the id chunk region becomes
       // the cp.async stage [2][kPullDepth][threads] of 16 B slots
@@ -888,6 +913,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       const uint32_t total = nuL * cpr;
       const uint32_t per = (total + Gs - 1) / Gs;
       const uint32_t lo = min(total, bx * per), hi = min(total, lo + per);
+      my_bytes += 16ull * (hi - lo);  // every item of the range is streamed
       const uint32_t r0 = cpow2 ? lo >> cbits : lo / cpr;
       const uint32_t ncols = lo < hi ? (cpow2 ? (hi - 1) >> cbits : (hi - 1) / cpr) - r0 + 1 : 0;
       if (ncols && base < r0 + ncols && base + c > r0) {
@@ -1035,6 +1061,13 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
     info[2] = pushed;
     info[3] = pulled;
     S.info2[slot * 2] = nbar;
+  }
+  if (S.cta_bytes) {
+    if (tid == 0) S.cta_bytes[slot * p.ctab_stride + bx] = my_bytes;
+    if (bx == 0)  // entries of a wider tiling's CTAs (not in this launch) read as 0
+      for (uint32_t i = Gs + tid; i < p.ctab_stride; i += kBucketThreads) S.cta_bytes[slot * p.ctab_stride + i] = 0;
+  }
+  if (bx == 0 && tid == 0) {
     if (cross && blockIdx.x == 0) *p.bar_epoch = bar_base + nbar;  // every CTA read it before barrier 1
   }
 }

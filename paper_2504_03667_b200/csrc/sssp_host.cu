@@ -190,6 +190,7 @@ struct Shard {
   void* d_adjT = nullptr;        // transpose in position order (nullptr: symmetric or absent)
   const void* pull_src = nullptr;// d_adjT, or d_adj when the matrix is symmetric
   uint64_t* d_info2 = nullptr;   // bucket: [B][2] barriers used, watchdog
+  uint64_t* d_ctab = nullptr;    // bucket: [B][ctab] matrix bytes loaded per CTA
   uint64_t* d_trace = nullptr;   // debug (SSSP_BUCKET_TRACE)
   bool peer_ipc[kMaxShards] = {};
   bool own_stream = true;        // false: shares the stream of the device's first shard
@@ -219,6 +220,7 @@ struct sssp_graph {
   uint64_t bseq = 0;                     // bucket launch tags (watchdog reports)
   uint32_t bslots = 1;                   // bucket: independent solves per launch (one shard)
   uint32_t bTb = 0, bGb = 0, bslots_b = 0;  // batch tiling: wider tiles, more slots per launch
+  uint32_t ctab = 0;                     // bucket: CTAs per solve slot in d_ctab (max tiling)
   uint64_t done_off = 0;                 // bucket: per-slot done flags (after the slot regions)
   uint64_t slots_bytes = 0;              // scan-engine exchange region (start of d_slots)
   uint64_t bar_off = 0, arrive_off = 0, epoch_off = 0, release_off = 0, ctrl_off = 0, bm_off = 0, ubm_off = 0, pkey_off = 0,
@@ -498,6 +500,11 @@ int alloc_state(sssp_graph* g, Shard& s) {
   for (int i = 0; i < 5; ++i)
     if (pool_alloc(s, bufs[i], sizes[i])) return SSSP_ERR_OOM;
   CK(cudaMemsetAsync(s.d_info2, 0, B * 2 * sizeof(uint64_t), s.stream));
+  if (g->bucket) {
+    g->ctab = std::max(g->bG, g->bGb);
+    if (pool_alloc(s, (void**)&s.d_ctab, B * g->ctab * sizeof(uint64_t))) return SSSP_ERR_OOM;
+    CK(cudaMemsetAsync(s.d_ctab, 0, B * g->ctab * sizeof(uint64_t), s.stream));
+  }
   s.h_sources = static_cast<uint32_t*>(pinned_get(B * sizeof(uint32_t)));
   s.h_info = static_cast<uint64_t*>(pinned_get(B * 4 * sizeof(uint64_t)));
   if (!s.h_sources || !s.h_info) return fail(SSSP_ERR_OOM, "pinned host allocation failed");
@@ -898,7 +905,7 @@ void destroy_graph(sssp_graph* g) {
     if (s.slots_pooled) pool_free(s, s.d_slots);
     else cudaFree(s.d_slots);
     for (void* p : {(void*)s.d_dist, (void*)s.d_pred, (void*)s.d_info, (void*)s.d_sources,
-                    (void*)s.d_visit, (void*)s.d_round_ns, (void*)s.d_info2, s.d_adjT})
+                    (void*)s.d_visit, (void*)s.d_round_ns, (void*)s.d_info2, s.d_adjT, (void*)s.d_ctab})
       pool_free(s, p);
     if (s.stream) cudaStreamSynchronize(s.stream);
     cudaFree(s.d_trace);
@@ -1072,6 +1079,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
           L.pred_out = s.d_pred + (uint64_t)i * s.loc_n;
           L.info = s.d_info + (uint64_t)i * 4;
           L.info2 = s.d_info2 + (uint64_t)i * 2;
+          L.cta_bytes = s.d_ctab + (uint64_t)i * g->ctab;
           L.shard = s.k;
         }
         bp.adjT_by_pos = s0.pull_src == s0.d_adj ? 0u : 1u;  // transpose rows: local positions
@@ -1096,10 +1104,10 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         // 16-deep register push, owner-pull limit (0 = balanced pulls only)
         static const uint32_t k_push_ldg = env_u64("SSSP_PUSH_BULK", 0) ? 0u : 1u;
         static const uint32_t k_depth16 = env_u64("SSSP_PUSH_DEPTH16", 0) ? 1u : 0u;
-        static const uint32_t k_owner = (uint32_t)env_u64("SSSP_OWNER_PULL_PIECES", 2);
+        static const uint32_t k_owner = (uint32_t)env_u64("SSSP_OWNER_PULL_COLS", 4);
         bp.push_ldg = k_push_ldg;
         bp.push_depth16 = k_depth16;
-        bp.owner_pieces = k_owner;
+        bp.owner_cols = k_owner;
         for (uint32_t j = 0; j < g->P; ++j) {
           char* base = reinterpret_cast<char*>(g->multiproc ? (void*)s0.peer[j] : (void*)g->sh[j].d_slots) +
                        g->slots_bytes;
@@ -1112,6 +1120,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.arrive = reinterpret_cast<unsigned long long*>(own0 + g->arrive_off);
         bp.release = reinterpret_cast<unsigned long long*>(own0 + g->release_off);
         bp.done = reinterpret_cast<uint32_t*>(own0 + g->done_off);
+        bp.ctab_stride = g->ctab;
         bp.timeout_ns = g->opt.timeout_ms * 1000000ull;
         if (getenv("SSSP_BUCKET_TRACE") && s0.k == 0) {  // debug: per-barrier timestamps
           if (!s0.d_trace) CK(cudaMalloc(&s0.d_trace, (64 + 2048) * 8));
@@ -1228,7 +1237,7 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
   const uint32_t k = g->pending;
   if (k == 0) return fail(SSSP_ERR_BAD_ARG, "nothing enqueued");
   double rounds = 0;
-  uint64_t iters = 0, last = 0, mis = 0, classes = 0, rows = 0, nbars = 0;
+  uint64_t iters = 0, last = 0, mis = 0, classes = 0, rows = 0, nbars = 0, nbytes = 0;
   bool timeout = false, bailed = false;
   for (auto& s : g->sh) {
     CK(cudaSetDevice(s.device));
@@ -1244,6 +1253,10 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
         timeout |= i2[2 * i + 1] == g->bseq - k + 1 + i;
         if (s.k == g->sh[0].k) nbars += i2[2 * i];
       }
+      std::vector<uint64_t> cb((uint64_t)k * g->ctab);
+      CK(cudaMemcpyAsync(cb.data(), s.d_ctab, cb.size() * 8, cudaMemcpyDeviceToHost, s.stream));
+      CK(cudaStreamSynchronize(s.stream));
+      for (uint64_t x : cb) nbytes += x;
     }
     CK(cudaStreamSynchronize(s.stream));
     float ms = 0;
@@ -1330,6 +1343,8 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     fill_reference_stats(g, st);
     st->exchanges = (g->bucket ? classes : iters) / k;
     st->barriers = g->bucket ? nbars / std::min<uint32_t>(k, 64) : st->exchanges;
+    st->bytes_read = g->bucket ? nbytes / k
+                               : iters / k * g->sh[0].row_stride * g->wbytes * g->P;
     st->matrix_bytes = g->matrix_bytes;
     st->weight_bytes = g->wbytes;
     st->ctas = g->cluster ? g->sh[0].C : g->sh[0].G;
@@ -2088,6 +2103,7 @@ int sssp_solve_dataparallel(sssp_graph* g, uint64_t source, uint64_t* dist_out, 
     st->iterations = info[0];
     st->rows_read = info[1] + g->n * (tree_passes + (flag ? info[2] : 0));
     st->relax_checks = st->rows_read * rs;
+    st->bytes_read = st->rows_read * rs * wb;
     st->matrix_bytes = g->matrix_bytes;
     st->weight_bytes = wb;
     st->ctas = G;

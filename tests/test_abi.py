@@ -43,7 +43,7 @@ def test_abi_constants_and_strings():
     for code in range(9):
         assert _native.lib.sssp_status_string(code)
     assert ctypes.sizeof(_native.Options) == 56
-    assert ctypes.sizeof(_native.Stats) == 160
+    assert ctypes.sizeof(_native.Stats) == 168
 
 
 def test_struct_layout_matches_header():

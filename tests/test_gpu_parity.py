@@ -350,6 +350,8 @@ def test_reference_counters_and_collective_stats(gpu, oracle_c):
     with gpu.DeviceGraph(gd, engine="bucket") as dg:
         rb = dg.solve(0)
     assert rb.stats["exchanges"] == rb.stats["classes"] and rb.stats["barriers"] >= 2
+    # matrix bytes the kernel loaded: at most the rows it touched (+ the source row)
+    assert 0 < rb.stats["bytes_read"] <= (rb.stats["rows_read"] + 1) * 2048 * rb.stats["weight_bytes"]
     # the C ABI struct carries the shard count's CollectiveStats too
     with gpu.DeviceGraph(g, [0, 0, 0]) as dg:
         r3 = dg.solve(0)

@@ -66,7 +66,7 @@ def main():
             ts, st = time_solves(dg, [0], a.reps, flush)
             info = dg.info()
         rows = st["rows_read"]
-        nb = rows * info.get("row_stride", g.n) * info["weight_bytes"]
+        nb = st["bytes_read"]
         print(json.dumps({"config": name, "n": g.n, "parity": ok, "engine": st["engine"],
                           "ms_mean": round(float(ts.mean()), 4), "ms_min": round(float(ts.min()), 4),
                           "ms_p50": round(float(np.median(ts)), 4),
