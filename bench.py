@@ -296,6 +296,8 @@ def main():
     ap.add_argument("--no-configs", action="store_true",
                     help="skip the per-config objects (BASELINE configs 1, 2, 4, 5)")
     ap.add_argument("--ref-skip-partitioned", action="store_true")
+    ap.add_argument("--no-host-driven", action="store_true",
+                    help="skip the host-driven per-round allreduce comparison (SURVEY §8e)")
     args = ap.parse_args()
     args.warmup = max(3, args.warmup)
 
@@ -508,6 +510,36 @@ def main():
         if world == 1:
             r1 = sdg.solve(args.source)
             assert r1 == res0, "scan engine != default engine"
+        # SURVEY §8e comparison: the same rounds with a HOST-driven per-round
+        # all_reduce(MIN) of the 8-byte key (NCCL at N > 1) between a
+        # local_min and a relax launch, padded_n rounds like the reference
+        if not args.no_host_driven:
+            from paper_2504_03667_b200 import distributed as D
+            hd = []
+            for _ in range(2):  # warm-up + timed
+                if dist is not None:
+                    dist.barrier()
+                dl, pl, secs = D.solve_host_driven(sdg, n, args.source)
+                hd.append(secs)
+            t = hd[-1]
+            if dist is not None:
+                tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+                dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+                t = float(tt[0])
+            same = None
+            if world == 1:
+                same = bool(np.array_equal(dl, res0.dist) and np.array_equal(pl, res0.pred))
+                if not same:
+                    raise SystemExit("PARITY FAILURE: host-driven rounds != device engine")
+            rounds_hd = P.pad_vertex_count(n, world)
+            scan["host_driven"] = {
+                "ms": round(t * 1e3, 3), "rounds": rounds_hd,
+                "us_per_round": round(t * 1e6 / rounds_hd, 3),
+                "collective": ("torch.distributed all_reduce(int64 MIN) per round, NCCL "
+                               if world > 1 else "none (one rank): ") + "between 2 launches",
+                "equals_device_engine": same,
+                "note": "host-driven local_min -> allreduce -> relax per round (sssp_nccl_*), "
+                        "the comparison for the device-initiated per-round exchange above"}
         sdg.close()
         # per-round latency histogram (%globaltimer at every round end; one
         # extra traced solve, outside the timed region)

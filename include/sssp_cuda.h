@@ -233,6 +233,21 @@ int sssp_round_times(sssp_graph* g, uint64_t* ns_out, uint64_t cap, uint64_t* co
  * (device %globaltimer).  Collective in shard mode: every rank must call. */
 int sssp_probe_sync(sssp_graph* g, uint32_t rounds, double* seconds_per_round);
 
+/* Host-driven comparison path: the reference's partitioned
+ * round (partitioned.hpp:142-154) with the allreduce done by the HOST between
+ * two launches -- begin(source) once, then every round
+ *   sssp_nccl_local_min(g, key)   local_min (:81-90) -> 8-byte key on the device
+ *   <caller: ncclAllReduce(key, int64, MIN) across the shards' ranks>
+ *   sssp_nccl_relax(g, key)       relax_owned (:106-119) with the winner
+ * for n rounds, then end() copies this shard's dist/pred (col_count entries;
+ * n for one process).  Key = (dist << 32 | vertex) ^ 2^63: signed MIN orders it
+ * as the (dist, vertex) MinLocPair.  Kernels run on sssp_stream(g, 0).  One
+ * local shard, 32-bit distances; results bit-identical to dijkstra_serial. */
+int sssp_nccl_begin(sssp_graph* g, uint64_t source);
+int sssp_nccl_local_min(sssp_graph* g, uint64_t* d_key);
+int sssp_nccl_relax(sssp_graph* g, const uint64_t* d_key);
+int sssp_nccl_end(sssp_graph* g, uint64_t* dist_out, uint64_t* pred_out);
+
 /* The bucket engine's synchronisation floor (SURVEY.md §8d roofline, sync
  * term): `launches` back-to-back cooperative launches of an empty kernel with
  * the solve's grid, block and shared memory doing `barriers` grid barriers;

@@ -30,7 +30,8 @@ EXPORTED = (
     "sssp_graph_create", "sssp_graph_create_from_edges", "sssp_shard_create", "sssp_shard_export", "sssp_shard_connect",
     "sssp_shard_range", "sssp_graph_destroy", "sssp_graph_info", "sssp_solve",
     "sssp_solve_batch", "sssp_enqueue", "sssp_finish", "sssp_stream",
-    "sssp_probe_sync", "sssp_probe_skeleton", "sssp_validate", "sssp_solve_dataparallel", "sssp_round_times", "sssp_block_weight_range", "sssp_gen_dense", "sssp_gen_sparse", "sssp_gen_bernoulli", "sssp_graph_from_edges", "sssp_parse_edge_list",
+    "sssp_probe_sync", "sssp_probe_skeleton", "sssp_nccl_begin", "sssp_nccl_local_min",
+    "sssp_nccl_relax", "sssp_nccl_end", "sssp_validate", "sssp_solve_dataparallel", "sssp_round_times", "sssp_block_weight_range", "sssp_gen_dense", "sssp_gen_sparse", "sssp_gen_bernoulli", "sssp_graph_from_edges", "sssp_parse_edge_list",
 )
 
 
@@ -123,6 +124,10 @@ def _load() -> ctypes.CDLL:
         "sssp_probe_sync": (ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.POINTER(ctypes.c_double)]),
         "sssp_probe_skeleton": (ctypes.c_int, [_vp, ctypes.c_uint32, ctypes.c_uint32,
                                                ctypes.POINTER(ctypes.c_double)]),
+        "sssp_nccl_begin": (ctypes.c_int, [_vp, ctypes.c_uint64]),
+        "sssp_nccl_local_min": (ctypes.c_int, [_vp, _vp]),
+        "sssp_nccl_relax": (ctypes.c_int, [_vp, _vp]),
+        "sssp_nccl_end": (ctypes.c_int, [_vp, _u64p, _u64p]),
         "sssp_validate": (ctypes.c_int, [_vp, ctypes.c_uint64, _u64p, _u64p, _u64p]),
         "sssp_solve_dataparallel": (ctypes.c_int, [_vp, ctypes.c_uint64, _u64p, _u64p, _u64p,
                                                    ctypes.POINTER(Stats)]),

@@ -24,6 +24,7 @@
 #include "dataparallel_kernel.cuh"
 #include "validate_kernel.cuh"
 #include "wide_kernel.cuh"
+#include "nccl_kernel.cuh"
 #include "dispatch.h"
 #include "host_narrow.h"
 
@@ -232,6 +233,10 @@ struct sssp_graph {
   uint32_t queued = 0;   // launches enqueued since the last finish
   uint64_t matrix_bytes = 0;
   uint64_t upload_bytes = 0;  // host->device bytes of the graph upload (stats)
+  // host-driven NCCL comparison path (nccl_kernel.cuh): per-position state
+  uint32_t* nc_dist = nullptr;
+  uint32_t* nc_pred = nullptr;
+  uint8_t* nc_vis = nullptr;
 };
 
 namespace {
@@ -896,6 +901,10 @@ int create_shard_objects(sssp_graph* g, uint32_t P, const int* devices, uint32_t
 }
 
 void destroy_graph(sssp_graph* g) {
+  if (g->nc_dist && !g->sh.empty()) {
+    cudaSetDevice(g->sh[0].device);
+    for (void* p : {(void*)g->nc_dist, (void*)g->nc_pred, (void*)g->nc_vis}) pool_free(g->sh[0], p);
+  }
   for (auto& s : g->sh) {
     cudaSetDevice(s.device);
     if (s.stream) cudaStreamSynchronize(s.stream);
@@ -1909,6 +1918,94 @@ int sssp_probe_skeleton(sssp_graph* g, uint32_t barriers, uint32_t launches,
   pool_free(s, sink);
   CK(cudaStreamSynchronize(s.stream));
   *seconds_per_launch = ms * 1e-3 / launches;
+  return SSSP_OK;
+}
+
+// ---- host-driven NCCL comparison path (nccl_kernel.cuh)
+namespace {
+int nccl_params(sssp_graph* g, NcclRoundParams* p) {
+  if (g->sh.size() != 1 || g->wide || !g->cluster)
+    return fail(SSSP_ERR_UNSUPPORTED, "NCCL comparison path: one local shard, cluster layout, 32-bit distances");
+  if (g->multiproc && !g->connected) return fail(SSSP_ERR_BAD_ARG, "shard not connected");
+  const Shard& s = g->sh[0];
+  p->adj = s.d_adj;
+  p->row_stride = s.row_stride;
+  p->npos = (uint32_t)s.row_stride;
+  p->Q = s.G;
+  p->qbits = bitlen(s.G) - 1;
+  p->lbits = bitlen(s.L) - 1;
+  p->loc_n = (uint32_t)s.loc_n;
+  p->col_base = (uint32_t)s.col_base;
+  p->n = (uint32_t)g->n;
+  p->dist = g->nc_dist;
+  p->pred = g->nc_pred;
+  p->visited = g->nc_vis;
+  return SSSP_OK;
+}
+unsigned nccl_grid(uint32_t npos) { return (unsigned)std::min<uint64_t>((npos + 255) / 256, 148ull * 8); }
+}  // namespace
+
+int sssp_nccl_begin(sssp_graph* g, uint64_t source) {
+  if (!g) return fail(SSSP_ERR_BAD_ARG, "null handle");
+  if (source >= g->n) return fail(SSSP_ERR_BAD_SOURCE, "dijkstra_partitioned: source out of range");
+  if (g->pending) return fail(SSSP_ERR_BAD_ARG, "a launch is pending");
+  NcclRoundParams p{};
+  int rc = nccl_params(g, &p);
+  if (rc) return rc;
+  Shard& s = g->sh[0];
+  CK(cudaSetDevice(s.device));
+  if (!g->nc_dist) {
+    if (pool_alloc(s, (void**)&g->nc_dist, s.row_stride * 4) || pool_alloc(s, (void**)&g->nc_pred, s.row_stride * 4) ||
+        pool_alloc(s, (void**)&g->nc_vis, s.row_stride))
+      return fail(SSSP_ERR_OOM, "NCCL path state");
+    nccl_params(g, &p);
+  }
+  nccl_init_kernel<<<nccl_grid(p.npos), 256, 0, s.stream>>>(p, (uint32_t)source);
+  CK(cudaGetLastError());
+  return SSSP_OK;
+}
+
+int sssp_nccl_local_min(sssp_graph* g, uint64_t* d_key) {
+  if (!g || !d_key) return fail(SSSP_ERR_BAD_ARG, "null argument");
+  NcclRoundParams p{};
+  int rc = nccl_params(g, &p);
+  if (rc) return rc;
+  if (!g->nc_dist) return fail(SSSP_ERR_BAD_ARG, "sssp_nccl_begin first");
+  nccl_local_min_kernel<<<1, kNcclMinThreads, 0, g->sh[0].stream>>>(p, d_key);
+  CK(cudaGetLastError());
+  return SSSP_OK;
+}
+
+int sssp_nccl_relax(sssp_graph* g, const uint64_t* d_key) {
+  if (!g || !d_key) return fail(SSSP_ERR_BAD_ARG, "null argument");
+  NcclRoundParams p{};
+  int rc = nccl_params(g, &p);
+  if (rc) return rc;
+  if (!g->nc_dist) return fail(SSSP_ERR_BAD_ARG, "sssp_nccl_begin first");
+  const unsigned grid = nccl_grid(p.npos);
+  cudaStream_t st = g->sh[0].stream;
+  if (g->wbytes == 1) nccl_relax_kernel<uint8_t><<<grid, 256, 0, st>>>(p, d_key);
+  else if (g->wbytes == 2) nccl_relax_kernel<uint16_t><<<grid, 256, 0, st>>>(p, d_key);
+  else nccl_relax_kernel<uint32_t><<<grid, 256, 0, st>>>(p, d_key);
+  CK(cudaGetLastError());
+  return SSSP_OK;
+}
+
+int sssp_nccl_end(sssp_graph* g, uint64_t* dist_out, uint64_t* pred_out) {
+  if (!g || !dist_out || !pred_out) return fail(SSSP_ERR_BAD_ARG, "null argument");
+  NcclRoundParams p{};
+  int rc = nccl_params(g, &p);
+  if (rc) return rc;
+  if (!g->nc_dist) return fail(SSSP_ERR_BAD_ARG, "sssp_nccl_begin first");
+  Shard& s = g->sh[0];
+  CK(cudaSetDevice(s.device));
+  nccl_out_kernel<<<nccl_grid(p.npos), 256, 0, s.stream>>>(p, s.d_dist, s.d_pred);
+  CK(cudaGetLastError());
+  if (s.cols) {
+    CK(cudaMemcpyAsync(dist_out, s.d_dist, s.cols * 8, cudaMemcpyDeviceToHost, s.stream));
+    CK(cudaMemcpyAsync(pred_out, s.d_pred, s.cols * 8, cudaMemcpyDeviceToHost, s.stream));
+  }
+  CK(cudaStreamSynchronize(s.stream));
   return SSSP_OK;
 }
 

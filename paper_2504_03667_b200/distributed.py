@@ -14,7 +14,7 @@ from typing import Optional, Sequence
 
 import numpy as np
 
-from . import ShardGraph, ShortestPathResult, pad_vertex_count
+from . import ShardGraph, ShortestPathResult, _p64, pad_vertex_count
 
 
 def shard_range(n: int, world: int, rank: int) -> tuple:
@@ -87,3 +87,61 @@ def dijkstra_distributed(block: np.ndarray, n: int, source: int, max_weight: int
         dist.barrier(group)
         sg.close()
     return gather_result(source, n, r.dist, r.pred, group)
+
+
+def solve_host_driven(dg, n: int, source: int, group=None) -> tuple:
+    """The comparison path of SURVEY.md §8e: the reference's partitioned round
+    (partitioned.hpp:142-154) with the per-round allreduce_minloc (:94-101)
+    issued by the HOST -- local_min kernel, ``all_reduce(key, MIN)`` (NCCL on a
+    GPU group; through a host copy on gloo), relax kernel -- for all padded_n
+    rounds, as the reference runs them (:205).  ``dg`` is this rank's
+    ShardGraph (or a one-shard DeviceGraph without a process group).  Returns
+    (dist, pred of the owned columns, device seconds of the rounds).  Same
+    results as the device P2P exchange; it exists to time that choice."""
+    import ctypes
+
+    import torch
+
+    from . import _native
+    lib = _native.lib
+    world = 1
+    dist = None
+    if group is not None or _dist_ready():
+        import torch.distributed as dist
+        world = dist.get_world_size(group)
+    rounds = pad_vertex_count(n, world)
+    _native.check(lib.sssp_nccl_begin(dg._h, source), "sssp_nccl_begin")
+    dev = torch.device("cuda", torch.cuda.current_device())
+    stream = torch.cuda.ExternalStream(dg.stream_ptr(), device=dev)
+    key = torch.empty(1, dtype=torch.int64, device=dev)
+    host = dist is not None and world > 1 and dist.get_backend(group) != "nccl"
+    keyh = torch.empty(1, dtype=torch.int64, pin_memory=True) if host else None
+    kp = ctypes.c_void_p(key.data_ptr())
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with torch.cuda.stream(stream):
+        e0.record(stream)
+        for _ in range(rounds):
+            _native.check(lib.sssp_nccl_local_min(dg._h, kp), "sssp_nccl_local_min")
+            if dist is not None and world > 1:
+                if host:
+                    keyh.copy_(key)
+                    stream.synchronize()
+                    dist.all_reduce(keyh, op=dist.ReduceOp.MIN, group=group)
+                    key.copy_(keyh, non_blocking=True)
+                else:
+                    dist.all_reduce(key, op=dist.ReduceOp.MIN, group=group)
+            _native.check(lib.sssp_nccl_relax(dg._h, kp), "sssp_nccl_relax")
+        e1.record(stream)
+    cols = dg.row_len
+    d = np.empty(cols, np.uint64)
+    p = np.empty(cols, np.uint64)
+    _native.check(lib.sssp_nccl_end(dg._h, _p64(d), _p64(p)), "sssp_nccl_end")
+    return d, p, e0.elapsed_time(e1) * 1e-3
+
+
+def _dist_ready() -> bool:
+    try:
+        import torch.distributed as dist
+        return dist.is_available() and dist.is_initialized()
+    except Exception:
+        return False

@@ -59,3 +59,69 @@ def test_two_ranks_one_gpu(gpu, n, directed):
         pr.join(60)
     for rank, out in res:
         assert out == [True, True], (rank, out)
+
+
+def _rank_host_driven(rank, world, port, n, seed, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port), RANK=str(rank),
+                      WORLD_SIZE=str(world))
+    import torch
+    import torch.distributed as dist
+    torch.cuda.set_device(0)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle
+        import paper_2504_03667_b200 as P
+        from paper_2504_03667_b200 import distributed as D
+        b, c = D.shard_range(n, world, rank)
+        block = P.generate_dense(n, seed, cols=(b, c))
+        sg = D.open_shard(block, n, max_weight=100, device=0, engine="cluster", timeout_ms=120000)
+        out = []
+        adj = oracle.C().dense(n, seed)
+        for src in (0, n - 1):
+            d_loc, p_loc, secs = D.solve_host_driven(sg, n, src)
+            res = D.gather_result(src, n, d_loc, p_loc)
+            d, p = oracle.C().serial(adj, n, src)
+            out.append(bool(np.array_equal(res.dist, d) and np.array_equal(res.pred, p)) and secs > 0)
+        dist.barrier()
+        sg.close()
+        q.put((rank, out))
+    except Exception as e:
+        q.put((rank, repr(e)))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_host_driven_allreduce_two_ranks(gpu):
+    """SURVEY §8e comparison path: local_min kernel -> host all_reduce(MIN) of
+    the packed key (gloo here: both ranks share the one GPU) -> relax kernel,
+    padded_n rounds; the gathered result equals dijkstra_serial."""
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _port()
+    procs = [ctx.Process(target=_rank_host_driven, args=(r, 2, port, 301, 5, q)) for r in range(2)]
+    for pr in procs:
+        pr.start()
+    res = [q.get(timeout=600) for _ in range(2)]
+    for pr in procs:
+        pr.join(60)
+    for rank, out in res:
+        assert out == [True, True], (rank, out)
+
+
+def test_host_driven_single_process(gpu, oracle_c):
+    """The same rounds without a process group (one shard): bit-exact, incl.
+    ties, zero weights and unreachable vertices (all padded_n rounds run)."""
+    from paper_2504_03667_b200 import distributed as D
+    rng = np.random.default_rng(9)
+    for n, directed in [(500, False), (777, True)]:
+        adj = np.where(rng.random((n, n)) < 0.02, rng.integers(0, 4, (n, n)), -1).astype(np.int64)
+        a = np.where(adj < 0, np.uint64(0xFFFFFFFFFFFFFFFF), adj.astype(np.uint64))
+        if not directed:
+            a = np.minimum(a, a.T)
+        np.fill_diagonal(a, 0)
+        g = gpu.Graph(n, directed, a.reshape(-1))
+        with gpu.DeviceGraph(g, engine="cluster") as dg:
+            for s in (0, n // 3):
+                dl, pl, secs = D.solve_host_driven(dg, n, s)
+                d, p = oracle_c.serial(g.adj, n, s)
+                assert np.array_equal(dl, d) and np.array_equal(pl, p), (n, s)
