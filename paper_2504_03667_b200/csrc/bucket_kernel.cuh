@@ -102,6 +102,8 @@ struct BucketParams {
   uint64_t slot_bytes;
   uint64_t out_stride;
   uint32_t* done;       // [kBucketMaxSlots] per-slot done flags (nslots > 1)
+  uint32_t dbg_reps;    // debug (SSSP_BUCKET_REPS): repeat the class-1 row scan
+  const uint32_t* rsum; // [n][4] row summaries (row_summary_kernel; one shard only) or nullptr
   uint32_t ctab_stride; // CTAs per slot in cta_bytes
 };
 
@@ -228,6 +230,7 @@ __host__ __device__ constexpr uint32_t bucket_round4(uint32_t x) { return (x + 3
 __host__ __device__ constexpr size_t bucket_smem_bytes(uint32_t T, uint32_t G, uint32_t words,
                                                        uint32_t wbytes);
 constexpr int kBucketChunk = kBucketThreads * 32 * 2;  // ids of one pass over 512 bitmap words
+constexpr uint32_t kIdCap = kBucketChunk / 2;           // ids of one push pass (the rest stages rows)
 
 // Dynamic smem: dist[T] u32 | pred[T] u32 | settled[T/32] u32 | lmin[GT] u32 |
 //               bitmap[nshards*row_stride/32] u32 | unsettled[same] u32 | chunk[kBucketChunk] u32 |
@@ -338,7 +341,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   // trace entry = phase code << 56 | %globaltimer (CTA 0 of shard 0, debug)
   auto stamp = [&](uint32_t code) {
     if (p.trace && me == 0 && slot == 0 && tid == 0 && ntr < 64)
-      p.trace[ntr++] = ((uint64_t)code << 56) | (globaltimer() & ((1ull << 56) - 1));
+      p.trace[ntr++] = ((uint64_t)code << 56) | ((uint64_t)clock64() & ((1ull << 56) - 1));
   };
   // One barrier over every CTA of every shard.  All shards in this launch:
   // the cooperative grid barrier (1.29 us at 256 CTAs, the fastest measured
@@ -490,20 +493,156 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   if (MULTI && bx == 0 && tid == 0) p.done[slot] = 0;  // read after the first barrier
   stamp(12);  // class-0 row slice loaded
   uint32_t fb = final_bound(0);  // class 0 = {source} at distance 0
-  publish((uint32_t)(bar_base & 1ull), fb);
-  barrier();
-  stamp(1);
 
   bool done = false;  // this slot's solve has settled every reachable vertex
   bool bailed = false;  // class budget exceeded (results invalid; host reruns)
   uint64_t pushed = 1, pulled = 0, settled = 1;
   uint64_t my_bytes = (uint64_t)T * sizeof(W);  // matrix bytes this CTA loaded (class 0: one slice)
   uint32_t step = 1;
+  uint32_t ids_n = 0xFFFFFFFFu;  // B_d ids already staged in schunk (class 1 from the row summary)
+
+  // ---- class 1 without an exchange (one shard).  rsum[source] holds what the
+  // exchange after class 0 would produce -- d1 = min_v w(source, v), |B_1|,
+  // the open-column count left after B_1, the finite count (row_summary_kernel)
+  // -- so every CTA knows the first class; B_1 itself is found by scanning row
+  // `source` (one row, L2-resident after the first CTA's miss).  A class-1
+  // PULL, or a class too large for one id pass, takes the exchange as before.
+  // With several slots the choice is made for all of them together, so every
+  // slot counts the same barriers.
+  bool local1 = false;
+  uint32_t l_d1 = DINF, l_bc = 0, l_uc = 0, l_fin = 0;
+  if (p.rsum) {
+    local1 = true;
+    for (uint32_t s2 = 0; s2 < (MULTI ? p.nslots : 1u); ++s2) {
+      const uint32_t src2 = MULTI ? p.slot_src[s2] : source;
+      const uint4 r4 = __ldg(reinterpret_cast<const uint4*>(p.rsum + (size_t)src2 * 4));
+      const bool pull1 = r4.x != DINF && r4.z != 0 && adjT != nullptr && r4.z < r4.y;
+      local1 = local1 && !pull1 && r4.y <= kIdCap;
+      if (src2 == source) {
+        l_d1 = r4.x;
+        l_bc = r4.y;
+        l_uc = r4.z;
+        l_fin = r4.w;
+      }
+    }
+  }
+  stamp(16);
+  bool pre = false;  // the first loop step's class decisions are already made
+  __shared__ uint32_t s_pre[4];  // its d, |B_d|, open count, relax (smem: not live across the loop)
+  if (local1) {
+    if (l_d1 == DINF) {  // no finite edge out of the source
+      done = true;
+    } else if (l_uc == 0) {  // nothing any class could lower (see the determination)
+      settled += l_fin;
+      done = true;
+    } else {
+      // B_1 = the positions of row `source` holding d1 (not the source, not padding)
+      for (uint32_t rr = 0; rr < p.dbg_reps; ++rr) {
+      if (tid == 0) s_cnt[0] = 0;
+      __syncthreads();
+      const uint4* row4 = reinterpret_cast<const uint4*>(adj + (size_t)source * p.row_stride);
+      const uint32_t pos_src = ((source & (p.Q - 1u)) << p.lbits) | (source >> p.qbits);
+      const uint32_t nch = (uint32_t)(p.row_stride * sizeof(W) / 16);
+      for (uint32_t c0 = 0; c0 < nch; c0 += kBucketThreads * 8) {
+        // each lane: a 16-bit mask of its chunk's d1 positions per 16 B chunk;
+        // one warp prefix + one shared atomic per warp place the ids (a
+        // per-lane branch on a match diverges in almost every warp)
+        uint32_t mk[8], cnt = 0;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const uint32_t j = c0 + tid + k * kBucketThreads;
+          mk[k] = 0;
+          if (j < nch) {
+            const uint4 v = __ldcg(row4 + j);
+            const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              if constexpr (sizeof(W) == 1) {  // exact zero-byte mask of w ^ d1x4 -> 4 bits
+                const uint32_t t = wd[e] ^ (l_d1 * 0x01010101u);
+                const uint32_t z = ~(((t & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | t | 0x7F7F7F7Fu);
+                mk[k] |= ((((z >> 7) * 0x00204081u) >> 21) & 0xFu) << (4 * e);
+              } else {
+#pragma unroll
+                for (int b = 0; b < 4 / (int)sizeof(W); ++b) {
+                  const uint32_t w = sizeof(W) == 4 ? wd[e] : (wd[e] >> (8 * sizeof(W) * b)) & WINF;
+                  if (w == l_d1) mk[k] |= 1u << (e * (4 / sizeof(W)) + b);
+                }
+              }
+            }
+            // not class members: the source's own entry and padding positions
+            if (j == pos_src / CPT) mk[k] &= ~(1u << (pos_src % CPT));
+            if (p.n < p.row_stride) {  // chunk = CPT positions of one run: ids vid0, vid0 + Q, ...
+              const uint32_t vid0 = pos_to_vid(j * CPT, p.Q, p.lbits, p.qbits);
+              const uint32_t nv = vid0 >= p.n ? 0u : min((uint32_t)CPT, (p.n - vid0 + p.Q - 1) >> p.qbits);
+              mk[k] &= nv >= 32 ? 0xFFFFFFFFu : (1u << nv) - 1u;
+            }
+          }
+          cnt += __popc(mk[k]);
+        }
+        if (!__any_sync(0xFFFFFFFFu, cnt != 0)) continue;
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+          if (lane >= (uint32_t)o) incl += t;
+        }
+        uint32_t base = 0;
+        if (lane == 31) base = atomicAdd(&s_cnt[0], incl);
+        base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - cnt;
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          for (uint32_t m = mk[k]; m; m &= m - 1) {
+            const uint32_t pos = (c0 + tid + k * kBucketThreads) * CPT + (__ffs(m) - 1);
+            schunk[base++] = pos_to_vid(pos, p.Q, p.lbits, p.qbits);
+          }
+      }
+      __syncthreads();
+      stamp(17);
+      }
+      // my tile's class-1 columns are settled now
+      for (uint32_t i = warp; i < TW; i += kBucketThreads / 32) {
+        const uint32_t bits = __ballot_sync(
+            0xFFFFFFFFu, !((ssettled[i] >> lane) & 1u) && sdist[i * 32 + lane] == l_d1);
+        if (lane == 0) ssettled[i] |= bits;
+      }
+      __syncthreads();
+      ids_n = s_cnt[0];  // == l_bc
+      settled += l_bc;
+      step = 2;
+      fb = final_bound(l_d1);
+      // push: a tile none of whose columns is open after B_1 skips the rows
+      const uint32_t lim = (uint32_t)umin64((uint64_t)l_d1 + p.wmin, (uint64_t)DINF - 1u);
+      bool open = false;
+      for (uint32_t col = tid; col < T; col += kBucketThreads)
+        open |= !((ssettled[col >> 5] >> (col & 31)) & 1u) && sdist[col] > lim;
+      const bool relax0 = __syncthreads_or(open);
+      if (!relax0) ids_n = 0xFFFFFFFFu;  // nothing to push into this tile
+      if (tid == 0) {
+        s_pre[0] = l_d1;
+        s_pre[1] = l_bc;
+        s_pre[2] = l_uc;
+        s_pre[3] = relax0;
+      }
+      __syncthreads();
+      pre = true;
+    }
+    stamp(15);
+  } else {
+    publish((uint32_t)(bar_base & 1ull), fb);
+    barrier();
+    stamp(1);
+  }
   while (!failed) {
     const uint32_t par = (uint32_t)((bar_base + nbar - 1) & 1ull);
     bool relax = false, pull = false, owner = false;
     uint32_t dk = 0, bcount = 0, ucount = 0;
-    if (!done) {
+    if (pre) {
+      pre = false;
+      dk = s_pre[0];
+      bcount = s_pre[1];
+      ucount = s_pre[2];
+      relax = s_pre[3] != 0;
+    } else if (!done) {
       // ---- the class: d = min over tiles, B_d = candidates of the tiles at d.
       // One memory round trip: every tile's (lmin, candidates, unsettled) and
       // the whole candidate bitmap are loaded together, then reduced in smem.
@@ -624,11 +763,16 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
       // per thread), otherwise passes of one word per thread (<= kIdCap ids
       // each); the rest of the chunk region stages the row slices
       constexpr uint32_t WMAX = 8;
-      constexpr uint32_t kIdCap = kBucketChunk / 2;
       const uint32_t wpt = (bcount <= kIdCap && words <= WMAX * kBucketThreads)
                                ? (words + kBucketThreads - 1) / kBucketThreads
                                : 1u;
       for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads * wpt) {
+        uint32_t tot;
+        if (ids_n != 0xFFFFFFFFu) {  // class 1 from the row summary: ids already in schunk
+          tot = ids_n;
+          ids_n = 0xFFFFFFFFu;
+          wbase = words;  // one pass
+        } else {
         const uint32_t w0 = wbase + tid * wpt;
         uint32_t bw[WMAX];
         uint32_t c = 0;
@@ -646,7 +790,8 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         }
         if (lane == 31) s_red[warp] = incl;
         __syncthreads();
-        uint32_t wofs = 0, tot = 0;
+        uint32_t wofs = 0;
+        tot = 0;
         for (uint32_t w2 = 0; w2 < kBucketThreads / 32; ++w2) {
           if (w2 < warp) wofs += s_red[w2];
           tot += s_red[w2];
@@ -656,6 +801,7 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
         for (uint32_t k2 = 0; k2 < WMAX; ++k2)
           for (uint32_t m = bw[k2]; m; m &= m - 1)
             schunk[o++] = gvid((w0 + k2) * 32 + (__ffs(m) - 1));
+        }
         stamp(4);
         if (kBucketAB && !p.push_ldg) {
           // Row slices staged by bulk copies: thread t issues the copies of
@@ -1054,6 +1200,10 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
     }
   }
   stamp(11);
+  if (p.trace && tid == 0 && slot == 0 && me < 1024) {  // debug: every CTA's start / end
+    p.trace[64 + 2048 + 2 * me] = t_start;
+    p.trace[64 + 2048 + 2 * me + 1] = globaltimer();
+  }
   if (bx == 0 && tid == 0) {
     uint64_t* const info = S.info + slot * 4;
     info[0] = settled;
@@ -1069,6 +1219,68 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
   }
   if (bx == 0 && tid == 0) {
     if (cross && blockIdx.x == 0) *p.bar_epoch = bar_base + nbar;  // every CTA read it before barrier 1
+  }
+}
+
+// Row summaries for class 1 (bucket_kernel's exchange-free first class, one
+// shard): for source u, exactly the values the exchange after class 0 yields
+// (dist after class 0 = row u, source and padding settled):
+//   [0] d1 = min finite w(u, v) over v != u (DINF: none)   [1] |B_1| = #{v : w == d1}
+//   [2] open columns after B_1: #{v : dist > fb0} minus B_1 when d1 > fb0
+//       (fb0 = 1 + wmin, final_bound(0); INF counts as open)
+//   [3] finite columns #{v : w != INF}
+// One CTA per row, two passes (min, then counts); run once at upload.
+template <typename W>
+__global__ void __launch_bounds__(256) row_summary_kernel(const W* __restrict__ adj, uint64_t row_stride,
+                                                          uint32_t n, uint32_t Q, uint32_t qbits,
+                                                          uint32_t lbits, uint32_t fb0, uint4* out) {
+  constexpr uint32_t WINF = WInf<W>::v, DINF = 0xFFFFFFFFu;
+  __shared__ uint32_t s_r[4][8];
+  const uint32_t u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const W* row = adj + (size_t)u * row_stride;
+  auto dist_at = [&](uint32_t pos) -> uint32_t {  // DINF also for the source and padding (settled)
+    const uint32_t v = pos_to_vid(pos, Q, lbits, qbits);
+    if (v >= n || v == u) return 0u;              // settled: not a candidate, not open
+    const uint32_t w = row[pos];
+    return w != WINF ? w : DINF;
+  };
+  uint32_t m = DINF;
+  for (uint32_t pos = tid; pos < row_stride; pos += 256) {
+    const uint32_t d = dist_at(pos);
+    if (d != 0u) m = min(m, d);
+  }
+  m = __reduce_min_sync(0xFFFFFFFFu, m);
+  if (lane == 0) s_r[0][warp] = m;
+  __syncthreads();
+  m = DINF;
+  for (int w2 = 0; w2 < 8; ++w2) m = min(m, s_r[0][w2]);
+  uint32_t eq = 0, open = 0, fin = 0;
+  for (uint32_t pos = tid; pos < row_stride; pos += 256) {
+    const uint32_t d = dist_at(pos);
+    if (d == 0u) continue;
+    const bool cls = m != DINF && d == m;
+    eq += cls ? 1u : 0u;
+    fin += d != DINF ? 1u : 0u;
+    open += (d > fb0 && !(cls && m > fb0)) ? 1u : 0u;
+  }
+  eq = __reduce_add_sync(0xFFFFFFFFu, eq);
+  open = __reduce_add_sync(0xFFFFFFFFu, open);
+  fin = __reduce_add_sync(0xFFFFFFFFu, fin);
+  if (lane == 0) {
+    s_r[1][warp] = eq;
+    s_r[2][warp] = open;
+    s_r[3][warp] = fin;
+  }
+  __syncthreads();
+  if (tid == 0) {
+    uint4 r = make_uint4(m, 0, 0, 0);
+    for (int w2 = 0; w2 < 8; ++w2) {
+      r.y += s_r[1][w2];
+      r.z += s_r[2][w2];
+      r.w += s_r[3][w2];
+    }
+    if (m == DINF) r.y = 0;
+    out[u] = r;
   }
 }
 

@@ -189,6 +189,7 @@ struct Shard {
   uint64_t* peer[kMaxShards] = {};
   // bucket engine (bucket_kernel.cuh)
   void* d_adjT = nullptr;        // transpose in position order (nullptr: symmetric or absent)
+  uint4* d_rsum = nullptr;       // bucket, one shard: per-row class-1 summaries (row_summary_kernel)
   const void* pull_src = nullptr;// d_adjT, or d_adj when the matrix is symmetric
   uint64_t* d_info2 = nullptr;   // bucket: [B][2] barriers used, watchdog
   uint64_t* d_ctab = nullptr;    // bucket: [B][ctab] matrix bytes loaded per CTA
@@ -798,6 +799,18 @@ int prepare_bucket_impl(sssp_graph* g) {
     const uint32_t Q = s.G, L = s.L, qb = bitlen(Q) - 1, lb = bitlen(L) - 1;
     const uint64_t rs = s.row_stride;
     s.pull_src = nullptr;
+    if (g->P == 1) {  // class-1 row summaries: one CTA per row, once per upload
+      if (!s.d_rsum && pool_alloc(s, (void**)&s.d_rsum, g->n * sizeof(uint4)) != SSSP_OK) return SSSP_ERR_OOM;
+      const uint32_t fb0 = (uint32_t)std::min<uint64_t>(1 + g->min_w, 0xFFFFFFFEull);
+      const unsigned nb = (unsigned)g->n;
+      if (g->wbytes == 1)
+        row_summary_kernel<uint8_t><<<nb, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, fb0, s.d_rsum);
+      else if (g->wbytes == 2)
+        row_summary_kernel<uint16_t><<<nb, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, fb0, s.d_rsum);
+      else
+        row_summary_kernel<uint32_t><<<nb, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, fb0, s.d_rsum);
+      CK(cudaGetLastError());
+    }
     if (rs % 64) continue;
     const uint64_t mbytes = g->n * rs * g->wbytes;
     if (g->P == 1) {
@@ -914,7 +927,8 @@ void destroy_graph(sssp_graph* g) {
     if (s.slots_pooled) pool_free(s, s.d_slots);
     else cudaFree(s.d_slots);
     for (void* p : {(void*)s.d_dist, (void*)s.d_pred, (void*)s.d_info, (void*)s.d_sources,
-                    (void*)s.d_visit, (void*)s.d_round_ns, (void*)s.d_info2, s.d_adjT, (void*)s.d_ctab})
+                    (void*)s.d_visit, (void*)s.d_round_ns, (void*)s.d_info2, s.d_adjT, (void*)s.d_ctab,
+                    (void*)s.d_rsum})
       pool_free(s, p);
     if (s.stream) cudaStreamSynchronize(s.stream);
     cudaFree(s.d_trace);
@@ -1047,7 +1061,8 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
     cfg.numAttrs = 1;
     void* args[] = {(void*)&wp};
     CK(cudaLaunchKernelExC(&cfg, wide_fn(g->wbytes), args));
-    CK(cudaEventRecord(s.ev1, s.stream));
+    // the end event is recorded by finish(): an event record between two
+    // back-to-back launches costs ~3 us of GPU time (tools/ubench_launch2.cu)
     g->pending = k;
     g->queued += 1;
     return SSSP_OK;
@@ -1132,11 +1147,16 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.ctab_stride = g->ctab;
         bp.timeout_ns = g->opt.timeout_ms * 1000000ull;
         if (getenv("SSSP_BUCKET_TRACE") && s0.k == 0) {  // debug: per-barrier timestamps
-          if (!s0.d_trace) CK(cudaMalloc(&s0.d_trace, (64 + 2048) * 8));
-          CK(cudaMemsetAsync(s0.d_trace, 0, (64 + 2048) * 8, s0.stream));
+          if (!s0.d_trace) CK(cudaMalloc(&s0.d_trace, (64 + 4096) * 8));
+          CK(cudaMemsetAsync(s0.d_trace, 0, (64 + 4096) * 8, s0.stream));
           bp.trace = s0.d_trace;
         }
         bp.seq = g->bseq + 1 + i;
+        static const uint32_t k_reps = (uint32_t)std::max<uint64_t>(1, env_u64("SSSP_BUCKET_REPS", 1));
+        bp.dbg_reps = k_reps;
+        // exchange-free class 1 (one shard; A/B: SSSP_BUCKET_LOCAL1=0)
+        static const bool k_local1 = env_u64("SSSP_BUCKET_LOCAL1", 1) != 0;
+        bp.rsum = k_local1 && g->P == 1 ? reinterpret_cast<const uint32_t*>(s0.d_rsum) : nullptr;
         void* args[] = {&bp};
         const uint32_t grid = tiles * (ns > 1 ? ns : bp.nlocal);
         // local shards other than the first wait for the launch on the
@@ -1146,10 +1166,12 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
       }
       i += ns;
     }
-    for (auto& s : g->sh) {
-      CK(cudaSetDevice(s.device));
-      CK(cudaEventRecord(s.ev1, s.stream));
-    }
+    for (const auto& gr : groups)  // group leaders record their end event in finish()
+      for (size_t li = 1; li < gr.size(); ++li) {
+        Shard& s = g->sh[gr[li]];
+        CK(cudaSetDevice(s.device));
+        CK(cudaEventRecord(s.ev1, s.stream));
+      }
     g->bseq += k;
     g->pending = k;
     g->queued += 1;
@@ -1216,7 +1238,8 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
     Shard& s0 = g->sh[grp[0]];
     CK(cudaSetDevice(s0.device));
     CK(launch_kernel(g, grp, (void*)s0.fn, k, ps, nullptr, 0, nullptr));
-    for (uint32_t li : grp) CK(cudaEventRecord(g->sh[li].ev1, g->sh[li].stream));
+    for (size_t li = 1; li < grp.size(); ++li)  // the leader records its end event in finish()
+      CK(cudaEventRecord(g->sh[grp[li]].ev1, g->sh[grp[li]].stream));
   }
   for (cudaEvent_t e : reset_ev) cudaEventDestroy(e);
   g->pending = k;
@@ -1245,6 +1268,13 @@ void fill_reference_stats(const sssp_graph* g, sssp_solve_stats* st) {
 int finish(sssp_graph* g, sssp_solve_stats* st) {
   const uint32_t k = g->pending;
   if (k == 0) return fail(SSSP_ERR_BAD_ARG, "nothing enqueued");
+  // end events of the launching streams (deferred by launch(): one record
+  // after the last queued launch instead of one between every two launches)
+  for (const auto& gr : device_groups(g)) {
+    Shard& s = g->sh[gr[0]];
+    CK(cudaSetDevice(s.device));
+    CK(cudaEventRecord(s.ev1, s.stream));
+  }
   double rounds = 0;
   uint64_t iters = 0, last = 0, mis = 0, classes = 0, rows = 0, nbars = 0, nbytes = 0;
   bool timeout = false, bailed = false;
@@ -1315,16 +1345,18 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     g->bucket = false;
   if (g->multiproc) g->exch_base = last + 1;
   if (g->bucket && g->sh[0].d_trace) {
-    std::vector<uint64_t> tr(64 + 2048);
+    std::vector<uint64_t> tr(64 + 4096);
     CK(cudaMemcpy(tr.data(), g->sh[0].d_trace, tr.size() * 8, cudaMemcpyDeviceToHost));
     // entries: phase code << 56 | %globaltimer (bucket_kernel.cuh stamp())
     static const char* names[] = {"start", "bar", "detld", "det", "enum", "pushld", "push",
-                                  "pullset", "pull", "pub0", "pub1", "wb", "row0", "owner"};
+                                  "pullset", "pull", "pub0", "pub1", "wb", "row0", "owner", "x14", "local1", "rsum", "scan"};
     const uint64_t tmask = (1ull << 56) - 1;
-    fprintf(stderr, "bucket trace (us since kernel start; phase:end):");
+    int khz = 0;
+    cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, g->sh[0].device);
+    fprintf(stderr, "bucket trace (us since kernel start at %d MHz; phase:end):", khz / 1000);
     for (int i = 1; i < 64 && tr[i]; ++i) {
       const uint32_t c = (uint32_t)(tr[i] >> 56);
-      fprintf(stderr, " %s:%.2f", c < 14 ? names[c] : "?", ((tr[i] & tmask) - (tr[0] & tmask)) * 1e-3);
+      fprintf(stderr, " %s:%.2f", c < 18 ? names[c] : "?", ((tr[i] & tmask) - (tr[0] & tmask)) * 1e3 / khz);
     }
     fprintf(stderr, "\n");
     // per-CTA span of the last pull step (start, end relative to kernel start)
@@ -1338,6 +1370,19 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     }
     if (nc) fprintf(stderr, "pull per CTA (%d): start %.2f..%.2f end %.2f..%.2f mean %.2f us\n", nc, smin,
                     smax, emin, emax, dsum / nc);
+    {  // every CTA's start / end (%globaltimer) relative to the earliest start
+      uint64_t s0t = ~0ull, s1t = 0, e0t = ~0ull, e1t = 0;
+      int m = 0;
+      for (int c = 0; c < 1024 && tr[64 + 2048 + 2 * c]; ++c, ++m) {
+        s0t = std::min(s0t, tr[64 + 2048 + 2 * c]);
+        s1t = std::max(s1t, tr[64 + 2048 + 2 * c]);
+        e0t = std::min(e0t, tr[64 + 2048 + 2 * c + 1]);
+        e1t = std::max(e1t, tr[64 + 2048 + 2 * c + 1]);
+      }
+      if (m)
+        fprintf(stderr, "CTA spans (%d): start 0..%.2f end %.2f..%.2f us (CTA 0 starts at %.2f)\n", m,
+                (s1t - s0t) * 1e-3, (e0t - s0t) * 1e-3, (e1t - s0t) * 1e-3, (tr[64 + 2048] - s0t) * 1e-3);
+    }
   }
   if (st) {
     st->transfer_in_s = g->transfer_in_s;

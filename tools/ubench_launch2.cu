@@ -1,0 +1,63 @@
+// ubench_launch2.cu -- per-launch cost of back-to-back cooperative launches in
+// the bucket kernel's shape (256 CTAs x 256 threads, 92 KB smem) as a function
+// of the kernel-parameter size and of an event record between launches.
+// Build: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o tools/ubench_launch2 tools/ubench_launch2.cu
+#include <cooperative_groups.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#define CK(x) do { cudaError_t e = (x); if (e != cudaSuccess) { printf("%s: %s\n", #x, cudaGetErrorString(e)); return 1; } } while (0)
+
+template <int W> struct Big { uint64_t w[W]; };
+
+template <int W>
+__global__ void __launch_bounds__(256, 2) k_empty(const Big<W> p) {
+  extern __shared__ uint32_t dyn[];
+  if (threadIdx.x == 0 && p.w[W - 1] == 12345) dyn[0] = 1;
+}
+__global__ void __launch_bounds__(256, 2) k_ptr(const uint64_t* p) {
+  extern __shared__ uint32_t dyn[];
+  if (threadIdx.x == 0 && p[0] == 12345) dyn[0] = 1;
+}
+
+template <int W>
+int run(cudaStream_t st, int ev_between, const char* name) {
+  Big<W> b{};
+  cudaEvent_t e0, e1, em;
+  CK(cudaEventCreate(&e0));
+  CK(cudaEventCreate(&e1));
+  CK(cudaEventCreate(&em));
+  const size_t smem = 92 * 1024;
+  CK(cudaFuncSetAttribute(k_empty<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+  const int K = 200;
+  float best = 1e9;
+  for (int rep = 0; rep < 5; ++rep) {
+    CK(cudaStreamSynchronize(st));
+    CK(cudaEventRecord(e0, st));
+    for (int i = 0; i < K; ++i) {
+      void* a1[] = {&b};
+      CK(cudaLaunchCooperativeKernel((void*)k_empty<W>, dim3(256), dim3(256), a1, smem, st));
+      if (ev_between) CK(cudaEventRecord(em, st));
+    }
+    CK(cudaEventRecord(e1, st));
+    CK(cudaEventSynchronize(e1));
+    float ms;
+    CK(cudaEventElapsedTime(&ms, e0, e1));
+    if (ms < best) best = ms;
+  }
+  printf("{\"bench\": \"launch2\", \"variant\": \"%s\", \"param_bytes\": %d, \"event_between\": %d, \"us_per_launch\": %.2f}\n",
+         name, (int)sizeof(Big<W>), ev_between, best * 1e3 / K);
+  return 0;
+}
+
+int main() {
+  cudaStream_t st;
+  CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (int ev = 0; ev < 2; ++ev) {
+    run<8>(st, ev, "coop empty");
+    run<48>(st, ev, "coop empty");
+    run<192>(st, ev, "coop empty");
+    run<512>(st, ev, "coop empty");
+  }
+  return 0;
+}
