@@ -29,6 +29,11 @@
 #include "host_narrow.h"
 
 using namespace sssp_b200;
+namespace sssp_b200 {  // kernels_bucket_u*.cu: variant 0 one shard, 1 slots, 2 sharded
+void* bucket_fn_u8(int variant);
+void* bucket_fn_u16(int variant);
+void* bucket_fn_u32(int variant);
+}  // namespace sssp_b200
 
 namespace {
 
@@ -189,7 +194,8 @@ struct Shard {
   uint64_t* peer[kMaxShards] = {};
   // bucket engine (bucket_kernel.cuh)
   void* d_adjT = nullptr;        // transpose in position order (nullptr: symmetric or absent)
-  uint4* d_rsum = nullptr;       // bucket, one shard: per-row class-1 summaries (row_summary_kernel)
+  uint4* d_rsum = nullptr;       // bucket, one shard: per-row class-1 summaries [n][2] (row_summary_kernel)
+  uint32_t* d_rlist = nullptr;   //   ... and the rows' class-1 id lists (row_list_kernel)
   const void* pull_src = nullptr;// d_adjT, or d_adj when the matrix is symmetric
   uint64_t* d_info2 = nullptr;   // bucket: [B][2] barriers used, watchdog
   uint64_t* d_ctab = nullptr;    // bucket: [B][ctab] matrix bytes loaded per CTA
@@ -669,12 +675,17 @@ int compute_max_batch(sssp_graph* g) {
   return SSSP_OK;
 }
 
-void* bucket_fn(uint32_t wbytes, bool multi = false) {
-  if (multi)
-    return wbytes == 1 ? (void*)bucket_kernel<uint8_t, true>
-           : wbytes == 2 ? (void*)bucket_kernel<uint16_t, true> : (void*)bucket_kernel<uint32_t, true>;
-  return wbytes == 1 ? (void*)bucket_kernel<uint8_t, false>
-         : wbytes == 2 ? (void*)bucket_kernel<uint16_t, false> : (void*)bucket_kernel<uint32_t, false>;
+uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* e = getenv(name);
+  return e && *e ? strtoull(e, nullptr, 10) : dflt;
+}
+
+// multi: several solves share the launch; one: a single shard (nshards == 1)
+void* bucket_fn(uint32_t wbytes, bool multi = false, bool one = true) {
+  (void)one;  // no one-shard instance (kernels_bucket_u8.cu)
+  const int v = multi ? 1 : 2;
+  return wbytes == 1 ? sssp_b200::bucket_fn_u8(v) : wbytes == 2 ? sssp_b200::bucket_fn_u16(v)
+                                                   : sssp_b200::bucket_fn_u32(v);
 }
 
 size_t bucket_smem(const sssp_graph* g, bool batch_tiles = false) {
@@ -701,7 +712,7 @@ int plan_bucket(sssp_graph* g) {
     return fail(SSSP_ERR_UNSUPPORTED, exact ? "bucket engine needs the cluster layout"
                                             : "bucket engine needs min weight >= 1");
   if (!(exact && shape)) return SSSP_OK;
-  void* fn = bucket_fn(g->wbytes);
+  void* fn = bucket_fn(g->wbytes, false, g->P == 1);
   uint32_t T = 128 / g->wbytes;
   if (const char* e = getenv("SSSP_BUCKET_TILE_BYTES"))  // tuning experiments: bytes of each row per CTA
     T = std::max<uint32_t>(32, (uint32_t)atoi(e) / g->wbytes);
@@ -718,6 +729,7 @@ int plan_bucket(sssp_graph* g) {
       CK(cudaSetDevice(s.device));
       CK(raise_smem(fn, smem));
       CK(raise_smem(bucket_fn(g->wbytes, true), smem));
+      CK(raise_smem(bucket_fn(g->wbytes, false, false), smem));
       uint32_t same = 0;
       for (const auto& t : g->sh) same += t.device == s.device ? 1 : 0;
       int per_sm = 0, sms = 0;
@@ -800,7 +812,7 @@ int prepare_bucket_impl(sssp_graph* g) {
     const uint64_t rs = s.row_stride;
     s.pull_src = nullptr;
     if (g->P == 1) {  // class-1 row summaries: one CTA per row, once per upload
-      if (!s.d_rsum && pool_alloc(s, (void**)&s.d_rsum, g->n * sizeof(uint4)) != SSSP_OK) return SSSP_ERR_OOM;
+      if (!s.d_rsum && pool_alloc(s, (void**)&s.d_rsum, g->n * 2 * sizeof(uint4)) != SSSP_OK) return SSSP_ERR_OOM;
       const uint32_t fb0 = (uint32_t)std::min<uint64_t>(1 + g->min_w, 0xFFFFFFFEull);
       const unsigned nb = (unsigned)g->n;
       if (g->wbytes == 1)
@@ -810,6 +822,34 @@ int prepare_bucket_impl(sssp_graph* g) {
       else
         row_summary_kernel<uint32_t><<<nb, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, fb0, s.d_rsum);
       CK(cudaGetLastError());
+      // class-1 id lists: rows whose class 1 fits one push pass, within a
+      // memory budget (a quarter of the matrix); the rest scan their row
+      std::vector<uint4> hs(2 * g->n);
+      CK(cudaMemcpyAsync(hs.data(), s.d_rsum, hs.size() * sizeof(uint4), cudaMemcpyDeviceToHost, s.stream));
+      CK(cudaStreamSynchronize(s.stream));
+      uint64_t total = 0;
+      const uint64_t budget = std::max<uint64_t>(1ull << 20, g->n * rs * g->wbytes / 4) / 4;
+      for (uint64_t u = 0; u < g->n; ++u) {
+        const uint4 r = hs[2 * u];
+        const bool listed = r.x != 0xFFFFFFFFu && r.y > 0 && r.y <= kIdCap && total + r.y <= budget;
+        hs[2 * u + 1] = make_uint4(listed ? (uint32_t)total : 0xFFFFFFFFu, 0, 0, 0);
+        if (listed) total += r.y;
+      }
+      CK(cudaMemcpyAsync(s.d_rsum, hs.data(), hs.size() * sizeof(uint4), cudaMemcpyHostToDevice, s.stream));
+      if (s.d_rlist) pool_free(s, s.d_rlist);
+      s.d_rlist = nullptr;
+      if (total && pool_alloc(s, (void**)&s.d_rlist, total * sizeof(uint32_t)) != SSSP_OK) return SSSP_ERR_OOM;
+      if (total) {
+        const uint32_t* rsw = reinterpret_cast<const uint32_t*>(s.d_rsum);
+        if (g->wbytes == 1)
+          row_list_kernel<uint8_t><<<nb, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, rsw, s.d_rlist);
+        else if (g->wbytes == 2)
+          row_list_kernel<uint16_t><<<nb, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, rsw, s.d_rlist);
+        else
+          row_list_kernel<uint32_t><<<nb, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, rsw, s.d_rlist);
+        CK(cudaGetLastError());
+      }
+      CK(cudaStreamSynchronize(s.stream));  // hs is freed on return
     }
     if (rs % 64) continue;
     const uint64_t mbytes = g->n * rs * g->wbytes;
@@ -928,7 +968,7 @@ void destroy_graph(sssp_graph* g) {
     else cudaFree(s.d_slots);
     for (void* p : {(void*)s.d_dist, (void*)s.d_pred, (void*)s.d_info, (void*)s.d_sources,
                     (void*)s.d_visit, (void*)s.d_round_ns, (void*)s.d_info2, s.d_adjT, (void*)s.d_ctab,
-                    (void*)s.d_rsum})
+                    (void*)s.d_rsum, (void*)s.d_rlist})
       pool_free(s, p);
     if (s.stream) cudaStreamSynchronize(s.stream);
     cudaFree(s.d_trace);
@@ -1013,10 +1053,6 @@ cudaError_t launch_kernel(sssp_graph* g, const std::vector<uint32_t>& grp, void*
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-uint64_t env_u64(const char* name, uint64_t dflt) {
-  const char* e = getenv(name);
-  return e && *e ? strtoull(e, nullptr, 10) : dflt;
-}
 
 // Enqueues one launch of k solves on every local shard.
 int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
@@ -1068,7 +1104,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
     return SSSP_OK;
   }
   if (g->bucket) {
-    void* fn = bucket_fn(g->wbytes);
+    void* fn = bucket_fn(g->wbytes, false, g->P == 1);
     const size_t smem = bucket_smem(g);
     for (auto& s : g->sh) {
       CK(cudaSetDevice(s.device));
@@ -1157,6 +1193,8 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         // exchange-free class 1 (one shard; A/B: SSSP_BUCKET_LOCAL1=0)
         static const bool k_local1 = env_u64("SSSP_BUCKET_LOCAL1", 1) != 0;
         bp.rsum = k_local1 && g->P == 1 ? reinterpret_cast<const uint32_t*>(s0.d_rsum) : nullptr;
+        static const bool k_lists = env_u64("SSSP_BUCKET_LISTS", 1) != 0;  // A/B: scan row s instead
+        bp.rlist = k_lists ? s0.d_rlist : nullptr;
         void* args[] = {&bp};
         const uint32_t grid = tiles * (ns > 1 ? ns : bp.nlocal);
         // local shards other than the first wait for the launch on the

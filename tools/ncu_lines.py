@@ -44,3 +44,22 @@ tot = sum(agg.values())
 print(f"total samples {tot}")
 for (f, l), s in agg.most_common(top):
     print(f"{f}:{l}  {s}  {100*s/tot:.1f}%  inst {ex[(f, l)]}")
+
+# stall-reason totals, and per-line breakdown for the top lines
+if len(sys.argv) > 5:
+    cols = [i for i, c in enumerate(hdr) if c.startswith("stall_") and "Not Issued" not in c]
+    tot_r = collections.Counter()
+    per_line = collections.defaultdict(collections.Counter)
+    for r in rows[2:]:
+        try:
+            a = int(r[ia], 16)
+        except Exception:
+            continue
+        key = omap.get(a - base, ("?", 0))
+        for i in cols:
+            v = int(r[i] or 0)
+            tot_r[hdr[i]] += v
+            per_line[key][hdr[i]] += v
+    print("stall totals:", ", ".join(f"{k[6:]} {v}" for k, v in tot_r.most_common(10)))
+    for (f, l), s in agg.most_common(int(sys.argv[5])):
+        print(f"{f}:{l}", ", ".join(f"{k[6:]} {v}" for k, v in per_line[(f, l)].most_common(4)))
