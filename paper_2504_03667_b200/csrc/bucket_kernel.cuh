@@ -103,6 +103,7 @@ struct BucketParams {
   uint64_t out_stride;
   uint32_t* done;       // [kBucketMaxSlots] per-slot done flags (nslots > 1)
   uint32_t dbg_reps;    // debug (SSSP_BUCKET_REPS): repeat the class-1 row scan
+  unsigned long long* spans;  // debug (SSSP_BUCKET_SPANS): [64][2] per launch: max ~start, max end
   const uint32_t* rsum; // [n][8] row summaries (row_summary_kernel; one shard only) or nullptr
   const uint32_t* rlist;  // class-1 id lists: row u's B_1 at rlist[rsum[u][4]] (~0u: none)
   uint32_t ctab_stride; // CTAs per slot in cta_bytes
@@ -216,6 +217,13 @@ __device__ __forceinline__ K warp_min_key(K k) {
 __device__ __forceinline__ uint64_t umin64(uint64_t a, uint64_t b) { return a < b ? a : b; }
 
 constexpr int kBucketThreads = 256;
+// Registers per thread: 2 CTAs x 256 threads per SM at <= 128.  (A full
+// register file costs ~2.3 us per back-to-back launch -- tools/ubench_launch2.cu,
+// 5.1 vs 2.8 us -- but capping this kernel at 120 or fewer registers spills and
+// loses more than that: config 2 50.6 -> 53.3 us, config 4 1.42 -> 1.47 ms.)
+#ifndef SSSP_BUCKET_MAXREG
+#define SSSP_BUCKET_MAXREG 128
+#endif
 
 // A/B variants measured and rejected: the bulk-copy push and
 // the 16-deep register push.  Compiled only with -DSSSP_BUCKET_AB=1 so the
@@ -250,7 +258,7 @@ constexpr uint32_t kIdCap = kBucketChunk / 2;           // ids of one push pass 
 // executes small (the instruction cache behind L0 is 32 KB; a miss is an L2
 // round trip).
 template <typename W, bool MULTI, bool ONE>
-__global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketParams p) {
+__global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams p) {
   namespace cg = cooperative_groups;
   using KT = BucketKey<W>;
   using K = typename KT::T;
@@ -1215,6 +1223,10 @@ __global__ void __launch_bounds__(kBucketThreads, 2) bucket_kernel(const BucketP
     }
   }
   stamp(11);
+  if (p.spans && tid == 0) {  // debug: launch span = (min CTA start, max CTA end), %globaltimer
+    atomicMax(&p.spans[(p.seq % 64) * 2], ~(unsigned long long)t_start);
+    atomicMax(&p.spans[(p.seq % 64) * 2 + 1], (unsigned long long)globaltimer());
+  }
   if (p.trace && tid == 0 && slot == 0 && me < 1024) {  // debug: every CTA's start / end
     p.trace[64 + 2048 + 2 * me] = t_start;
     p.trace[64 + 2048 + 2 * me + 1] = globaltimer();

@@ -200,6 +200,7 @@ struct Shard {
   uint64_t* d_info2 = nullptr;   // bucket: [B][2] barriers used, watchdog
   uint64_t* d_ctab = nullptr;    // bucket: [B][ctab] matrix bytes loaded per CTA
   uint64_t* d_trace = nullptr;   // debug (SSSP_BUCKET_TRACE)
+  unsigned long long* d_spans = nullptr;  // debug (SSSP_BUCKET_SPANS): [64][2] launch spans
   bool peer_ipc[kMaxShards] = {};
   bool own_stream = true;        // false: shares the stream of the device's first shard
   KernelFn fn = nullptr;
@@ -972,6 +973,7 @@ void destroy_graph(sssp_graph* g) {
       pool_free(s, p);
     if (s.stream) cudaStreamSynchronize(s.stream);
     cudaFree(s.d_trace);
+    cudaFree(s.d_spans);
     const uint64_t B = g->max_batch;
     pinned_put(s.h_sources, B * sizeof(uint32_t));
     pinned_put(s.h_info, B * 4 * sizeof(uint64_t));
@@ -1188,6 +1190,11 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
           bp.trace = s0.d_trace;
         }
         bp.seq = g->bseq + 1 + i;
+        if (getenv("SSSP_BUCKET_SPANS") && !s0.d_spans) {
+          CK(cudaMalloc(&s0.d_spans, 128 * 8));
+          CK(cudaMemset(s0.d_spans, 0, 128 * 8));
+        }
+        bp.spans = s0.d_spans;
         static const uint32_t k_reps = (uint32_t)std::max<uint64_t>(1, env_u64("SSSP_BUCKET_REPS", 1));
         bp.dbg_reps = k_reps;
         // exchange-free class 1 (one shard; A/B: SSSP_BUCKET_LOCAL1=0)
@@ -1304,7 +1311,7 @@ void fill_reference_stats(const sssp_graph* g, sssp_solve_stats* st) {
 }
 
 int finish(sssp_graph* g, sssp_solve_stats* st) {
-  const uint32_t k = g->pending;
+  const uint32_t k = g->pending, nqueued = g->queued;
   if (k == 0) return fail(SSSP_ERR_BAD_ARG, "nothing enqueued");
   // end events of the launching streams (deferred by launch(): one record
   // after the last queued launch instead of one between every two launches)
@@ -1382,6 +1389,26 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
   if (g->bucket && g->opt.engine == SSSP_ENGINE_AUTO && k > 0 && classes / k > g->n / 8)
     g->bucket = false;
   if (g->multiproc) g->exch_base = last + 1;
+  if (g->bucket && g->sh[0].d_spans && k == 1 && nqueued > 1) {  // debug: gaps between launches
+    std::vector<unsigned long long> sp(128);
+    CK(cudaMemcpy(sp.data(), g->sh[0].d_spans, 128 * 8, cudaMemcpyDeviceToHost));
+    double sum_span = 0, sum_gap = 0;
+    int ns = 0, ng = 0;
+    const uint64_t last = g->bseq, first = g->bseq + 1 - std::min<uint64_t>(nqueued, 64);
+    for (uint64_t q = first; q <= last; ++q) {
+      const unsigned long long st0 = ~sp[(q % 64) * 2], en = sp[(q % 64) * 2 + 1];
+      if (!sp[(q % 64) * 2] || !en) continue;
+      sum_span += (en - st0) * 1e-3;
+      ++ns;
+      if (q > first && sp[((q - 1) % 64) * 2 + 1]) {
+        sum_gap += (st0 - sp[((q - 1) % 64) * 2 + 1]) * 1e-3;
+        ++ng;
+      }
+    }
+    fprintf(stderr, "launch spans: %d launches, mean span %.2f us, mean gap %.2f us\n", ns, ns ? sum_span / ns : 0.0,
+            ng ? sum_gap / ng : 0.0);
+    CK(cudaMemset(g->sh[0].d_spans, 0, 128 * 8));
+  }
   if (g->bucket && g->sh[0].d_trace) {
     std::vector<uint64_t> tr(64 + 4096);
     CK(cudaMemcpy(tr.data(), g->sh[0].d_trace, tr.size() * 8, cudaMemcpyDeviceToHost));

@@ -15,6 +15,42 @@ __global__ void __launch_bounds__(256, 2) k_empty(const Big<W> p) {
   extern __shared__ uint32_t dyn[];
   if (threadIdx.x == 0 && p.w[W - 1] == 12345) dyn[0] = 1;
 }
+// the same empty launch, but the kernel holds 128 registers and ~40 KB of code
+// (a never-taken branch): does register / code footprint change launch cost?
+#define FAT_BODY \
+  extern __shared__ uint32_t dyn[]; \
+  if (p.w[0] == 777) { \
+    uint32_t r[100]; \
+    _Pragma("unroll") for (int i = 0; i < 100; ++i) r[i] = (uint32_t)p.w[i % 192] * (i + 3); \
+    _Pragma("unroll 1") for (int it = 0; it < (int)p.w[1]; ++it) { \
+      _Pragma("unroll") for (int i = 0; i < 100; ++i) r[i] = __byte_perm(r[i], r[(i + 7) % 100], 0x5140) + r[(i * 13) % 100]; \
+    } \
+    uint32_t acc = 0; \
+    _Pragma("unroll") for (int i = 0; i < 100; ++i) acc ^= r[i]; \
+    dyn[threadIdx.x] = acc; \
+  } \
+  if (threadIdx.x == 0 && p.w[191] == 12345) dyn[0] = 1;
+template <int MAXR>
+__global__ void __launch_bounds__(256, 1) __maxnreg__(MAXR) k_fatr(const Big<192> p) { FAT_BODY }
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fat(const Big<192> p) {
+  extern __shared__ uint32_t dyn[];
+  if (p.w[0] == 777) {
+    uint32_t r[100];
+#pragma unroll
+    for (int i = 0; i < 100; ++i) r[i] = (uint32_t)p.w[i % 192] * (i + 3);
+#pragma unroll 1
+    for (int it = 0; it < (int)p.w[1]; ++it) {
+#pragma unroll
+      for (int i = 0; i < 100; ++i) r[i] = __byte_perm(r[i], r[(i + 7) % 100], 0x5140) + r[(i * 13) % 100];
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 100; ++i) acc ^= r[i];
+    dyn[threadIdx.x] = acc;
+  }
+  if (threadIdx.x == 0 && p.w[191] == 12345) dyn[0] = 1;
+}
 __global__ void __launch_bounds__(256, 2) k_ptr(const uint64_t* p) {
   extern __shared__ uint32_t dyn[];
   if (threadIdx.x == 0 && p[0] == 12345) dyn[0] = 1;
@@ -53,6 +89,41 @@ int run(cudaStream_t st, int ev_between, const char* name) {
 int main() {
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  auto fat = [&](void* fn, const char* name, int grid = 256, int threads = 256) -> int {
+    Big<192> b{};
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
+    cudaFuncAttributes fa;
+    CK(cudaFuncGetAttributes(&fa, fn));
+    cudaEvent_t e0, e1;
+    CK(cudaEventCreate(&e0));
+    CK(cudaEventCreate(&e1));
+    float best = 1e9;
+    for (int rep = 0; rep < 5; ++rep) {
+      CK(cudaStreamSynchronize(st));
+      CK(cudaEventRecord(e0, st));
+      for (int i = 0; i < 200; ++i) {
+        void* a1[] = {&b};
+        CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), a1, 92 * 1024, st));
+      }
+      CK(cudaEventRecord(e1, st));
+      CK(cudaEventSynchronize(e1));
+      float ms;
+      CK(cudaEventElapsedTime(&ms, e0, e1));
+      if (ms < best) best = ms;
+    }
+    printf("{\"bench\": \"launch2\", \"variant\": \"%s\", \"regs\": %d, \"code_bytes\": %d, \"param_bytes\": 1536, \"grid\": %d, \"threads\": %d, \"us_per_launch\": %.2f}\n",
+           name, fa.numRegs, 0, grid, threads, best * 1e3 / 200);
+    return 0;
+  };
+  fat((void*)k_fat<2>, "coop fat code, 2 CTAs/SM regs");
+  fat((void*)k_fat<2>, "coop fat code, 1 CTA/SM", 148);
+  fat((void*)k_fatr<120>, "coop fat code, maxnreg 120");
+  fat((void*)k_fatr<112>, "coop fat code, maxnreg 112");
+  fat((void*)k_fatr<96>, "coop fat code, maxnreg 96");
+  fat((void*)k_fat<2>, "coop fat code, 128 CTAs", 128);
+  fat((void*)k_fat<2>, "coop fat code, 128 threads", 256, 128);
+  fat((void*)k_fat<4>, "coop fat code, <=64 regs");
+  fat((void*)k_fat<8>, "coop fat code, <=32 regs");
   for (int ev = 0; ev < 2; ++ev) {
     run<8>(st, ev, "coop empty");
     run<48>(st, ev, "coop empty");
