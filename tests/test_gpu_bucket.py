@@ -244,3 +244,26 @@ def test_auto_picks_scan_engine_on_the_first_call(gpu, oracle_c):
     gd = gpu.generate_dense(1000, 42)
     rd = gpu.dijkstra(gd, 0)
     assert rd.stats["engine"] == 3
+
+
+@pytest.mark.parametrize("wmax", [100, 3000, 70000])
+@pytest.mark.parametrize("n", [256, 1000, 4096])
+def test_bucket_symmetry_detection_single_element(gpu, oracle_c, n, wmax):
+    """The upload's symmetry check (symmetric_check_wide_kernel on 128 B row
+    segments, symmetric_check_kernel otherwise) decides whether pull steps may
+    read row v as column v: a symmetric matrix keeps no transpose, and ONE
+    asymmetric element anywhere -- including the first and last rows and
+    columns -- makes the upload build it (matrix_bytes doubles)."""
+    rng = np.random.default_rng(n + wmax)
+    adj = rand_graph(rng, n, 1, wmax, 0.3, False)
+    g = gpu.Graph(n, False, adj.copy())
+    info, _ = check(gpu, oracle_c, g, 0, engine="bucket")
+    base = info["matrix_bytes"]
+    assert base < 2 * n * n * info["weight_bytes"]  # symmetric: no transpose
+    for (u, v) in [(0, n - 1), (n - 1, 0), (n // 2, n // 3), (1, 0)]:
+        a2 = adj.copy()
+        a2[u, v] = INF if a2[u, v] != INF else np.uint64(wmax)
+        g2 = gpu.Graph(n, True, a2)
+        for s in (0, u, v):
+            info2, _ = check(gpu, oracle_c, g2, s, engine="bucket")
+        assert info2["matrix_bytes"] > base, (u, v)  # the transpose was built
