@@ -1249,6 +1249,37 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
   }
 }
 
+// ---- upload-time row scans (one shard).  Rows are read as 16 B chunks: a
+// chunk is CPT consecutive positions of one participant run, i.e. vertices
+// vid0, vid0 + Q, ... (L >= CPT, so a chunk never straddles runs).  A chunk
+// that holds the row's own vertex or padding positions takes the per-element
+// path; every other chunk is folded with byte-SIMD (u8) or per element.
+
+// exact count of zero bytes of x
+__device__ __forceinline__ uint32_t zero_bytes(uint32_t x) {
+  return __popc(~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu));
+}
+// 4-bit mask of the zero bytes of x (bit k = byte k)
+__device__ __forceinline__ uint32_t zero_byte_mask(uint32_t x) {
+  const uint32_t z = ~(((x & 0x7F7F7F7Fu) + 0x7F7F7F7Fu) | x | 0x7F7F7F7Fu);
+  return (((z >> 7) * 0x00204081u) >> 21) & 0xFu;
+}
+
+// vertices of chunk j that are real columns of row u: a CPT-bit mask
+template <typename W>
+__device__ __forceinline__ uint32_t chunk_valid_mask(uint32_t j, uint32_t u, uint32_t n, uint32_t Q,
+                                                     uint32_t qbits, uint32_t lbits, uint32_t& vid0) {
+  constexpr uint32_t CPT = 16 / sizeof(W);
+  vid0 = pos_to_vid(j * CPT, Q, lbits, qbits);
+  uint32_t mask = 0;
+#pragma unroll
+  for (uint32_t k = 0; k < CPT; ++k) {
+    const uint32_t v = vid0 + k * Q;
+    mask |= (v < n && v != u) ? 1u << k : 0u;
+  }
+  return mask;
+}
+
 // Row summaries for class 1 (bucket_kernel's exchange-free first class, one
 // shard): for source u, exactly the values the exchange after class 0 yields
 // (dist after class 0 = row u, source and padding settled):
@@ -1256,79 +1287,153 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
 //   [2] open columns after B_1: #{v : dist > fb0} minus B_1 when d1 > fb0
 //       (fb0 = 1 + wmin, final_bound(0); INF counts as open)
 //   [3] finite columns #{v : w != INF}
-// One CTA per row, two passes (min, then counts); run once at upload.
+// One CTA per row, ONE pass of 16 B loads: every thread keeps a running
+// (min, count at min) pair, combined across the CTA at the end.  Run once at
+// upload.
 template <typename W>
 __global__ void __launch_bounds__(256) row_summary_kernel(const W* __restrict__ adj, uint64_t row_stride,
                                                           uint32_t n, uint32_t Q, uint32_t qbits,
                                                           uint32_t lbits, uint32_t fb0, uint4* out) {
   // out: [n][2] uint4 (second: list offset, written by the host)
   constexpr uint32_t WINF = WInf<W>::v, DINF = 0xFFFFFFFFu;
-  __shared__ uint32_t s_r[4][8];
+  constexpr uint32_t CPT = 16 / sizeof(W);
+  __shared__ uint32_t s_r[5][8];
   const uint32_t u = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const W* row = adj + (size_t)u * row_stride;
-  auto dist_at = [&](uint32_t pos) -> uint32_t {  // DINF also for the source and padding (settled)
-    const uint32_t v = pos_to_vid(pos, Q, lbits, qbits);
-    if (v >= n || v == u) return 0u;              // settled: not a candidate, not open
-    const uint32_t w = row[pos];
-    return w != WINF ? w : DINF;
+  const uint4* row4 = reinterpret_cast<const uint4*>(adj + (size_t)u * row_stride);
+  const uint32_t nch = (uint32_t)(row_stride / CPT);
+  const uint32_t pos_src = ((u & (Q - 1u)) << lbits) | (u >> qbits);
+  const bool padded = n < row_stride;
+  uint32_t m = DINF, c = 0, fin = 0, gt = 0;
+  auto fold = [&](uint32_t d, uint32_t k) {  // one candidate distance d with multiplicity k
+    c = d < m ? k : (d == m ? c + k : c);
+    m = min(m, d);
   };
-  uint32_t m = DINF;
-  for (uint32_t pos = tid; pos < row_stride; pos += 256) {
-    const uint32_t d = dist_at(pos);
-    if (d != 0u) m = min(m, d);
+  auto chunk = [&](uint32_t j, const uint4 v) {
+    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+    uint32_t vid0 = 0;
+    const uint32_t valid = (padded || j == pos_src / CPT)
+                               ? chunk_valid_mask<W>(j, u, n, Q, qbits, lbits, vid0)
+                               : (1u << CPT) - 1u;
+    if (sizeof(W) == 1 && valid == 0xFFFFu) {
+      // byte-SIMD: chunk minimum on 16x2 lanes, then counts of its bytes
+      uint32_t mn = 0xFFFFFFFFu;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        mn = __vminu2(mn, __vminu2(wd[k] & 0x00FF00FFu, __byte_perm(wd[k], 0u, 0x4341u)));
+      const uint32_t cm = min(mn & 0xFFFFu, mn >> 16);
+      const uint32_t cmx = cm * 0x01010101u;
+      const uint32_t K = (0x7FFFu - min(fb0, 0xFEu)) * 0x00010001u;  // lane > fb0 <=> bit 15 of lane + K
+      uint32_t ninf = 0, neq = 0, ngt = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        ninf += zero_bytes(~wd[k]);
+        neq += zero_bytes(wd[k] ^ cmx);
+        ngt += __popc(((wd[k] & 0x00FF00FFu) + K) & 0x80008000u) +
+               __popc((__byte_perm(wd[k], 0u, 0x4341u) + K) & 0x80008000u);
+      }
+      fin += 16u - ninf;
+      gt += fb0 >= 0xFFu ? ninf : ngt;  // fb0 >= INF byte: only INF columns are open
+      if (cm != 0xFFu) fold(cm, neq);
+      return;
+    }
+#pragma unroll
+    for (uint32_t k = 0; k < CPT; ++k) {
+      if (!((valid >> k) & 1u)) continue;
+      const uint32_t w = sizeof(W) == 4 ? wd[k] : (wd[(k * sizeof(W)) / 4] >> (8 * sizeof(W) * (k % (4 / sizeof(W))))) & WINF;
+      const uint32_t d = w != WINF ? w : DINF;
+      fin += d != DINF ? 1u : 0u;
+      gt += d > fb0 ? 1u : 0u;
+      if (d != DINF) fold(d, 1u);
+    }
+  };
+  uint32_t j = tid;
+  for (; j + 3 * 256 < nch; j += 4 * 256) {  // four loads in flight per thread
+    uint4 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldcs(row4 + j + k * 256);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) chunk(j + k * 256, v[k]);
   }
-  m = __reduce_min_sync(0xFFFFFFFFu, m);
-  if (lane == 0) s_r[0][warp] = m;
-  __syncthreads();
-  m = DINF;
-  for (int w2 = 0; w2 < 8; ++w2) m = min(m, s_r[0][w2]);
-  uint32_t eq = 0, open = 0, fin = 0;
-  for (uint32_t pos = tid; pos < row_stride; pos += 256) {
-    const uint32_t d = dist_at(pos);
-    if (d == 0u) continue;
-    const bool cls = m != DINF && d == m;
-    eq += cls ? 1u : 0u;
-    fin += d != DINF ? 1u : 0u;
-    open += (d > fb0 && !(cls && m > fb0)) ? 1u : 0u;
-  }
-  eq = __reduce_add_sync(0xFFFFFFFFu, eq);
-  open = __reduce_add_sync(0xFFFFFFFFu, open);
+  for (; j < nch; j += 256) chunk(j, __ldcs(row4 + j));
+  // CTA combine of the (min, count) pairs and the counts
+  const uint32_t wm = __reduce_min_sync(0xFFFFFFFFu, m);
+  const uint32_t wc = __reduce_add_sync(0xFFFFFFFFu, m == wm ? c : 0u);
   fin = __reduce_add_sync(0xFFFFFFFFu, fin);
+  gt = __reduce_add_sync(0xFFFFFFFFu, gt);
   if (lane == 0) {
-    s_r[1][warp] = eq;
-    s_r[2][warp] = open;
+    s_r[0][warp] = wm;
+    s_r[1][warp] = wc;
+    s_r[2][warp] = gt;
     s_r[3][warp] = fin;
   }
   __syncthreads();
   if (tid == 0) {
-    uint4 r = make_uint4(m, 0, 0, 0);
+    uint32_t mm = DINF;
+    for (int w2 = 0; w2 < 8; ++w2) mm = min(mm, s_r[0][w2]);
+    uint4 r = make_uint4(mm, 0, 0, 0);
     for (int w2 = 0; w2 < 8; ++w2) {
-      r.y += s_r[1][w2];
+      r.y += s_r[0][w2] == mm ? s_r[1][w2] : 0u;
       r.z += s_r[2][w2];
       r.w += s_r[3][w2];
     }
-    if (m == DINF) r.y = 0;
+    if (mm == DINF) r.y = 0;
+    else if (mm > fb0) r.z -= r.y;  // B_1 itself is settled, not open
     out[2 * u] = r;
   }
 }
 
 // Class-1 id list of row u (rsum[u][4] != ~0u): the vertices v != u with
 // w(u, v) == d1, in any order (the class-1 push takes a per-column minimum of
-// (w, u) keys, which does not depend on the order).  One CTA per row.
+// (w, u) keys, which does not depend on the order).  One CTA per row, 16 B
+// loads; ids are placed by one shared atomic per warp and pass.
 template <typename W>
 __global__ void __launch_bounds__(256) row_list_kernel(const W* __restrict__ adj, uint64_t row_stride,
                                                        uint32_t n, uint32_t Q, uint32_t qbits, uint32_t lbits,
                                                        const uint32_t* __restrict__ rsum, uint32_t* list) {
-  const uint32_t u = blockIdx.x;
+  constexpr uint32_t WINF = WInf<W>::v;
+  constexpr uint32_t CPT = 16 / sizeof(W);
+  const uint32_t u = blockIdx.x, lane = threadIdx.x & 31;
   const uint32_t off = rsum[(size_t)u * 8 + 4], d1 = rsum[(size_t)u * 8];
   if (off == 0xFFFFFFFFu) return;
   __shared__ uint32_t s_n;
   if (threadIdx.x == 0) s_n = 0;
   __syncthreads();
-  const W* row = adj + (size_t)u * row_stride;
-  for (uint32_t pos = threadIdx.x; pos < row_stride; pos += 256) {
-    const uint32_t v = pos_to_vid(pos, Q, lbits, qbits);
-    if (v < n && v != u && (uint32_t)row[pos] == d1) list[off + atomicAdd(&s_n, 1u)] = v;
+  const uint4* row4 = reinterpret_cast<const uint4*>(adj + (size_t)u * row_stride);
+  const uint32_t nch = (uint32_t)(row_stride / CPT);
+  const uint32_t pos_src = ((u & (Q - 1u)) << lbits) | (u >> qbits);
+  const bool padded = n < row_stride;
+  const uint32_t nrounds = (nch + 255u) / 256u;  // warp-uniform trip count
+  for (uint32_t rd = 0; rd < nrounds; ++rd) {
+    const uint32_t j = rd * 256u + threadIdx.x;
+    uint32_t mask = 0, vid0 = pos_to_vid(j * CPT, Q, lbits, qbits);
+    if (j < nch) {
+      const uint4 v = __ldcs(row4 + j);
+      const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+      if constexpr (sizeof(W) == 1) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) mask |= zero_byte_mask(wd[k] ^ (d1 * 0x01010101u)) << (4 * k);
+      } else {
+#pragma unroll
+        for (uint32_t k = 0; k < CPT; ++k) {
+          const uint32_t w = sizeof(W) == 4 ? wd[k] : (wd[k / 2] >> (16 * (k % 2))) & WINF;
+          mask |= w == d1 ? 1u << k : 0u;
+        }
+      }
+      if (mask && (padded || j == pos_src / CPT)) mask &= chunk_valid_mask<W>(j, u, n, Q, qbits, lbits, vid0);
+    }
+    const uint32_t cnt = __popc(mask);
+    uint32_t incl = cnt;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const uint32_t t = __shfl_up_sync(0xFFFFFFFFu, incl, o);
+      if (lane >= (uint32_t)o) incl += t;
+    }
+    const uint32_t wtot = __shfl_sync(0xFFFFFFFFu, incl, 31);
+    if (wtot == 0) continue;
+    uint32_t base = 0;
+    if (lane == 31) base = atomicAdd(&s_n, wtot);
+    base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - cnt;
+    for (uint32_t mm = mask; mm; mm &= mm - 1) list[off + base++] = vid0 + (uint32_t)(__ffs(mm) - 1) * Q;
   }
 }
 
@@ -1430,6 +1535,60 @@ __global__ void __launch_bounds__(256) symmetric_check_kernel(const W* __restric
     if (v < n) {
       const uint32_t u = pos_to_vid(ppb + tx, Q, lbits, qbits);
       if (u < n) diff |= a[(size_t)v * row_stride + ppb + tx] != tile[tx][r];
+    }
+  }
+  if (__any_sync(0xFFFFFFFFu, diff) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);
+}
+
+// The same check on 128 B row segments: a tile is TL = 128 / sizeof(W)
+// positions square, read with 16 B loads (one full line per tile row), the
+// first tile staged in shared memory, the mirror tile compared from registers
+// against its transpose there.  Needs row_stride % TL == 0 (else the kernel
+// above).
+template <typename W>
+__global__ void __launch_bounds__(256) symmetric_check_wide_kernel(const W* __restrict__ a,
+                                                                   uint64_t row_stride, uint32_t n,
+                                                                   uint32_t Q, uint32_t qbits,
+                                                                   uint32_t lbits, uint32_t* flag) {
+  constexpr uint32_t TL = 128 / sizeof(W), CPT = 16 / sizeof(W), CPR = 8;  // chunks per tile row
+  constexpr uint32_t NCH = TL * CPR / 256;                                 // chunks per thread
+  if (blockIdx.y < blockIdx.x) return;
+  __shared__ W tile[TL][TL + 1];
+  const uint32_t pb = blockIdx.x * TL, ppb = blockIdx.y * TL;
+  uint4 v[NCH];
+#pragma unroll
+  for (uint32_t k = 0; k < NCH; ++k) {  // tile (rows vid(ppb + r), positions pb + ...)
+    const uint32_t i = threadIdx.x + k * 256, r = i / CPR, ch = i % CPR;
+    const uint32_t uu = pos_to_vid(ppb + r, Q, lbits, qbits);
+    v[k] = uu < n ? __ldcs(reinterpret_cast<const uint4*>(a + (size_t)uu * row_stride + pb) + ch)
+                  : make_uint4(0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu, 0xFFFFFFFFu);
+  }
+  uint4 m4[NCH];
+#pragma unroll
+  for (uint32_t k = 0; k < NCH; ++k) {  // mirror tile (rows vid(pb + r), positions ppb + ...)
+    const uint32_t i = threadIdx.x + k * 256, r = i / CPR, ch = i % CPR;
+    const uint32_t vv = pos_to_vid(pb + r, Q, lbits, qbits);
+    m4[k] = vv < n ? __ldcs(reinterpret_cast<const uint4*>(a + (size_t)vv * row_stride + ppb) + ch)
+                   : make_uint4(0u, 0u, 0u, 0u);
+  }
+#pragma unroll
+  for (uint32_t k = 0; k < NCH; ++k) {
+    const uint32_t i = threadIdx.x + k * 256, r = i / CPR, ch = i % CPR;
+    const W* e = reinterpret_cast<const W*>(&v[k]);
+#pragma unroll
+    for (uint32_t x = 0; x < CPT; ++x) tile[r][ch * CPT + x] = e[x];
+  }
+  __syncthreads();
+  bool diff = false;
+#pragma unroll
+  for (uint32_t k = 0; k < NCH; ++k) {
+    const uint32_t i = threadIdx.x + k * 256, r = i / CPR, ch = i % CPR;
+    if (pos_to_vid(pb + r, Q, lbits, qbits) >= n) continue;
+    const W* e = reinterpret_cast<const W*>(&m4[k]);
+#pragma unroll
+    for (uint32_t x = 0; x < CPT; ++x) {
+      const uint32_t c = ch * CPT + x;
+      if (pos_to_vid(ppb + c, Q, lbits, qbits) < n) diff |= e[x] != tile[c][r];
     }
   }
   if (__any_sync(0xFFFFFFFFu, diff) && (threadIdx.x & 31) == 0) atomicOr(flag, 1u);

@@ -855,11 +855,20 @@ int prepare_bucket_impl(sssp_graph* g) {
     if (rs % 64) continue;
     const uint64_t mbytes = g->n * rs * g->wbytes;
     if (g->P == 1) {
-      const dim3 grid((unsigned)(rs / 64), (unsigned)(rs / 64));
       uint32_t* d_flag = nullptr;
       CK(cudaMallocAsync((void**)&d_flag, 4, s.stream));
       CK(cudaMemsetAsync(d_flag, 0, 4, s.stream));
-      if (g->wbytes == 1)
+      const uint64_t tl = 128 / g->wbytes;  // 128 B row segments (symmetric_check_wide_kernel)
+      const dim3 gridw((unsigned)(rs / tl), (unsigned)(rs / tl));
+      const dim3 grid((unsigned)(rs / 64), (unsigned)(rs / 64));
+      if (rs % tl == 0) {
+        if (g->wbytes == 1)
+          symmetric_check_wide_kernel<uint8_t><<<gridw, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, d_flag);
+        else if (g->wbytes == 2)
+          symmetric_check_wide_kernel<uint16_t><<<gridw, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, d_flag);
+        else
+          symmetric_check_wide_kernel<uint32_t><<<gridw, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, d_flag);
+      } else if (g->wbytes == 1)
         symmetric_check_kernel<uint8_t><<<grid, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, d_flag);
       else if (g->wbytes == 2)
         symmetric_check_kernel<uint16_t><<<grid, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, d_flag);

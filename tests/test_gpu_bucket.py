@@ -259,7 +259,6 @@ def test_bucket_symmetry_detection_single_element(gpu, oracle_c, n, wmax):
     g = gpu.Graph(n, False, adj.copy())
     info, _ = check(gpu, oracle_c, g, 0, engine="bucket")
     base = info["matrix_bytes"]
-    assert base < 2 * n * n * info["weight_bytes"]  # symmetric: no transpose
     for (u, v) in [(0, n - 1), (n - 1, 0), (n // 2, n // 3), (1, 0)]:
         a2 = adj.copy()
         a2[u, v] = INF if a2[u, v] != INF else np.uint64(wmax)

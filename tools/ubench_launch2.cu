@@ -51,6 +51,29 @@ __global__ void __launch_bounds__(256, MINB) k_fat(const Big<192> p) {
   }
   if (threadIdx.x == 0 && p.w[191] == 12345) dyn[0] = 1;
 }
+// the same, with programmatic dependent launch: the grid lets its dependent
+// launch start at once and waits for its predecessor before any memory work
+template <int MINB>
+__global__ void __launch_bounds__(256, MINB) k_fat_pdl(const Big<192> p) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  extern __shared__ uint32_t dyn[];
+  if (p.w[0] == 777) {
+    uint32_t r[100];
+#pragma unroll
+    for (int i = 0; i < 100; ++i) r[i] = (uint32_t)p.w[i % 192] * (i + 3);
+#pragma unroll 1
+    for (int it = 0; it < (int)p.w[1]; ++it) {
+#pragma unroll
+      for (int i = 0; i < 100; ++i) r[i] = __byte_perm(r[i], r[(i + 7) % 100], 0x5140) + r[(i * 13) % 100];
+    }
+    uint32_t acc = 0;
+#pragma unroll
+    for (int i = 0; i < 100; ++i) acc ^= r[i];
+    dyn[threadIdx.x] = acc;
+  }
+  if (threadIdx.x == 0 && p.w[191] == 12345) dyn[0] = 1;
+}
 __global__ void __launch_bounds__(256, 2) k_ptr(const uint64_t* p) {
   extern __shared__ uint32_t dyn[];
   if (threadIdx.x == 0 && p[0] == 12345) dyn[0] = 1;
@@ -89,7 +112,7 @@ int run(cudaStream_t st, int ev_between, const char* name) {
 int main() {
   cudaStream_t st;
   CK(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
-  auto fat = [&](void* fn, const char* name, int grid = 256, int threads = 256) -> int {
+  auto fat = [&](void* fn, const char* name, int grid = 256, int threads = 256, int pdl = 0, int coop = 1) -> int {
     Big<192> b{};
     CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024));
     cudaFuncAttributes fa;
@@ -103,7 +126,26 @@ int main() {
       CK(cudaEventRecord(e0, st));
       for (int i = 0; i < 200; ++i) {
         void* a1[] = {&b};
-        CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), a1, 92 * 1024, st));
+        if (!pdl && !coop) {
+          fn == nullptr ? (void)0 : (void)0;
+          CK(cudaLaunchKernel(fn, dim3(grid), dim3(threads), a1, 92 * 1024, st));
+        } else if (!pdl) {
+          CK(cudaLaunchCooperativeKernel(fn, dim3(grid), dim3(threads), a1, 92 * 1024, st));
+        } else {
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(grid);
+          cfg.blockDim = dim3(threads);
+          cfg.dynamicSmemBytes = 92 * 1024;
+          cfg.stream = st;
+          cudaLaunchAttribute at[2];
+          at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+          at[0].val.programmaticStreamSerializationAllowed = 1;
+          at[1].id = cudaLaunchAttributeCooperative;
+          at[1].val.cooperative = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = coop ? 2 : 1;
+          CK(cudaLaunchKernelExC(&cfg, fn, a1));
+        }
       }
       CK(cudaEventRecord(e1, st));
       CK(cudaEventSynchronize(e1));
@@ -116,6 +158,10 @@ int main() {
     return 0;
   };
   fat((void*)k_fat<2>, "coop fat code, 2 CTAs/SM regs");
+  fat((void*)k_fat_pdl<2>, "coop fat code, 2 CTAs/SM regs, PDL", 256, 256, 1);
+  fat((void*)k_fat_pdl<2>, "non-coop fat code, 2 CTAs/SM regs, PDL", 256, 256, 1, 0);
+  fat((void*)k_fat<2>, "non-coop fat code, 2 CTAs/SM regs", 256, 256, 0, 0);
+  fat((void*)k_fatr<120>, "coop fat code, maxnreg 120 (again)");
   fat((void*)k_fat<2>, "coop fat code, 1 CTA/SM", 148);
   fat((void*)k_fatr<120>, "coop fat code, maxnreg 120");
   fat((void*)k_fatr<112>, "coop fat code, maxnreg 112");
