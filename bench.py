@@ -370,9 +370,13 @@ def main():
         ev_s = torch.cuda.Event(enable_timing=True)
         ev_e = torch.cuda.Event(enable_timing=True)
         ev_s.record(stream)
+        t_h0 = time.perf_counter()
         for i in range(steps):  # queued back to back in stream order
             dg.enqueue([srcs[i % len(srcs)]])
+        t_h1 = time.perf_counter()
         ev_e.record(stream)
+        if os.environ.get("SSSP_BENCH_DEBUG"):
+            print(f"time_engine: host enqueue {1e6 * (t_h1 - t_h0) / steps:.2f} us/solve", file=sys.stderr)
         st = dg.finish()
         kern = [st["rounds_s"]]
         torch.cuda.synchronize()

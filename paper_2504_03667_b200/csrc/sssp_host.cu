@@ -1215,8 +1215,24 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         const uint32_t grid = tiles * (ns > 1 ? ns : bp.nlocal);
         // local shards other than the first wait for the launch on the
         // group's stream (their own streams record the completion below)
-        CK(cudaLaunchCooperativeKernel(ns > 1 ? bucket_fn(g->wbytes, true) : fn, dim3(grid),
-                                       dim3(kBucketThreads), args, wide ? smem_b : smem, s0.stream));
+        // cooperative + programmatic stream serialisation: a solve queued
+        // behind another is launched while its predecessor drains (the kernel
+        // waits on griddepcontrol.wait before any memory access); A/B:
+        // SSSP_BUCKET_PDL=0
+        static const bool k_pdl = env_u64("SSSP_BUCKET_PDL", 1) != 0;
+        cudaLaunchConfig_t cfg{};
+        cudaLaunchAttribute la[2];
+        la[0].id = cudaLaunchAttributeCooperative;
+        la[0].val.cooperative = 1;
+        la[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        la[1].val.programmaticStreamSerializationAllowed = 1;
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kBucketThreads);
+        cfg.dynamicSmemBytes = wide ? smem_b : smem;
+        cfg.stream = s0.stream;
+        cfg.attrs = la;
+        cfg.numAttrs = k_pdl ? 2 : 1;
+        CK(cudaLaunchKernelExC(&cfg, ns > 1 ? bucket_fn(g->wbytes, true) : fn, args));
       }
       i += ns;
     }
@@ -2023,13 +2039,24 @@ int sssp_probe_skeleton(sssp_graph* g, uint32_t barriers, uint32_t launches,
   uint32_t* sink = nullptr;
   CK(pool_alloc(s, (void**)&sink, 64) == SSSP_OK ? cudaSuccess : cudaErrorMemoryAllocation);
   void* args[] = {(void*)&barriers, (void*)&sink};
-  for (int w = 0; w < 3; ++w)
-    CK(cudaLaunchCooperativeKernel((void*)bucket_skeleton_kernel, dim3(g->bG), dim3(kBucketThreads),
-                                   args, smem, s.stream));
+  // launched exactly as the solves are: cooperative + programmatic stream
+  // serialisation (SSSP_BUCKET_PDL)
+  static const bool k_pdl = env_u64("SSSP_BUCKET_PDL", 1) != 0;
+  cudaLaunchConfig_t cfg{};
+  cudaLaunchAttribute la[2];
+  la[0].id = cudaLaunchAttributeCooperative;
+  la[0].val.cooperative = 1;
+  la[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  la[1].val.programmaticStreamSerializationAllowed = 1;
+  cfg.gridDim = dim3(g->bG);
+  cfg.blockDim = dim3(kBucketThreads);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s.stream;
+  cfg.attrs = la;
+  cfg.numAttrs = k_pdl ? 2 : 1;
+  for (int w = 0; w < 3; ++w) CK(cudaLaunchKernelExC(&cfg, (void*)bucket_skeleton_kernel, args));
   CK(cudaEventRecord(s.ev0, s.stream));
-  for (uint32_t i = 0; i < launches; ++i)
-    CK(cudaLaunchCooperativeKernel((void*)bucket_skeleton_kernel, dim3(g->bG), dim3(kBucketThreads),
-                                   args, smem, s.stream));
+  for (uint32_t i = 0; i < launches; ++i) CK(cudaLaunchKernelExC(&cfg, (void*)bucket_skeleton_kernel, args));
   CK(cudaEventRecord(s.ev1, s.stream));
   CK(cudaEventSynchronize(s.ev1));
   float ms = 0;
