@@ -154,6 +154,10 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gsrc) {
   const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void cp_async4(void* smem_dst, const void* gsrc) {
+  const uint32_t sa = (uint32_t)__cvta_generic_to_shared(smem_dst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(sa), "l"(gsrc) : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_async_wait() {
@@ -489,6 +493,32 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
     return (uint32_t)umin64((uint64_t)dlast + 1u + p.wmin, (uint64_t)DINF - 1u);
   };
 
+  bool local1 = false;
+  uint32_t l_d1 = DINF, l_bc = 0, l_uc = 0, l_fin = 0;
+  const uint32_t l_off = p.rsum && p.rlist ? __ldg(p.rsum + (size_t)source * 8 + 4) : 0xFFFFFFFFu;
+  if (p.rsum) {
+    local1 = true;
+    for (uint32_t s2 = 0; s2 < (MULTI ? p.nslots : 1u); ++s2) {
+      const uint32_t src2 = MULTI ? p.slot_src[s2] : source;
+      const uint4 r4 = __ldg(reinterpret_cast<const uint4*>(p.rsum + (size_t)src2 * 8));
+      const bool pull1 = r4.x != DINF && r4.z != 0 && adjT != nullptr && r4.z < r4.y;
+      local1 = local1 && !pull1 && r4.y <= kIdCap;
+      if (src2 == source) {
+        l_d1 = r4.x;
+        l_bc = r4.y;
+        l_uc = r4.z;
+        l_fin = r4.w;
+      }
+    }
+  }
+  // The class-1 id list (an upload product, read-only) is copied into the id
+  // chunk asynchronously here, so its round trip overlaps the class-0 row
+  // slice below instead of following it; visible after the init barrier.
+  const bool pre_ids = local1 && l_d1 != DINF && l_uc != 0 && l_off != 0xFFFFFFFFu;
+  if (pre_ids) {
+    for (uint32_t i = tid; i < l_bc; i += kBucketThreads) cp_async4(&schunk[i], p.rlist + l_off + i);
+    cp_async_commit();
+  }
   // ---- init: dist = INF, pred = NONE, padding settled (serial.hpp:32-36),
   // then class 0 = {source} -- with every weight >= 1 the only vertex at
   // distance 0 -- settled and its row pushed by every CTA over its own tile
@@ -509,6 +539,7 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
     sdist[i] = src ? 0u : (w != WINF ? w : DINF);
     spred[i] = (!src && w != WINF) ? source : 0xFFFFFFFFu;
   }
+  if (pre_ids) cp_async_wait<0>();
   __syncthreads();
   // Buffer parity = parity of the barrier that follows the publish, counted
   // GLOBALLY (the count continues across launches): a fast shard's next
@@ -534,24 +565,6 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
   // PULL, or a class too large for one id pass, takes the exchange as before.
   // With several slots the choice is made for all of them together, so every
   // slot counts the same barriers.
-  bool local1 = false;
-  uint32_t l_d1 = DINF, l_bc = 0, l_uc = 0, l_fin = 0;
-  const uint32_t l_off = p.rsum && p.rlist ? __ldg(p.rsum + (size_t)source * 8 + 4) : 0xFFFFFFFFu;
-  if (p.rsum) {
-    local1 = true;
-    for (uint32_t s2 = 0; s2 < (MULTI ? p.nslots : 1u); ++s2) {
-      const uint32_t src2 = MULTI ? p.slot_src[s2] : source;
-      const uint4 r4 = __ldg(reinterpret_cast<const uint4*>(p.rsum + (size_t)src2 * 8));
-      const bool pull1 = r4.x != DINF && r4.z != 0 && adjT != nullptr && r4.z < r4.y;
-      local1 = local1 && !pull1 && r4.y <= kIdCap;
-      if (src2 == source) {
-        l_d1 = r4.x;
-        l_bc = r4.y;
-        l_uc = r4.z;
-        l_fin = r4.w;
-      }
-    }
-  }
   stamp(16);
   bool pre = false;  // the first loop step's class decisions are already made
   __shared__ uint32_t s_pre[4];  // its d, |B_d|, open count, relax (smem: not live across the loop)
@@ -564,8 +577,7 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
     } else {
       // B_1 = the positions of row `source` holding d1 (not the source, not padding):
       // the list built at upload (row_list_kernel), else a scan of the row
-      if (l_off != 0xFFFFFFFFu) {
-        for (uint32_t i = tid; i < l_bc; i += kBucketThreads) schunk[i] = __ldg(p.rlist + l_off + i);
+      if (pre_ids) {  // ids already in schunk (copied at kernel start)
         if (tid == 0) s_cnt[0] = l_bc;
       } else
       for (uint32_t rr = 0; rr < p.dbg_reps; ++rr) {
@@ -919,13 +931,26 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
         __syncthreads();
         stamp(5);
       }
+      // fold the row groups that share a warp with shuffles first (TPR < 32:
+      // 32/TPR groups per warp), so the cross-warp combine reads one partial
+      // per warp instead of one per row group
+      const uint32_t gpw = TPR < 32 ? 32u / TPR : 1u;  // row groups per warp
+      for (uint32_t o = TPR; o < 32; o <<= 1) {
 #pragma unroll
-      for (int j = 0; j < CPT; ++j) scomb[tid * CPT + j] = best[j];
+        for (int j = 0; j < CPT; ++j) {
+          const K x = __shfl_xor_sync(0xFFFFFFFFu, best[j], o);
+          best[j] = x < best[j] ? x : best[j];
+        }
+      }
+      if (gpw == 1 || lane < TPR) {
+#pragma unroll
+        for (int j = 0; j < CPT; ++j) scomb[((rg / gpw) * TPR + ct) * CPT + j] = best[j];
+      }
       __syncthreads();
       for (uint32_t col = tid; col < T; col += kBucketThreads) {
         const uint32_t cth = col / CPT, j = col % CPT;
         K k = KT::kNone;
-        for (uint32_t g2 = 0; g2 < RG; ++g2) {
+        for (uint32_t g2 = 0; g2 < RG / gpw; ++g2) {
           const K x = scomb[(g2 * TPR + cth) * CPT + j];
           k = x < k ? x : k;
         }
