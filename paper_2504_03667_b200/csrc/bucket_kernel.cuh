@@ -368,8 +368,10 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
   // trace entry = phase code << 56 | %globaltimer (CTA 0 of shard 0, debug)
   const bool tr_on = p.trace != nullptr && me == 0 && slot == 0 && tid == 0;
   auto stamp = [&](uint32_t code) {
-    if (tr_on && ntr < 64)
-      p.trace[ntr++] = ((uint64_t)code << 56) | ((uint64_t)clock64() & ((1ull << 56) - 1));
+    if (tr_on && ntr < 512) {  // stamps 64..511 live after the per-CTA spans (4096 words)
+      p.trace[ntr < 64 ? ntr : 4096 + ntr] = ((uint64_t)code << 56) | ((uint64_t)clock64() & ((1ull << 56) - 1));
+      ++ntr;
+    }
   };
 
   // One barrier over every CTA of every shard.  All shards in this launch:

@@ -1194,8 +1194,8 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.ctab_stride = g->ctab;
         bp.timeout_ns = g->opt.timeout_ms * 1000000ull;
         if (getenv("SSSP_BUCKET_TRACE") && s0.k == 0) {  // debug: per-barrier timestamps
-          if (!s0.d_trace) CK(cudaMalloc(&s0.d_trace, (64 + 4096) * 8));
-          CK(cudaMemsetAsync(s0.d_trace, 0, (64 + 4096) * 8, s0.stream));
+          if (!s0.d_trace) CK(cudaMalloc(&s0.d_trace, (512 + 4096) * 8));
+          CK(cudaMemsetAsync(s0.d_trace, 0, (512 + 4096) * 8, s0.stream));
           bp.trace = s0.d_trace;
         }
         bp.seq = g->bseq + 1 + i;
@@ -1435,7 +1435,7 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     CK(cudaMemset(g->sh[0].d_spans, 0, 128 * 8));
   }
   if (g->bucket && g->sh[0].d_trace) {
-    std::vector<uint64_t> tr(64 + 4096);
+    std::vector<uint64_t> tr(512 + 4096);
     CK(cudaMemcpy(tr.data(), g->sh[0].d_trace, tr.size() * 8, cudaMemcpyDeviceToHost));
     // entries: phase code << 56 | %globaltimer (bucket_kernel.cuh stamp())
     static const char* names[] = {"start", "bar", "detld", "det", "enum", "pushld", "push",
@@ -1444,9 +1444,10 @@ int finish(sssp_graph* g, sssp_solve_stats* st) {
     int khz = 0;
     cudaDeviceGetAttribute(&khz, cudaDevAttrClockRate, g->sh[0].device);
     fprintf(stderr, "bucket trace (us since kernel start at %d MHz; phase:end):", khz / 1000);
-    for (int i = 1; i < 64 && tr[i]; ++i) {
-      const uint32_t c = (uint32_t)(tr[i] >> 56);
-      fprintf(stderr, " %s:%.2f", c < 18 ? names[c] : "?", ((tr[i] & tmask) - (tr[0] & tmask)) * 1e3 / khz);
+    for (int i = 1; i < 512 && tr[i < 64 ? i : 4096 + i]; ++i) {
+      const uint64_t t = tr[i < 64 ? i : 4096 + i];
+      const uint32_t c = (uint32_t)(t >> 56);
+      fprintf(stderr, " %s:%.2f", c < 18 ? names[c] : "?", ((t & tmask) - (tr[0] & tmask)) * 1e3 / khz);
     }
     fprintf(stderr, "\n");
     // per-CTA span of the last pull step (start, end relative to kernel start)
