@@ -913,6 +913,26 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
                 vb[m] = __ldg(reinterpret_cast<const uint4*>(
                     reinterpret_cast<const uint8_t*>(adj + (size_t)ub[m] * p.row_stride + p0) + ct * 16));
             }
+            if constexpr (sizeof(W) == 1) {
+              // u8: rows in pairs through the 3-input minimum (VIMNMX3): one
+              // PRMT per key + half a min instead of a whole one; an odd last
+              // row of the class takes the 2-input minimum.
+#pragma unroll
+              for (int m = 0; m < DEPTH; m += 2) {
+                if (ub[m] == 0xFFFFFFFFu) break;
+                const uint32_t w0[4] = {vb[m].x, vb[m].y, vb[m].z, vb[m].w};
+                if (ub[m + 1] != 0xFFFFFFFFu) {
+                  const uint32_t w1[4] = {vb[m + 1].x, vb[m + 1].y, vb[m + 1].z, vb[m + 1].w};
+#pragma unroll
+                  for (int j = 0; j < CPT; ++j)
+                    best[j] = __vimin3_u32(best[j], chunk_key<W>(w0[j / 4], j, ub[m]),
+                                           chunk_key<W>(w1[j / 4], j, ub[m + 1]));
+                } else {
+#pragma unroll
+                  for (int j = 0; j < CPT; ++j) best[j] = min(best[j], chunk_key<W>(w0[j / 4], j, ub[m]));
+                }
+              }
+            } else {
 #pragma unroll
             for (int m = 0; m < DEPTH; ++m) {
               if (ub[m] == 0xFFFFFFFFu) break;
@@ -923,6 +943,7 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
                 const K k = chunk_key<W>(wd[(j * sizeof(W)) / 4], j, ub[m]);
                 best[j] = k < best[j] ? k : best[j];
               }
+            }
             }
           }
         };
