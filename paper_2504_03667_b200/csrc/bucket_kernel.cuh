@@ -107,6 +107,14 @@ struct BucketParams {
   const uint32_t* rsum; // [n][8] row summaries (row_summary_kernel; one shard only) or nullptr
   const uint32_t* rlist;  // class-1 id lists: row u's B_1 at rlist[rsum[u][4]] (~0u: none)
   uint32_t ctab_stride; // CTAs per slot in cta_bytes
+  // Sparse tile lists (tile_list_kernel; one shard, u8/u16, built at upload
+  // for sparse matrices): the finite entries of row u inside tile t are
+  // sp_ent[sp_off[u*G+t] .. sp_off[u*G+t+1]), each (position << 8*sizeof(W) | w);
+  // row-major, so row u's entries are sp_ent[sp_off[u*G] .. sp_off[(u+1)*G]).
+  // nullptr: the push streams the dense row slices.
+  const uint32_t* sp_off;
+  const uint32_t* sp_ent;
+  uint32_t sp_split;    // classes of >= this many rows push row-split (0: never)
 };
 
 __device__ __forceinline__ uint32_t pos_to_vid(uint32_t pos, uint32_t Q, uint32_t lbits,
@@ -261,7 +269,9 @@ constexpr uint32_t kIdCap = kBucketChunk / 2;           // ids of one push pass 
 // the shard / cross-launch bookkeeping folds away, which keeps the code a solve
 // executes small (the instruction cache behind L0 is 32 KB; a miss is an L2
 // round trip).
-template <typename W, bool MULTI, bool ONE>
+// SP: the sparse-list instance (p.sp_off set); the dense instances compile
+// without any of its code.
+template <typename W, bool MULTI, bool ONE, bool SP = false>
 __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams p) {
   namespace cg = cooperative_groups;
   using KT = BucketKey<W>;
@@ -391,7 +401,9 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __shared__ uint32_t s_fail;
+  __shared__ unsigned long long s_spb;  // sparse-list bytes this CTA loaded
   if (tid == 0) s_fail = 0;
+  if (SP && tid == 0) s_spb = 0;
   uint64_t nbar = 0;
   bool failed = false;
   const uint64_t t_start = globaltimer();
@@ -495,6 +507,15 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
     return (uint32_t)umin64((uint64_t)dlast + 1u + p.wmin, (uint64_t)DINF - 1u);
   };
 
+  // Row-split ("spread") sparse push for large classes: the class rows are
+  // divided over every warp of the slot, each row's whole entry list goes to
+  // the per-column global key array pkey by atomicMin, and every tile applies
+  // its columns after one extra barrier -- instead of every CTA walking every
+  // class row for its own tile.  Uniform: depends on the class size only.
+  // Only after a determination (every tile's publish reset its pkey words).
+  auto spread_ok = [&](uint32_t bc) -> bool {
+    return SP && sizeof(W) <= 2 && p.sp_off != nullptr && p.sp_split != 0 && bc >= p.sp_split;
+  };
   bool local1 = false;
   uint32_t l_d1 = DINF, l_bc = 0, l_uc = 0, l_fin = 0;
   const uint32_t l_off = p.rsum && p.rlist ? __ldg(p.rsum + (size_t)source * 8 + 4) : 0xFFFFFFFFu;
@@ -503,7 +524,7 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
     for (uint32_t s2 = 0; s2 < (MULTI ? p.nslots : 1u); ++s2) {
       const uint32_t src2 = MULTI ? p.slot_src[s2] : source;
       const uint4 r4 = __ldg(reinterpret_cast<const uint4*>(p.rsum + (size_t)src2 * 8));
-      const bool pull1 = r4.x != DINF && r4.z != 0 && adjT != nullptr && r4.z < r4.y;
+      const bool pull1 = r4.x != DINF && r4.z != 0 && adjT != nullptr && r4.z < r4.y && !(SP && p.sp_off != nullptr);
       local1 = local1 && !pull1 && r4.y <= kIdCap;
       if (src2 == source) {
         l_d1 = r4.x;
@@ -679,14 +700,14 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
   }
   while (!failed) {
     const uint32_t par = (uint32_t)((bar_base + nbar - 1) & 1ull);
-    bool relax = false, pull = false, owner = false;
+    bool relax = false, pull = false, owner = false, spread = false;
     uint32_t dk = 0, bcount = 0, ucount = 0;
     if (pre) {
       pre = false;
       dk = s_pre[0];
       bcount = s_pre[1];
       ucount = s_pre[2];
-      relax = s_pre[3] != 0;
+      relax = s_pre[3] != 0;  // class 1 never spreads: pkey is reset by the first publish
     } else if (!done) {
       // ---- the class: d = min over tiles, B_d = candidates of the tiles at d.
       // One memory round trip: every tile's (lmin, candidates, unsettled) and
@@ -774,7 +795,7 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
         } else {
           settled += bcount;
           relax = true;
-          pull = adjT != nullptr && ucount < bcount;
+          pull = adjT != nullptr && ucount < bcount && !(SP && p.sp_off != nullptr);  // sparse: push
           // small pulls run on the column owners: no partial minima to
           // combine, so no extra barrier (uniform: every CTA read the same counts)
           // (a column read in id order stops at its first w == wmin hit; a
@@ -789,16 +810,53 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
             for (uint32_t col = tid; col < T; col += kBucketThreads)
               open |= !((ssettled[col >> 5] >> (col & 31)) & 1u) && sdist[col] > lim;
             relax = __syncthreads_or(open);
+            spread = spread_ok(bcount);
           }
         }
       }
     }
     if (!MULTI && done) break;
 
-    if (relax && !pull) {
+    if ((relax || spread) && !pull) {
       // ---- PUSH: stream the rows of B_d (ascending ids), per-column min key
       pushed += bcount;
-      my_bytes += (uint64_t)bcount * T * sizeof(W);  // every class row's slice of this tile
+      // sparse lists: per class row its tile's (column, w) entries, folded
+      // into one per-column key array by shared atomicMin (the minimum of
+      // (w, u) keys does not depend on the order); dense: every class row's
+      // slice of this tile
+      const bool sparse = SP && sizeof(W) <= 2 && p.sp_off != nullptr;
+      constexpr uint32_t WB = sizeof(W) <= 2 ? 8u * (uint32_t)sizeof(W) : 16u, WM = (1u << WB) - 1u;
+      if (spread) {
+        // warp gw of the slot walks B_d bitmap words gw, gw + GW, ...: lane l
+        // loads the extent of the row at bit l, then the warp walks each set
+        // bit's entry list (no id enumeration; row loads overlap across bits)
+        const uint32_t GW = Gs * (kBucketThreads / 32), gw = bx * (kBucketThreads / 32) + warp;
+        uint32_t nb = 0;
+        for (uint32_t wi = gw; wi < words; wi += GW) {
+          const uint32_t bits = sbm[wi];
+          if (!bits) continue;  // warp-uniform
+          const bool mine = (bits >> lane) & 1u;
+          const uint32_t u = mine ? gvid(wi * 32 + lane) : 0u;
+          const uint32_t b = mine ? __ldg(p.sp_off + (size_t)u * G) : 0u;
+          const uint32_t e = mine ? __ldg(p.sp_off + (size_t)(u + 1) * G) : 0u;
+          nb += mine ? 8u + 4u * (e - b) : 0u;
+          for (uint32_t mm = bits; mm; mm &= mm - 1) {
+            const uint32_t j = (uint32_t)(__ffs(mm) - 1);
+            const uint32_t uj = __shfl_sync(0xFFFFFFFFu, u, j);
+            const uint32_t bj = __shfl_sync(0xFFFFFFFFu, b, j), ej = __shfl_sync(0xFFFFFFFFu, e, j);
+            for (uint32_t i = bj + lane; i < ej; i += 32) {
+              const uint32_t ent = __ldg(p.sp_ent + i);
+              smem_min(&pkey[ent >> WB], KT::make(ent & WM, uj));
+            }
+          }
+        }
+        nb = __reduce_add_sync(0xFFFFFFFFu, nb);
+        if (lane == 0) atomicAdd(&s_spb, (unsigned long long)nb);
+      } else if (sparse) {
+        for (uint32_t col = tid; col < T; col += kBucketThreads) scomb[col] = KT::kNone;
+      } else {
+        my_bytes += (uint64_t)bcount * T * sizeof(W);
+      }
       const uint32_t rg = tid / TPR, ct = tid - rg * TPR;  // row group, column thread
       K best[CPT];
 #pragma unroll
@@ -811,7 +869,7 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
       const uint32_t wpt = (bcount <= kIdCap && words <= WMAX * kBucketThreads)
                                ? (words + kBucketThreads - 1) / kBucketThreads
                                : 1u;
-      for (uint32_t wbase = 0; wbase < words; wbase += kBucketThreads * wpt) {
+      for (uint32_t wbase = spread ? words : 0u; wbase < words; wbase += kBucketThreads * wpt) {
         uint32_t tot;
         if (ids_n != 0xFFFFFFFFu) {  // class 1 from the row summary: ids already in schunk
           tot = ids_n;
@@ -947,7 +1005,36 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
             }
           }
         };
-        if (kBucketAB && p.push_depth16 && tot > 8 * RG && tot <= 16 * RG)
+        if (sparse) {
+          // 4 rows per thread in flight: the extents of all four, then the
+          // first entry of each (most rows hold 0 or 1 entries in a tile), then
+          // the rare remainder
+          const uint32_t* const off = p.sp_off + me;  // + u * G
+          uint32_t nb = 0;
+          for (uint32_t r0 = tid; r0 < tot; r0 += 4 * kBucketThreads) {
+            uint32_t ub[4], b[4], e[4], f[4];
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              const uint32_t r = r0 + m * kBucketThreads;
+              ub[m] = r < tot ? schunk[r] : 0u;
+              b[m] = r < tot ? __ldg(off + (size_t)ub[m] * G) : 0u;
+              e[m] = r < tot ? __ldg(off + (size_t)ub[m] * G + 1) : 0u;
+            }
+#pragma unroll
+            for (int m = 0; m < 4; ++m) f[m] = b[m] < e[m] ? __ldg(p.sp_ent + b[m]) : 0u;
+#pragma unroll
+            for (int m = 0; m < 4; ++m) {
+              nb += 8u + 4u * (e[m] - b[m]);
+              if (b[m] < e[m]) smem_min(&scomb[(f[m] >> WB) - p0], KT::make(f[m] & WM, ub[m]));
+              for (uint32_t i = b[m] + 1; i < e[m]; ++i) {
+                const uint32_t ent = __ldg(p.sp_ent + i);
+                smem_min(&scomb[(ent >> WB) - p0], KT::make(ent & WM, ub[m]));
+              }
+            }
+          }
+          nb = __reduce_add_sync(0xFFFFFFFFu, nb);
+          if (lane == 0) atomicAdd(&s_spb, (unsigned long long)nb);
+        } else if (kBucketAB && p.push_depth16 && tot > 8 * RG && tot <= 16 * RG)
           batches(std::integral_constant<int, 16>{});
         else
           batches(std::integral_constant<int, 8>{});
@@ -958,22 +1045,24 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
       // 32/TPR groups per warp), so the cross-warp combine reads one partial
       // per warp instead of one per row group
       const uint32_t gpw = TPR < 32 ? 32u / TPR : 1u;  // row groups per warp
-      for (uint32_t o = TPR; o < 32; o <<= 1) {
+      if (!spread) {
+      for (uint32_t o = TPR; !sparse && o < 32; o <<= 1) {
 #pragma unroll
         for (int j = 0; j < CPT; ++j) {
           const K x = __shfl_xor_sync(0xFFFFFFFFu, best[j], o);
           best[j] = x < best[j] ? x : best[j];
         }
       }
-      if (gpw == 1 || lane < TPR) {
+      if (!sparse && (gpw == 1 || lane < TPR)) {
 #pragma unroll
         for (int j = 0; j < CPT; ++j) scomb[((rg / gpw) * TPR + ct) * CPT + j] = best[j];
       }
       __syncthreads();
+      const uint32_t ngrp = sparse ? 1u : RG / gpw;  // sparse: group 0's slots = scomb[col]
       for (uint32_t col = tid; col < T; col += kBucketThreads) {
         const uint32_t cth = col / CPT, j = col % CPT;
         K k = KT::kNone;
-        for (uint32_t g2 = 0; g2 < RG / gpw; ++g2) {
+        for (uint32_t g2 = 0; g2 < ngrp; ++g2) {
           const K x = scomb[(g2 * TPR + cth) * CPT + j];
           k = x < k ? x : k;
         }
@@ -986,6 +1075,7 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
         }
       }
       __syncthreads();
+      }
       stamp(6);
     } else if (relax && owner) {
       // ---- PULL on the column owners (small pulls), in ascending vertex id.
@@ -1235,12 +1325,12 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
     }
     // the pull's extra barrier (every partial minimum is in pkey); with
     // several slots every step has it, so all CTAs count the same barriers
-    if ((pull && !owner) || MULTI) {
+    if ((pull && !owner) || spread || MULTI) {
       stamp(8);
       barrier();
       stamp(1);
     }
-    if (relax && pull && !owner) {
+    if ((relax && pull && !owner) || spread) {
       for (uint32_t col = tid; col < T; col += kBucketThreads) {
         if ((ssettled[col >> 5] >> (col & 31)) & 1u) continue;
         const K k = ld_cg(&pkey[p0 + col]);
@@ -1296,7 +1386,7 @@ __global__ void __maxnreg__(SSSP_BUCKET_MAXREG) bucket_kernel(const BucketParams
     S.info2[slot * 2] = nbar;
   }
   if (S.cta_bytes) {
-    if (tid == 0) S.cta_bytes[slot * p.ctab_stride + bx] = my_bytes;
+    if (tid == 0) S.cta_bytes[slot * p.ctab_stride + bx] = my_bytes + (SP ? s_spb : 0ull);
     if (bx == 0)  // entries of a wider tiling's CTAs (not in this launch) read as 0
       for (uint32_t i = Gs + tid; i < p.ctab_stride; i += kBucketThreads) S.cta_bytes[slot * p.ctab_stride + i] = 0;
   }
@@ -1490,6 +1580,63 @@ __global__ void __launch_bounds__(256) row_list_kernel(const W* __restrict__ adj
     if (lane == 31) base = atomicAdd(&s_n, wtot);
     base = __shfl_sync(0xFFFFFFFFu, base, 31) + incl - cnt;
     for (uint32_t mm = mask; mm; mm &= mm - 1) list[off + base++] = vid0 + (uint32_t)(__ffs(mm) - 1) * Q;
+  }
+}
+
+// Sparse tile lists (BucketParams::sp_off / sp_ent), two passes over the
+// matrix, one CTA per row u: COUNT writes cnt[u*G+t] = the finite real
+// entries of row u in tile t (positions [t*T, (t+1)*T)), cnt[n*G] = 0; an
+// exclusive scan turns cnt into offsets (lists in (row, tile) order); FILL places each entry (position - t*T) << 16 | w
+// (position << 8*sizeof(W) | w) behind its tile's cursor (order inside a list
+// is free: the push takes a per-column minimum).  Per-tile counters live in shared memory (G <= 1024).
+template <typename W, bool FILL>
+__global__ void __launch_bounds__(256) tile_list_kernel(const W* __restrict__ adj, uint64_t row_stride,
+                                                        uint32_t n, uint32_t Q, uint32_t qbits, uint32_t lbits,
+                                                        uint32_t T, uint32_t G, uint32_t* cnt_off,
+                                                        uint32_t* ent) {
+  constexpr uint32_t WINF = WInf<W>::v;
+  constexpr uint32_t CPT = 16 / sizeof(W);
+  const uint32_t u = blockIdx.x;
+  __shared__ uint32_t sc[1024];
+  for (uint32_t t = threadIdx.x; t < G; t += 256)
+    sc[t] = FILL ? cnt_off[(size_t)u * G + t] : 0u;
+  __syncthreads();
+  const uint4* row4 = reinterpret_cast<const uint4*>(adj + (size_t)u * row_stride);
+  const uint32_t nch = (uint32_t)(row_stride / CPT);
+  const uint32_t pos_src = ((u & (Q - 1u)) << lbits) | (u >> qbits);
+  const bool padded = n < row_stride;
+  for (uint32_t j = threadIdx.x; j < nch; j += 256) {
+    const uint4 v = __ldcs(row4 + j);
+    const uint32_t wd[4] = {v.x, v.y, v.z, v.w};
+    uint32_t mask = 0, vid0;
+    if constexpr (sizeof(W) == 1) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) mask |= (zero_byte_mask(~wd[k]) ^ 0xFu) << (4 * k);
+    } else {
+#pragma unroll
+      for (uint32_t k = 0; k < CPT; ++k) {
+        const uint32_t w = sizeof(W) == 4 ? wd[k] : (wd[k / 2] >> (16 * (k % 2))) & WINF;
+        mask |= w != WINF ? 1u << k : 0u;
+      }
+    }
+    if (mask && (padded || j == pos_src / CPT)) mask &= chunk_valid_mask<W>(j, u, n, Q, qbits, lbits, vid0);
+    if (!mask) continue;
+    const uint32_t t = (j * CPT) / T;
+    if (!FILL) {
+      atomicAdd(&sc[t], (uint32_t)__popc(mask));
+    } else {
+      for (uint32_t mm = mask; mm; mm &= mm - 1) {
+        const uint32_t k = (uint32_t)(__ffs(mm) - 1);
+        const uint32_t w = sizeof(W) == 1 ? (wd[k / 4] >> (8 * (k % 4))) & 0xFFu
+                                          : (wd[k / 2] >> (16 * (k % 2))) & 0xFFFFu;
+        ent[atomicAdd(&sc[t], 1u)] = ((j * CPT + k) << (8 * sizeof(W))) | w;
+      }
+    }
+  }
+  if (!FILL) {
+    __syncthreads();
+    for (uint32_t t = threadIdx.x; t < G; t += 256) cnt_off[(size_t)u * G + t] = sc[t];
+    if (u == 0 && threadIdx.x == 0) cnt_off[(size_t)n * G] = 0u;  // terminator: the end of the last list
   }
 }
 

@@ -9,6 +9,8 @@ namespace sssp_b200 {
 // slower than the general one at config 3 (26.4 vs 24.7 us: register spills at
 // the 128-register bound), so none is built.
 void* bucket_fn_u16(int variant) {
+  // variant 3: the sparse-list instance (one shard, single solves)
+  if (variant == 3) return (void*)bucket_kernel<uint16_t, false, false, true>;
   return variant == 1 ? (void*)bucket_kernel<uint16_t, true, true> : (void*)bucket_kernel<uint16_t, false, false>;
 }
 }  // namespace sssp_b200

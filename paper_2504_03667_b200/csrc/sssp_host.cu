@@ -6,6 +6,7 @@
 // persistent kernel (scan_kernel.cuh), and the launch / finish / D2H of a
 // solve.  No CPU solve path exists: every error surfaces as a status code.
 #include <cuda_runtime.h>
+#include <cub/device/device_scan.cuh>
 
 #include <algorithm>
 #include <atomic>
@@ -196,6 +197,9 @@ struct Shard {
   void* d_adjT = nullptr;        // transpose in position order (nullptr: symmetric or absent)
   uint4* d_rsum = nullptr;       // bucket, one shard: per-row class-1 summaries [n][2] (row_summary_kernel)
   uint32_t* d_rlist = nullptr;   //   ... and the rows' class-1 id lists (row_list_kernel)
+  uint32_t* d_spoff = nullptr;   // bucket, one shard, sparse matrix: tile-list offsets [n*G+1]
+  uint32_t* d_spent = nullptr;   //   ... and entries (tile_list_kernel); sp_T = their tile
+  uint32_t sp_T = 0;
   const void* pull_src = nullptr;// d_adjT, or d_adj when the matrix is symmetric
   uint64_t* d_info2 = nullptr;   // bucket: [B][2] barriers used, watchdog
   uint64_t* d_ctab = nullptr;    // bucket: [B][ctab] matrix bytes loaded per CTA
@@ -682,9 +686,9 @@ uint64_t env_u64(const char* name, uint64_t dflt) {
 }
 
 // multi: several solves share the launch; one: a single shard (nshards == 1)
-void* bucket_fn(uint32_t wbytes, bool multi = false, bool one = true) {
+void* bucket_fn(uint32_t wbytes, bool multi = false, bool one = true, bool sparse = false) {
   (void)one;  // no one-shard instance (kernels_bucket_u8.cu)
-  const int v = multi ? 1 : 2;
+  const int v = multi ? 1 : sparse && wbytes <= 2 ? 3 : 2;
   return wbytes == 1 ? sssp_b200::bucket_fn_u8(v) : wbytes == 2 ? sssp_b200::bucket_fn_u16(v)
                                                    : sssp_b200::bucket_fn_u32(v);
 }
@@ -731,6 +735,7 @@ int plan_bucket(sssp_graph* g) {
       CK(raise_smem(fn, smem));
       CK(raise_smem(bucket_fn(g->wbytes, true), smem));
       CK(raise_smem(bucket_fn(g->wbytes, false, false), smem));
+      if (g->wbytes <= 2) CK(raise_smem(bucket_fn(g->wbytes, false, false, true), smem));
       uint32_t same = 0;
       for (const auto& t : g->sh) same += t.device == s.device ? 1 : 0;
       int per_sm = 0, sms = 0;
@@ -850,8 +855,61 @@ int prepare_bucket_impl(sssp_graph* g) {
           row_list_kernel<uint32_t><<<nb, 256, 0, s.stream>>>((const uint32_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, rsw, s.d_rlist);
         CK(cudaGetLastError());
       }
+      // Sparse tile lists: when the finite entries take at most 1/8 of the
+      // matrix bytes as 4 B list entries, the push reads each class row's
+      // entries in its tile instead of the dense 128 B slice (config 4:
+      // 0.1 % density -> ~0.13 entries per row and tile).  u8/u16 only (the
+      // entry packs w in 16 bits).
+      uint64_t finite = 0;
+      for (uint64_t u = 0; u < g->n; ++u) finite += hs[2 * u].w;
+      pool_free(s, s.d_spoff);
+      pool_free(s, s.d_spent);
+      s.d_spoff = s.d_spent = nullptr;
+      s.sp_T = 0;
+      const uint32_t T = g->bT, G = g->bG;
+      static const bool k_sparse = env_u64("SSSP_BUCKET_SPARSE", 1) != 0;  // A/B: dense push
+      if (k_sparse && g->wbytes <= 2 && G <= 1024 && rs <= (g->wbytes == 1 ? (1ull << 24) : (1ull << 16)) &&
+          finite * 4 * 8 <= g->n * rs * g->wbytes &&
+          (uint64_t)G * g->n + 1 < (1ull << 31)) {
+        const double tl0 = now_s();
+        const size_t ncnt = (size_t)G * g->n + 1;
+        uint32_t* d_cnt = nullptr;
+        if (pool_alloc(s, (void**)&d_cnt, ncnt * 4) != SSSP_OK ||
+            pool_alloc(s, (void**)&s.d_spoff, ncnt * 4) != SSSP_OK)
+          return SSSP_ERR_OOM;
+        if (g->wbytes == 1)
+          tile_list_kernel<uint8_t, false><<<nb, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, T, G, d_cnt, nullptr);
+        else
+          tile_list_kernel<uint16_t, false><<<nb, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, T, G, d_cnt, nullptr);
+        CK(cudaGetLastError());
+        size_t tmp_bytes = 0;
+        CK(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, d_cnt, s.d_spoff, (int)ncnt, s.stream));
+        void* d_tmp = nullptr;
+        if (pool_alloc(s, &d_tmp, std::max<size_t>(tmp_bytes, 16)) != SSSP_OK) return SSSP_ERR_OOM;
+        CK(cub::DeviceScan::ExclusiveSum(d_tmp, tmp_bytes, d_cnt, s.d_spoff, (int)ncnt, s.stream));
+        pool_free(s, d_tmp);
+        pool_free(s, d_cnt);
+        // the list total = the terminator's offset (its count is 0)
+        uint32_t total_ent = 0;
+        CK(cudaMemcpyAsync(&total_ent, s.d_spoff + ncnt - 1, 4, cudaMemcpyDeviceToHost, s.stream));
+        CK(cudaStreamSynchronize(s.stream));
+        if (pool_alloc(s, (void**)&s.d_spent, std::max<uint64_t>(total_ent, 1) * 4) != SSSP_OK) return SSSP_ERR_OOM;
+        if (g->wbytes == 1)
+          tile_list_kernel<uint8_t, true><<<nb, 256, 0, s.stream>>>((const uint8_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, T, G, s.d_spoff, s.d_spent);
+        else
+          tile_list_kernel<uint16_t, true><<<nb, 256, 0, s.stream>>>((const uint16_t*)s.d_adj, rs, (uint32_t)g->n, Q, qb, lb, T, G, s.d_spoff, s.d_spent);
+        CK(cudaGetLastError());
+        s.sp_T = T;
+        if (getenv("SSSP_UPLOAD_TRACE")) {
+          CK(cudaStreamSynchronize(s.stream));
+          fprintf(stderr, "tile lists: %u entries, %u tiles, %.2f ms\n", total_ent, G, (now_s() - tl0) * 1e3);
+        }
+      }
       CK(cudaStreamSynchronize(s.stream));  // hs is freed on return
     }
+    // sparse tile lists: every step pushes, so no pull source (symmetry check,
+    // transpose) is needed
+    if (s.d_spoff) continue;
     if (rs % 64) continue;
     const uint64_t mbytes = g->n * rs * g->wbytes;
     if (g->P == 1) {
@@ -978,7 +1036,7 @@ void destroy_graph(sssp_graph* g) {
     else cudaFree(s.d_slots);
     for (void* p : {(void*)s.d_dist, (void*)s.d_pred, (void*)s.d_info, (void*)s.d_sources,
                     (void*)s.d_visit, (void*)s.d_round_ns, (void*)s.d_info2, s.d_adjT, (void*)s.d_ctab,
-                    (void*)s.d_rsum, (void*)s.d_rlist})
+                    (void*)s.d_rsum, (void*)s.d_rlist, (void*)s.d_spoff, (void*)s.d_spent})
       pool_free(s, p);
     if (s.stream) cudaStreamSynchronize(s.stream);
     cudaFree(s.d_trace);
@@ -1211,6 +1269,11 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         bp.rsum = k_local1 && g->P == 1 ? reinterpret_cast<const uint32_t*>(s0.d_rsum) : nullptr;
         static const bool k_lists = env_u64("SSSP_BUCKET_LISTS", 1) != 0;  // A/B: scan row s instead
         bp.rlist = k_lists ? s0.d_rlist : nullptr;
+        const bool sp = g->P == 1 && ns <= 1 && s0.d_spoff && s0.sp_T == bp.T;  // lists of this tiling (single solves)
+        bp.sp_off = sp ? s0.d_spoff : nullptr;
+        bp.sp_ent = sp ? s0.d_spent : nullptr;
+        static const uint32_t k_split = (uint32_t)env_u64("SSSP_SPLIT_ROWS", 512);  // 0: never row-split
+        bp.sp_split = k_split;
         void* args[] = {&bp};
         const uint32_t grid = tiles * (ns > 1 ? ns : bp.nlocal);
         // local shards other than the first wait for the launch on the
@@ -1232,7 +1295,7 @@ int launch(sssp_graph* g, const uint64_t* sources, uint32_t k) {
         cfg.stream = s0.stream;
         cfg.attrs = la;
         cfg.numAttrs = k_pdl ? 2 : 1;
-        CK(cudaLaunchKernelExC(&cfg, ns > 1 ? bucket_fn(g->wbytes, true) : fn, args));
+        CK(cudaLaunchKernelExC(&cfg, ns > 1 ? bucket_fn(g->wbytes, true) : sp ? bucket_fn(g->wbytes, false, false, true) : fn, args));
       }
       i += ns;
     }

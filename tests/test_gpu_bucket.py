@@ -266,3 +266,51 @@ def test_bucket_symmetry_detection_single_element(gpu, oracle_c, n, wmax):
         for s in (0, u, v):
             info2, _ = check(gpu, oracle_c, g2, s, engine="bucket")
         assert info2["matrix_bytes"] > base, (u, v)  # the transpose was built
+
+
+@pytest.mark.parametrize("wmax", [30, 254, 3000])
+@pytest.mark.parametrize("n,density,directed", [(1000, 0.01, True), (1500, 0.004, False),
+                                                (3000, 0.002, True), (4096, 0.02, False)])
+def test_bucket_sparse_tile_lists(gpu, oracle_c, n, density, directed, wmax):
+    # density <= 1/32 (u8) / 1/16 (u16): the upload builds per-tile finite-entry
+    # lists (tile_list_kernel) and every push reads them instead of the dense
+    # row slices, pulls off; n not a power of two pads the positions.  Kernel-
+    # counted bytes drop below a dense slice per pushed row.
+    rng = np.random.default_rng(n + wmax + directed)
+    adj = rand_graph(rng, n, 1, wmax, density, directed)
+    for u in range(10, 60):  # a light path: many classes, small B_d
+        adj[u, u + 1] = 1
+    g = gpu.Graph(n, directed, adj.ravel())
+    srcs = [0, 10, n - 1, 17]
+    want = [oracle_c.serial(g.adj, n, s) for s in srcs]
+    with gpu.DeviceGraph(g, engine="bucket") as dg:
+        info = dg.info()
+        assert info["engine"] == 3 and info["weight_bytes"] == (1 if wmax < 255 else 2)
+        for s, (d, p) in zip(srcs, want):
+            r = dg.solve(s)
+            assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p), (s, "single")
+            # dense: every pushed row costs its whole (padded) row across the
+            # tiles; sparse: 8 B of offsets per tile + 4 B per finite entry
+            wb = info["weight_bytes"]
+            if r.stats["rows_read"] > 8:
+                assert r.stats["bytes_read"] < r.stats["rows_read"] * n * wb / 2, r.stats
+        for s, r in zip(srcs, dg.solve_batch(srcs)):
+            d, p = want[srcs.index(s)]
+            assert np.array_equal(r.dist, d) and np.array_equal(r.pred, p), (s, "batch")
+
+
+@pytest.mark.parametrize("split", ["1", "0"])
+def test_bucket_sparse_row_split_push(split):
+    # the row-split push (classes of >= SSSP_SPLIT_ROWS rows: rows divided over
+    # every warp, global atomicMin into the per-column keys, one extra barrier)
+    # forced on every class after the first (1), and the tile-local sparse push
+    # only (0): the sparse-list cases above rerun in a fresh process (the
+    # switch is read once per process)
+    import os
+    import subprocess
+    import sys
+    env = dict(os.environ, SSSP_SPLIT_ROWS=split)
+    r = subprocess.run([sys.executable, "-m", "pytest", "-q", "-x", "-p", "no:cacheprovider",
+                        f"{__file__}::test_bucket_sparse_tile_lists", f"{__file__}::test_bucket_multislot_batches"],
+                       env=env, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stdout[-3000:] + r.stderr[-2000:]
