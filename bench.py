@@ -260,6 +260,13 @@ def run_configs(P, torch, peak, args) -> dict:
             rows /= k
             nb /= k
             info = dg.info()
+            lat = None
+            if ENG[st["engine"]] == "bucket":  # the sync skeleton bound (as the headline's)
+                nbar = int(st["barriers"])
+                t_skel = dg.probe_skeleton(nbar, 100) * 1e3
+                t_hbm = nb / (peak * 1e9) * 1e3
+                lat = {"bound": "sync+hbm", "barriers": nbar, "t_skeleton_ms": round(t_skel, 5),
+                       "t_hbm_ms": round(t_hbm, 5), "frac": round((t_skel + t_hbm) / ms, 4)}
         out[name] = {"workload": wl, "n": g.n, "engine": ENG[st["engine"]],
                      "ms_per_solve": round(ms, 4), "kernel_ms": round(st["rounds_s"] * 1e3, 4),
                      "sources": f"{k} rotating (0, 7919, ...)", "classes": st["classes"],
@@ -267,6 +274,7 @@ def run_configs(P, torch, peak, args) -> dict:
                      "weight_bytes": info["weight_bytes"],
                      "roofline": {"bound": "hbm", "achieved_gbs": round(nb / (ms * 1e-3) / 1e9, 1),
                                   "frac": round(nb / (ms * 1e-3) / 1e9 / peak, 4)},
+                     "latency_roofline": lat,
                      "parity": "source 0 dist and pred bit-identical to dijkstra_serial; all %d "
                                "timed sources validate_result-valid" % k,
                      "cpu_baseline": {"value": round(cpu_s * 1e3, 2), "unit": "ms", "cores": 1,
